@@ -1,0 +1,164 @@
+/*
+ * b200moe -- C ABI of the B200-native E8T2 MoE layer.
+ *
+ * The reference (`moefold`, a numpy package) has no FFI: its "plugin
+ * interface" is the Python module API of moefold/moe.py, moefold/upcycle.py and
+ * moefold/tensor.py:503 (importance_penalty).  Each entry point below replaces
+ * the numpy work behind one of those functions; the host package
+ * `paper_2412_09952_b200` binds them with ctypes and keeps
+ * the reference's Python signatures on top.
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless named *_host.  No function
+ *    allocates: outputs and workspaces are caller-owned (PyTorch's allocator).
+ *  - All work is enqueued on `stream`; nothing synchronises the host.
+ *  - bf16 tensors are passed as `void*` (row-major, contiguous).
+ *  - Return 0 on success or a negative B200MOE_ERR_* code; the message is in
+ *    b200moe_last_error() (thread-local).  Codes map to the reference's
+ *    exception classes (moefold/errors.py:12-25): SHAPE -> ShapeError,
+ *    CONFIG -> ConfigError, GATE -> GateError, CUDA -> RuntimeError.
+ *  - Device-side gate errors (a token row with no finite kept logit,
+ *    moefold/tensor.py:283-284) are reported through `err_flag` (int32, set to
+ *    1), checked by the host when routing statistics are materialised.
+ *
+ * Layouts
+ *  - x, dx:              [T, H] bf16
+ *  - W_g, W_noise:       [H, E] fp32 (reference [in, out] layout, moe.py:133,143)
+ *  - logits, gates, probs, noise_act, z, dg, dh, dn: [T, E] fp32
+ *  - slot_rank:          [T, E] int32: rank of token t among the kept tokens of
+ *                        expert e in token order, -1 if (t, e) is not kept
+ *  - expert segments:    permuted activations are grouped by expert; segment s
+ *                        starts at row seg_base[s], holds seg_count[s] rows and
+ *                        is zero-padded to a multiple of 128 rows.
+ *  - expert weights:     W1, W3 [E_local, F, H], W2 [E_local, H, F] bf16
+ *                        (= the reference's w1 [H,F], w2 [F,H], w3 [H,F] of each
+ *                        expert, transposed; upcycle_copy produces them).
+ */
+#ifndef B200MOE_H
+#define B200MOE_H
+
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B200MOE_OK 0
+#define B200MOE_ERR_SHAPE (-1)
+#define B200MOE_ERR_CONFIG (-2)
+#define B200MOE_ERR_GATE (-3)
+#define B200MOE_ERR_CUDA (-4)
+
+#define B200MOE_ROUTER_MIXTRAL 0 /* moe.py:171 gate_mixtral */
+#define B200MOE_ROUTER_ST 1      /* moe.py:176 gate_st */
+#define B200MOE_POLICY_POSITION 0
+#define B200MOE_POLICY_SCORE 1
+#define B200MOE_LAYOUT_COMPACT 0 /* seg_base = prefix of round_up(count,128) */
+#define B200MOE_LAYOUT_FIXED 1   /* seg_base[e] = e * seg_stride (EP send buffers) */
+
+const char* b200moe_last_error(void);
+int b200moe_version(void);
+
+/* Router forward (K1).  Replaces moe.py:136-149 router_logits + moe.py:152-186
+ * top_k_mask / gate_mixtral / gate_st + tensor.py:267-297 softmax.
+ * h = x.W_g (+ z * softplus(x.W_noise) when z != NULL).  gates are bit-exact
+ * with numpy float32 given the same logits.  probs (router_type st): full
+ * softmax s; may be NULL for mixtral.  noise_act = x.W_noise (needed by the
+ * backward; NULL when z == NULL).  workspace: >= 2*H*E floats. */
+int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E,
+                       int k, int router_type, float* logits, float* gates, float* probs, float* noise_act,
+                       float* workspace, int32_t* err_flag, cudaStream_t stream);
+
+/* Gating only, from given fp32 logits (moe.py:152-186).  Used to check the
+ * device gate arithmetic against the reference's own gates bit-for-bit.
+ * topk_mask (uint8 [T,E], nullable) = top_k_mask(logits, k) (moe.py:152). */
+int b200moe_gate_from_logits(const float* logits, int T, int E, int k, int router_type, float* gates, float* probs,
+                             uint8_t* topk_mask, int32_t* err_flag, cudaStream_t stream);
+
+/* Capacity + dispatch (K1b).  Replaces moe.py:189-240 (expert_capacity is
+ * evaluated by the host; capacity < 0 means dropless).  A slot exists iff
+ * gate > 0; `position` keeps the earliest tokens, `score` the largest gates
+ * (stable, position breaks ties).  Outputs slot_rank [T,E], counts [E]
+ * (= RoutingStats.assigned), seg_base [E], gate_mass [E] (sum of kept gates),
+ * importance [E] (sum of all gates, the aux-loss input), stats[2] =
+ * {dropped, total_slots} (int64).  workspace: >= 64 ints, zeroed once. */
+int b200moe_dispatch(const float* gates, int T, int E, int capacity, int policy, int layout, int seg_stride,
+                     int32_t* slot_rank, int32_t* counts, int32_t* seg_base, float* gate_mass, float* importance,
+                     int64_t* stats, int32_t* workspace, cudaStream_t stream);
+
+/* Token permute (K2): xp[seg_base[e] + slot_rank[t,e]] = x[t] for every kept
+ * (t,e); pad rows of each segment up to a multiple of 128 are zeroed.
+ * Replaces tensor.py:371-380 take_rows (moe.py:276). */
+int b200moe_permute(const void* x, const int32_t* slot_rank, const int32_t* seg_base, const int32_t* counts, int T,
+                    int H, int E, void* xp, cudaStream_t stream);
+
+/* Weighted combine (K5): y[t] = sum_{e kept, ascending} gates[t,e] * o[row(t,e)]
+ * (fp32 accumulation, bf16 out); fully dropped tokens get exactly 0.
+ * Replaces moe.py:278-282 (mul + put_rows + add). */
+int b200moe_combine(const void* o, const float* gates, const int32_t* slot_rank, const int32_t* seg_base, int T,
+                    int H, int E, void* y, cudaStream_t stream);
+
+/* Combine backward (K6): dout[row] = gates[t,e]*dy[t]; dg[t,e] = <dy[t], o[row]>
+ * (0 where not kept); pad rows of dout zeroed. */
+int b200moe_combine_bwd(const void* dy, const void* o, const float* gates, const int32_t* slot_rank,
+                        const int32_t* seg_base, const int32_t* counts, int T, int H, int E, void* dout, float* dg,
+                        cudaStream_t stream);
+
+/* Router backward (K10+K11): dg_total = dg + dgates_ext (strided, may be NULL);
+ * dh = softmax' (mixtral over the kept k, st over all E with the top-k mask);
+ * dx[t] = sum_{kept e ascending} dxp[row] + dh.W_g^T (+ dn.W_noise^T with
+ * dn = dh*z*sigmoid(noise_act)).  Writes dx (bf16), dh, dn (fp32, dn only with
+ * noise).  Replaces tensor.py:292-295, 224, 375-378 and moe.py's router matmuls. */
+int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
+                       const float* dgates_ext, int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates,
+                       const float* probs, const float* w_g, const float* w_noise, const float* z,
+                       const float* noise_act, int T, int H, int E, int router_type, void* dx, float* dh, float* dn,
+                       float* workspace, cudaStream_t stream);
+
+/* Router weight gradients: dW_g = x^T.dh, dW_noise = x^T.dn (fp32, [H,E]),
+ * deterministic (fixed-order partial sums).  workspace: >= ceil(T/128)*H*E*2
+ * floats. */
+int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T, int H, int E, float* dw_g,
+                         float* dw_noise, float* workspace, cudaStream_t stream);
+
+/* Importance (CV^2) penalty, tensor.py:503-521: loss = var(imp)/mean(imp)^2
+ * with imp = sum_t gates[t,:].  Forward writes imp [E] and loss [1] (fp32);
+ * backward writes dimp[e] = gscale[0] * dloss/dimp_e (the per-token gradient
+ * is dimp broadcast over tokens). */
+int b200moe_importance_fwd(const float* gates, int T, int E, float* imp, float* loss, int32_t* err_flag,
+                           cudaStream_t stream);
+int b200moe_importance_bwd(const float* imp, const float* gscale, int E, float* dimp, cudaStream_t stream);
+
+/* Grouped expert GEMMs on tcgen05/TMEM/TMA (see gemm.cu).  `rows` = rows of
+ * the permuted activation buffers.  H and F must be multiples of 256. */
+int b200moe_expert_fwd1(const void* xp, const void* w1, const void* w3, const int* seg_base, const int* seg_count,
+                        const int* seg_expert, int nseg, int rows, int H, int F, int E_local, void* a_out,
+                        void* b_out, void* h_out, cudaStream_t stream);
+int b200moe_expert_fwd2(const void* h, const void* w2, const int* seg_base, const int* seg_count,
+                        const int* seg_expert, int nseg, int rows, int H, int F, int E_local, void* o_out,
+                        cudaStream_t stream);
+int b200moe_expert_bwd2(const void* dout, const void* w2, const void* a_pre, const void* b_pre, const int* seg_base,
+                        const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
+                        void* da_out, void* db_out, cudaStream_t stream);
+int b200moe_expert_bwd1(const void* da, const void* db, const void* w1, const void* w3, const int* seg_base,
+                        const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
+                        void* dxp_out, cudaStream_t stream);
+int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const void* da, const void* db,
+                         const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows, int H,
+                         int F, int E_local, void* dw1, void* dw2, void* dw3, cudaStream_t stream);
+int b200moe_gemm_set_cta_group(int cta_group);
+int b200moe_gemm_set_max_ctas(int n);
+
+/* Online upcycling copy (K12), upcycle.py:104-112 / 216-224: replicate one
+ * dense FFN ([in,out] layout: w1,w3 [H,F], w2 [F,H]; fp32 or bf16 source,
+ * src_is_fp32) into E_local experts of the kernel layout (W1,W3 [E,F,H],
+ * W2 [E,H,F], bf16, round-to-nearest-even).  Bitwise equal to the reference
+ * copy after the dtype cast. */
+int b200moe_upcycle_copy(const void* w1, const void* w2, const void* w3, int src_is_fp32, int H, int F, int E_local,
+                         void* W1, void* W2, void* W3, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200MOE_H */

@@ -1,0 +1,109 @@
+"""ctypes binding of the b200moe C ABI (include/b200moe.h).
+
+The product path has exactly one implementation: the sm_100a CUDA library
+built in-tree at paper_2412_09952_b200/lib/libb200moe.so.  If it is missing or
+no CUDA device is present, every op raises -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigError, GateError, ShapeError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libb200moe.so")
+
+OK, ERR_SHAPE, ERR_CONFIG, ERR_GATE, ERR_CUDA = 0, -1, -2, -3, -4
+ROUTER = {"mixtral": 0, "st": 1}
+POLICY = {"position": 0, "score": 1}
+LAYOUT_COMPACT, LAYOUT_FIXED = 0, 1
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+
+# name -> argtypes (every function returns int status)
+SIGNATURES = {
+    "b200moe_router_fwd": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
+    "b200moe_gate_from_logits": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P],
+    "b200moe_dispatch": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "b200moe_permute": [_P, _P, _P, _P, _I, _I, _I, _P, _P],
+    "b200moe_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _P],
+    "b200moe_combine_bwd": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P],
+    "b200moe_router_bwd": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P,
+                           _P, _P],
+    "b200moe_router_wgrad": [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P],
+    "b200moe_importance_fwd": [_P, _I, _I, _P, _P, _P, _P],
+    "b200moe_importance_bwd": [_P, _P, _I, _P, _P],
+    "b200moe_expert_fwd1": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
+    "b200moe_expert_fwd2": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
+    "b200moe_expert_bwd2": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P],
+    "b200moe_expert_bwd1": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
+    "b200moe_expert_wgrad": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
+    "b200moe_gemm_set_cta_group": [_I],
+    "b200moe_gemm_set_max_ctas": [_I],
+    "b200moe_upcycle_copy": [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P],
+    "b200moe_version": [],
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeLibraryMissing(RuntimeError):
+    """The CUDA library was not built (run __graft_entry__.build())."""
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and type the native library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeLibraryMissing(
+                    f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, argtypes in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = argtypes
+                fn.restype = ctypes.c_int
+            lib.b200moe_last_error.argtypes = []
+            lib.b200moe_last_error.restype = ctypes.c_char_p
+            _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return sorted(list(SIGNATURES) + ["b200moe_last_error"])
+
+
+def call(name: str, *args) -> None:
+    """Invoke a C entry point and map its status onto the reference exceptions."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc == OK:
+        return
+    msg = (lib.b200moe_last_error() or b"").decode(errors="replace")
+    if rc == ERR_SHAPE:
+        raise ShapeError(msg)
+    if rc == ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == ERR_GATE:
+        raise GateError(msg)
+    raise RuntimeError(f"{name}: {msg} (status {rc})")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream

@@ -1,0 +1,96 @@
+// Shared helpers for the b200moe CUDA library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/b200moe.h"
+
+#ifndef __CUDACC__
+#error "compile with nvcc"
+#endif
+
+namespace b200moe {
+
+// Thread-local error message behind b200moe_last_error().
+void set_error(const char* fmt, ...);
+
+#define B200_CHECK_ARG(cond, code, ...)          \
+    do {                                         \
+        if (!(cond)) {                           \
+            ::b200moe::set_error(__VA_ARGS__);   \
+            return (code);                       \
+        }                                        \
+    } while (0)
+
+#define B200_CHECK_LAUNCH(what)                                                     \
+    do {                                                                            \
+        cudaError_t _e = cudaGetLastError();                                        \
+        if (_e != cudaSuccess) {                                                    \
+            ::b200moe::set_error("%s: %s", (what), cudaGetErrorString(_e));          \
+            return B200MOE_ERR_CUDA;                                                \
+        }                                                                           \
+    } while (0)
+
+constexpr int kNumSMs = 148;     // B200
+constexpr int kSegPad = 128;     // expert segments are zero-padded to this many rows
+
+__host__ __device__ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// 8 bf16 packed in a uint4 -> 8 floats
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 t = __bfloat1622float2(p[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+
+__device__ __forceinline__ uint4 pack8(const float* f) {
+    uint4 u;
+    __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return u;
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, const uint4& v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Segment table: where each expert segment of the permuted activation buffer
+// lives.  base[s] = first row, count[s] = valid rows (device), expert[s] =
+// local expert index.  Rows [count, round_up(count,128)) are zero-filled.
+struct SegTable {
+    const int* base;
+    const int* count;
+    const int* expert;
+    int nseg;
+};
+
+}  // namespace b200moe

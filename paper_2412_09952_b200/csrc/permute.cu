@@ -1,0 +1,239 @@
+// Token permute (K2), weighted combine (K5) and combine backward (K6).
+//
+// Reference: moefold/moe.py:272-282 (per expert: take_rows, ffn, multiply by the
+// gate column, put_rows, add in expert order) and the backward closures
+// tensor.py:185 (mul), :389 (put_rows), :375 (take_rows).  Every kernel is a
+// warp per token with 128-bit loads/stores; the per-token sum over its kept
+// experts runs in ascending expert order (deterministic, no atomics).
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace b200moe {
+
+constexpr int kPermThreads = 256;  // 8 warps
+constexpr int kVecPerLane = 8;     // uint4 per lane per pass (4 KB per warp pass)
+
+// Kept experts of token t (ascending) -> rows; returns the count.
+__device__ __forceinline__ int token_rows(const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
+                                          int t, int E, int* rows, int* experts) {
+    const int lane = threadIdx.x & 31;
+    int r = -1;
+    if (lane < E) {
+        const int rk = slot_rank[(size_t)t * E + lane];
+        if (rk >= 0) r = seg_base[lane] + rk;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, r >= 0);
+    int n = 0;
+    unsigned mm = m;
+    while (mm) {
+        const int e = __ffs(mm) - 1;
+        mm &= mm - 1;
+        rows[n] = __shfl_sync(0xffffffffu, r, e);
+        experts[n] = e;
+        ++n;
+    }
+    return n;
+}
+
+// Zero rows [seg_base[e]+counts[e], seg_base[e]+round_up(counts[e],128)) of buf.
+__device__ __forceinline__ void zero_pad_rows(__nv_bfloat16* buf, const int32_t* seg_base, const int32_t* counts,
+                                              int e, int H) {
+    const int c = counts[e];
+    const size_t r0 = (size_t)seg_base[e] + c;
+    const size_t r1 = (size_t)seg_base[e] + round_up(c, kSegPad);
+    const size_t nvec = (r1 - r0) * (H / 8);
+    uint4* p = reinterpret_cast<uint4*>(buf + r0 * H);
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    for (size_t i = threadIdx.x; i < nvec; i += blockDim.x) p[i] = zero;
+}
+
+__global__ void __launch_bounds__(kPermThreads)
+permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ slot_rank,
+               const int32_t* __restrict__ seg_base, const int32_t* __restrict__ counts, int T, int H, int E,
+               int token_blocks, __nv_bfloat16* __restrict__ xp) {
+    if ((int)blockIdx.x >= token_blocks) {
+        zero_pad_rows(xp, seg_base, counts, blockIdx.x - token_blocks, H);
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * (kPermThreads / 32) + (threadIdx.x >> 5);
+    if (t >= T) return;
+    int rows[32], experts[32];
+    const int n = token_rows(slot_rank, seg_base, t, E, rows, experts);
+    if (n == 0) return;
+    const int nvec = H / 8;
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * H);
+    for (int base = 0; base < nvec; base += 32 * kVecPerLane) {
+        uint4 v[kVecPerLane];
+#pragma unroll
+        for (int i = 0; i < kVecPerLane; ++i) {
+            const int j = base + i * 32 + lane;
+            if (j < nvec) v[i] = ld_nc_v4(src + j);
+        }
+        for (int r = 0; r < n; ++r) {
+            uint4* dst = reinterpret_cast<uint4*>(xp + (size_t)rows[r] * H);
+#pragma unroll
+            for (int i = 0; i < kVecPerLane; ++i) {
+                const int j = base + i * 32 + lane;
+                if (j < nvec) dst[j] = v[i];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPermThreads)
+combine_kernel(const __nv_bfloat16* __restrict__ o, const float* __restrict__ gates,
+               const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base, int T, int H, int E,
+               __nv_bfloat16* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * (kPermThreads / 32) + (threadIdx.x >> 5);
+    if (t >= T) return;
+    int rows[32], experts[32];
+    const int n = token_rows(slot_rank, seg_base, t, E, rows, experts);
+    float g[32];
+    for (int r = 0; r < n; ++r) g[r] = gates[(size_t)t * E + experts[r]];
+    const int nvec = H / 8;
+    uint4* dst = reinterpret_cast<uint4*>(y + (size_t)t * H);
+    for (int base = 0; base < nvec; base += 32 * 4) {
+        float acc[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+        for (int r = 0; r < n; ++r) {
+            const uint4* src = reinterpret_cast<const uint4*>(o + (size_t)rows[r] * H);
+            uint4 v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = base + i * 32 + lane;
+                if (j < nvec) v[i] = ld_nc_v4(src + j);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float f[8];
+                unpack8(v[i], f);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(g[r], f[c], acc[i][c]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = base + i * 32 + lane;
+            if (j < nvec) dst[j] = pack8(acc[i]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPermThreads)
+combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ o,
+                   const float* __restrict__ gates, const int32_t* __restrict__ slot_rank,
+                   const int32_t* __restrict__ seg_base, const int32_t* __restrict__ counts, int T, int H, int E,
+                   int token_blocks, __nv_bfloat16* __restrict__ dout, float* __restrict__ dg) {
+    if ((int)blockIdx.x >= token_blocks) {
+        zero_pad_rows(dout, seg_base, counts, blockIdx.x - token_blocks, H);
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * (kPermThreads / 32) + (threadIdx.x >> 5);
+    if (t >= T) return;
+    int rows[32], experts[32];
+    const int n = token_rows(slot_rank, seg_base, t, E, rows, experts);
+    float g[32], dot[32];
+    for (int r = 0; r < n; ++r) {
+        g[r] = gates[(size_t)t * E + experts[r]];
+        dot[r] = 0.f;
+    }
+    const int nvec = H / 8;
+    const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)t * H);
+    for (int base = 0; base < nvec; base += 32 * 4) {
+        float d[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = base + i * 32 + lane;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (j < nvec) v = ld_nc_v4(src + j);
+            unpack8(v, d[i]);
+        }
+        for (int r = 0; r < n; ++r) {
+            const uint4* os = reinterpret_cast<const uint4*>(o + (size_t)rows[r] * H);
+            uint4* ds = reinterpret_cast<uint4*>(dout + (size_t)rows[r] * H);
+            float s = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = base + i * 32 + lane;
+                if (j < nvec) {
+                    float f[8], w[8];
+                    unpack8(ld_nc_v4(os + j), f);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        s = fmaf(d[i][c], f[c], s);
+                        w[c] = g[r] * d[i][c];
+                    }
+                    ds[j] = pack8(w);
+                }
+            }
+            dot[r] += s;
+        }
+    }
+    float* dgt = dg + (size_t)t * E;
+    if (lane < E) dgt[lane] = 0.f;
+    __syncwarp();
+    for (int r = 0; r < n; ++r) {
+        const float s = warp_sum(dot[r]);
+        if (lane == 0) dgt[experts[r]] = s;
+    }
+}
+
+}  // namespace b200moe
+
+using namespace b200moe;
+
+namespace {
+int check_perm(int T, int H, int E) {
+    B200_CHECK_ARG(T >= 1, B200MOE_ERR_CONFIG, "tokens_per_batch must be >= 1, got %d", T);
+    B200_CHECK_ARG(E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "n_experts %d outside [1,32]", E);
+    B200_CHECK_ARG(H % 8 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 8, got %d", H);
+    return B200MOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int b200moe_permute(const void* x, const int32_t* slot_rank, const int32_t* seg_base, const int32_t* counts, int T,
+                    int H, int E, void* xp, cudaStream_t stream) {
+    int rc = check_perm(T, H, E);
+    if (rc) return rc;
+    const int tb = ceil_div(T, kPermThreads / 32);
+    permute_kernel<<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts, T, H,
+                                                         E, tb, (__nv_bfloat16*)xp);
+    B200_CHECK_LAUNCH("permute");
+    return B200MOE_OK;
+}
+
+int b200moe_combine(const void* o, const float* gates, const int32_t* slot_rank, const int32_t* seg_base, int T,
+                    int H, int E, void* y, cudaStream_t stream) {
+    int rc = check_perm(T, H, E);
+    if (rc) return rc;
+    const int tb = ceil_div(T, kPermThreads / 32);
+    combine_kernel<<<tb, kPermThreads, 0, stream>>>((const __nv_bfloat16*)o, gates, slot_rank, seg_base, T, H, E,
+                                                     (__nv_bfloat16*)y);
+    B200_CHECK_LAUNCH("combine");
+    return B200MOE_OK;
+}
+
+int b200moe_combine_bwd(const void* dy, const void* o, const float* gates, const int32_t* slot_rank,
+                        const int32_t* seg_base, const int32_t* counts, int T, int H, int E, void* dout, float* dg,
+                        cudaStream_t stream) {
+    int rc = check_perm(T, H, E);
+    if (rc) return rc;
+    const int tb = ceil_div(T, kPermThreads / 32);
+    combine_bwd_kernel<<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)o,
+                                                             gates, slot_rank, seg_base, counts, T, H, E, tb,
+                                                             (__nv_bfloat16*)dout, dg);
+    B200_CHECK_LAUNCH("combine_bwd");
+    return B200MOE_OK;
+}
+
+}  // extern "C"

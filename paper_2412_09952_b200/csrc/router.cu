@@ -1,0 +1,565 @@
+// Router forward (K1), gating from logits, and capacity dispatch (K1b).
+//
+// Reference semantics (moefold):
+//   logits   moe.py:136-149   h = x.W_g (+ z * softplus(x.W_noise))
+//   top-k    moe.py:152-162   stable argsort(-h): ties -> lowest index, NaN last
+//   mixtral  moe.py:171-173   softmax over the kept k (tensor.py:267-297)
+//   st       moe.py:176-186   softmax over all E, times the logit top-k mask
+//   dispatch moe.py:206-240   slot iff gate > 0; capacity by token position or
+//                             by gate (stable, position breaks ties)
+// The gate arithmetic reproduces numpy float32 bit-for-bit: numpy's exp
+// (npexp.cuh), its pairwise row sum, IEEE division, no FTZ.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "npexp.cuh"
+
+namespace b200moe {
+
+constexpr int kMaxE = 32;
+
+// ---------------------------------------------------------------- gating core
+// numpy's pairwise sum of a contiguous row of n <= 128 float32 values
+// (numpy/_core/src/umath/loops_utils.h.src pairwise_sum).
+template <int EP>
+__device__ __forceinline__ float np_rowsum(const float (&v)[EP], int n) {
+    if (n < 8) {
+        float r = 0.0f;
+#pragma unroll
+        for (int i = 0; i < EP; ++i)
+            if (i < n) r = __fadd_rn(r, v[i]);
+        return r;
+    }
+    float r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (j < EP) ? v[j % EP] : 0.f;
+    int full = n - (n % 8);
+#pragma unroll
+    for (int i = 8; i < EP; i += 8) {
+        if (i < full) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], v[(i + j) % EP]);
+        }
+    }
+    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int i = 8; i < EP; ++i)
+        if (i >= full && i < n) res = __fadd_rn(res, v[i]);
+    return res;
+}
+
+// Compute gates (and st probs) of one token from its E logits. Returns false on
+// a GateError row (no finite kept entry).
+template <int EP>
+__device__ __forceinline__ bool gate_row(const float (&h)[EP], int E, int k, int router_type, float (&g)[EP],
+                                         float (&p)[EP], uint32_t* sel_out = nullptr) {
+    // ---- stable top-k on -h (NaN last)
+    uint32_t sel = 0;
+    for (int it = 0; it < k; ++it) {
+        int best = -1;
+        float bv = 0.f;
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+            if (e >= E || (sel >> e) & 1u) continue;
+            const float v = h[e];
+            if (best < 0) { best = e; bv = v; continue; }
+            const bool bnan = (bv != bv), vnan = (v != v);
+            if ((bnan && !vnan) || (!bnan && !vnan && v > bv)) { best = e; bv = v; }
+        }
+        sel |= 1u << best;
+    }
+    if (sel_out) *sel_out = sel;
+    // ---- softmax keep mask
+    uint32_t keep = 0;
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+        if (e >= E) continue;
+        const bool fin = isfinite(h[e]);
+        if (router_type == B200MOE_ROUTER_MIXTRAL) { if (fin && ((sel >> e) & 1u)) keep |= 1u << e; }
+        else if (fin) keep |= 1u << e;
+    }
+    if (keep == 0) {
+#pragma unroll
+        for (int e = 0; e < EP; ++e) { g[e] = 0.f; p[e] = 0.f; }
+        return false;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < EP; ++e)
+        if ((keep >> e) & 1u) mx = fmaxf(mx, h[e]);
+    float ev[EP];
+#pragma unroll
+    for (int e = 0; e < EP; ++e) ev[e] = ((keep >> e) & 1u) ? np_expf(__fsub_rn(h[e], mx)) : 0.0f;
+    const float den = np_rowsum<EP>(ev, E);
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+        const float pe = __fdiv_rn(ev[e], den);
+        p[e] = pe;
+        if (router_type == B200MOE_ROUTER_MIXTRAL) g[e] = pe;
+        else g[e] = __fmul_rn(pe, ((sel >> e) & 1u) ? 1.0f : 0.0f);
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------- K1
+// Swizzle W [H, E] (fp32) into float4 blocks laid out so that lane-consecutive
+// h-blocks are address-consecutive: index ((j * (EP/4) + e4) * (H/4) + hb).
+template <int EP>
+__global__ void swizzle_w_kernel(const float* __restrict__ w, int H, int E, float4* __restrict__ out) {
+    const int n = (H / 4) * 4 * (EP / 4);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int hb = i % (H / 4);
+        const int rest = i / (H / 4);
+        const int e4 = rest % (EP / 4);
+        const int j = rest / (EP / 4);
+        const int h = hb * 4 + j;
+        float v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int e = e4 * 4 + c;
+            v[c] = (e < E) ? w[(size_t)h * E + e] : 0.f;
+        }
+        out[i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+// Butterfly reduce-scatter: 32 values per lane -> lane l holds the warp sum of value l.
+__device__ __forceinline__ float reduce_scatter32(float (&v)[32]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const float send = upper ? v[i] : v[i + n / 2];
+            const float keep = upper ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
+
+constexpr int kRouterThreads = 512;
+
+template <int EP, bool kNoise, bool kSmemW>
+__global__ void __launch_bounds__(kRouterThreads, 1)
+router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict__ wsw, const float4* __restrict__ wnsw,
+                  const float* __restrict__ z, int T, int H, int E, int k, int router_type,
+                  float* __restrict__ logits, float* __restrict__ gates, float* __restrict__ probs,
+                  float* __restrict__ noise_act, int32_t* __restrict__ err_flag) {
+    constexpr int TT = 32 / EP;  // tokens per warp iteration
+    extern __shared__ float4 smem_w[];
+    const int nvec = H * EP / 4;
+    const float4* W = wsw;
+    if constexpr (kSmemW) {
+        for (int i = threadIdx.x; i < nvec; i += blockDim.x) smem_w[i] = wsw[i];
+        __syncthreads();
+        W = smem_w;
+    }
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int HB = H / 4;
+
+    for (int t0 = (blockIdx.x * (blockDim.x >> 5) + warp) * TT; t0 < T; t0 += nwarps * TT) {
+        float acc[32], accn[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) { acc[i] = 0.f; accn[i] = 0.f; }
+        for (int hb = lane; hb < HB; hb += 32) {
+            float xv[TT][4];
+#pragma unroll
+            for (int tt = 0; tt < TT; ++tt) {
+                const int t = t0 + tt;
+                if (t < T) {
+                    const uint2 u = *reinterpret_cast<const uint2*>(x + (size_t)t * H + hb * 4);
+                    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+                    const float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
+                    xv[tt][0] = f0.x; xv[tt][1] = f0.y; xv[tt][2] = f1.x; xv[tt][3] = f1.y;
+                } else {
+                    xv[tt][0] = xv[tt][1] = xv[tt][2] = xv[tt][3] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+#pragma unroll
+                for (int e4 = 0; e4 < EP / 4; ++e4) {
+                    const float4 w = W[(j * (EP / 4) + e4) * HB + hb];
+#pragma unroll
+                    for (int tt = 0; tt < TT; ++tt) {
+                        float* a = acc + tt * EP + e4 * 4;
+                        a[0] = fmaf(xv[tt][j], w.x, a[0]);
+                        a[1] = fmaf(xv[tt][j], w.y, a[1]);
+                        a[2] = fmaf(xv[tt][j], w.z, a[2]);
+                        a[3] = fmaf(xv[tt][j], w.w, a[3]);
+                    }
+                    if constexpr (kNoise) {
+                        const float4 wn = __ldg(&wnsw[(j * (EP / 4) + e4) * HB + hb]);
+#pragma unroll
+                        for (int tt = 0; tt < TT; ++tt) {
+                            float* a = accn + tt * EP + e4 * 4;
+                            a[0] = fmaf(xv[tt][j], wn.x, a[0]);
+                            a[1] = fmaf(xv[tt][j], wn.y, a[1]);
+                            a[2] = fmaf(xv[tt][j], wn.z, a[2]);
+                            a[3] = fmaf(xv[tt][j], wn.w, a[3]);
+                        }
+                    }
+                }
+            }
+        }
+        // lane l now owns value l: token t0 + l / EP, expert l % EP
+        float hv = reduce_scatter32(acc);
+        const int tt_mine = lane / EP;
+        const int e_mine = lane % EP;
+        const int t_mine = t0 + tt_mine;
+        const bool live = (t_mine < T) && (e_mine < E);
+        if constexpr (kNoise) {
+            const float an = reduce_scatter32(accn);
+            if (live) {
+                const float zz = z[(size_t)t_mine * E + e_mine];
+                const float sp = fmaxf(an, 0.f) + log1pf(expf(-fabsf(an)));
+                hv = hv + zz * sp;
+                noise_act[(size_t)t_mine * E + e_mine] = an;
+            }
+        }
+        if (live) logits[(size_t)t_mine * E + e_mine] = hv;
+        // gather this token's row inside its EP-lane group
+        float row[EP];
+        const int gbase = tt_mine * EP;
+#pragma unroll
+        for (int e = 0; e < EP; ++e) row[e] = __shfl_sync(0xffffffffu, hv, gbase + e);
+        float g[EP], p[EP];
+        const bool ok = gate_row<EP>(row, E, k, router_type, g, p);
+        if (live) {
+            float ge = 0.f, pe = 0.f;
+#pragma unroll
+            for (int e = 0; e < EP; ++e)
+                if (e == e_mine) { ge = g[e]; pe = p[e]; }
+            gates[(size_t)t_mine * E + e_mine] = ge;
+            if (probs) probs[(size_t)t_mine * E + e_mine] = pe;
+            if (!ok && e_mine == 0) atomicExch(err_flag, 1);
+        }
+    }
+}
+
+template <int EP>
+__global__ void gate_from_logits_kernel(const float* __restrict__ logits, int T, int E, int k, int router_type,
+                                        float* __restrict__ gates, float* __restrict__ probs,
+                                        uint8_t* __restrict__ topk, int32_t* __restrict__ err_flag) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+        float h[EP], g[EP], p[EP];
+#pragma unroll
+        for (int e = 0; e < EP; ++e) h[e] = (e < E) ? logits[(size_t)t * E + e] : 0.f;
+        uint32_t sel = 0;
+        const bool ok = gate_row<EP>(h, E, k, router_type, g, p, &sel);
+        if (!ok) atomicExch(err_flag, 1);
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+            if (e < E) {
+                gates[(size_t)t * E + e] = g[e];
+                if (probs) probs[(size_t)t * E + e] = p[e];
+                if (topk) topk[(size_t)t * E + e] = (sel >> e) & 1u;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K1b dispatch
+constexpr int kDispThreads = 1024;
+constexpr int kDispItems = 8;  // tokens per thread per chunk
+
+// Block-wide exclusive scan of one int per thread; returns the prefix and
+// writes the block total to *total.
+__device__ __forceinline__ int block_excl_scan(int v, int* sm, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += n;
+    }
+    __syncthreads();
+    if (lane == 31) sm[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = (lane < nw) ? sm[lane] : 0;
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += n;
+        }
+        if (lane < nw) sm[lane] = wi - w;
+        if (lane == 31) sm[32] = wi;
+    }
+    __syncthreads();
+    const int res = sm[warp] + incl - v;
+    *total = sm[32];
+    return res;
+}
+
+__device__ __forceinline__ float block_sum_f(float v, float* sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sm[warp] = v;
+    __syncthreads();
+    float r = 0.f;
+    if (warp == 0) {
+        r = (lane < nw) ? sm[lane] : 0.f;
+        r = warp_sum(r);
+        if (lane == 0) sm[0] = r;
+    }
+    __syncthreads();
+    r = sm[0];
+    return r;
+}
+
+__global__ void __launch_bounds__(kDispThreads)
+dispatch_kernel(const float* __restrict__ gates, int T, int E, int capacity, int policy, int layout, int seg_stride,
+                int32_t* __restrict__ slot_rank, int32_t* __restrict__ counts, int32_t* __restrict__ seg_base,
+                float* __restrict__ gate_mass, float* __restrict__ importance, int64_t* __restrict__ stats,
+                int32_t* __restrict__ ws) {
+    __shared__ int sm_i[40];
+    __shared__ float sm_f[40];
+    __shared__ int hist[256];
+    __shared__ int sel_info[4];
+    __shared__ bool am_last;
+    const int e = blockIdx.x;
+    const int chunk = kDispThreads * kDispItems;
+    const bool dropless = capacity < 0;
+
+    // ---- pass 1: slot count and importance
+    int nslots = 0;
+    float imp = 0.f;
+    for (int base = 0; base < T; base += chunk) {
+        int c = 0;
+        for (int i = 0; i < kDispItems; ++i) {
+            const int t = base + threadIdx.x * kDispItems + i;
+            if (t < T) {
+                const float g = gates[(size_t)t * E + e];
+                imp += g;
+                c += (g > 0.f);
+            }
+        }
+        int tot;
+        block_excl_scan(c, sm_i, &tot);
+        nslots += tot;
+    }
+    imp = block_sum_f(imp, sm_f);
+
+    // ---- score policy with overflow: radix-select the capacity-th largest gate
+    const bool select = (policy == B200MOE_POLICY_SCORE) && !dropless && nslots > capacity;
+    uint32_t thr = 0;
+    int need_ties = 0;
+    if (select) {
+        uint32_t prefix = 0, pmask = 0;
+        int remaining = capacity;  // how many of the matching keys we still take
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+            for (int t = threadIdx.x; t < T; t += blockDim.x) {
+                const float g = gates[(size_t)t * E + e];
+                if (g > 0.f) {
+                    const uint32_t key = __float_as_uint(g);
+                    if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int cum = 0, d = 255;
+                for (; d > 0; --d) {
+                    if (cum + hist[d] >= remaining) break;
+                    cum += hist[d];
+                }
+                sel_info[0] = d;
+                sel_info[1] = remaining - cum;
+            }
+            __syncthreads();
+            prefix |= (uint32_t)sel_info[0] << shift;
+            pmask |= 255u << shift;
+            remaining = sel_info[1];
+            __syncthreads();
+        }
+        thr = prefix;
+        need_ties = remaining;  // number of keys == thr to keep (in token order)
+    }
+
+    // ---- pass 2: kept flags and ranks in token order
+    int kept_total = 0, ties_seen = 0, slots_seen = 0;
+    float mass = 0.f;
+    for (int base = 0; base < T; base += chunk) {
+        float gv[kDispItems];
+        int nslot = 0, ntie = 0;
+        for (int i = 0; i < kDispItems; ++i) {
+            const int t = base + threadIdx.x * kDispItems + i;
+            gv[i] = (t < T) ? gates[(size_t)t * E + e] : 0.f;
+            nslot += gv[i] > 0.f;
+            ntie += (select && gv[i] > 0.f && __float_as_uint(gv[i]) == thr);
+        }
+        int tot_slot, tot_tie;
+        const int slot_pre = block_excl_scan(nslot, sm_i, &tot_slot) + slots_seen;
+        int tie_pre = 0;
+        if (select) tie_pre = block_excl_scan(ntie, sm_i, &tot_tie) + ties_seen;
+        // decide kept per item
+        int kflags = 0, nk = 0;
+        int sp = slot_pre, tp = tie_pre;
+        for (int i = 0; i < kDispItems; ++i) {
+            bool kept = false;
+            if (gv[i] > 0.f) {
+                if (dropless) kept = true;
+                else if (!select) kept = sp < capacity;
+                else {
+                    const uint32_t key = __float_as_uint(gv[i]);
+                    if (key > thr) kept = true;
+                    else if (key == thr) { kept = tp < need_ties; ++tp; }
+                }
+                ++sp;
+            }
+            if (kept) { kflags |= 1 << i; ++nk; mass += gv[i]; }
+        }
+        int tot_kept;
+        int kp = block_excl_scan(nk, sm_i, &tot_kept) + kept_total;
+        for (int i = 0; i < kDispItems; ++i) {
+            const int t = base + threadIdx.x * kDispItems + i;
+            if (t < T) slot_rank[(size_t)t * E + e] = ((kflags >> i) & 1) ? kp++ : -1;
+        }
+        kept_total += tot_kept;
+        slots_seen += tot_slot;
+        if (select) ties_seen += tot_tie;
+    }
+    mass = block_sum_f(mass, sm_f);
+
+    if (threadIdx.x == 0) {
+        counts[e] = kept_total;
+        gate_mass[e] = mass;
+        importance[e] = imp;
+        ws[8 + e] = nslots;
+        __threadfence();
+        const int ticket = atomicAdd(&ws[0], 1);
+        am_last = (ticket == (int)gridDim.x - 1);
+    }
+    __syncthreads();
+    if (am_last && threadIdx.x == 0) {
+        __threadfence();
+        int acc = 0;
+        long long dropped = 0, total = 0;
+        for (int i = 0; i < E; ++i) {
+            const int c = ((volatile int32_t*)counts)[i];
+            const int s = ((volatile int32_t*)ws)[8 + i];
+            seg_base[i] = (layout == B200MOE_LAYOUT_FIXED) ? i * seg_stride : acc;
+            acc += round_up(c, kSegPad);
+            dropped += s - c;
+            total += s;
+        }
+        stats[0] = dropped;
+        stats[1] = total;
+        ws[0] = 0;  // reset the ticket for the next launch
+    }
+}
+
+}  // namespace b200moe
+
+using namespace b200moe;
+
+namespace {
+template <int EP>
+int router_fwd_impl(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E,
+                    int k, int router_type, float* logits, float* gates, float* probs, float* noise_act,
+                    float* workspace, int32_t* err_flag, cudaStream_t stream) {
+    float4* wsw = reinterpret_cast<float4*>(workspace);
+    float4* wnsw = reinterpret_cast<float4*>(workspace + (size_t)H * EP);
+    swizzle_w_kernel<EP><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
+    const bool noise = z != nullptr;
+    if (noise) swizzle_w_kernel<EP><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
+    const size_t wbytes = (size_t)H * EP * sizeof(float);
+    const bool smem_w = wbytes <= 160 * 1024;
+    constexpr int TT = 32 / EP;
+    const int warps_needed = ceil_div(T, TT);
+    int grid = ceil_div(warps_needed, kRouterThreads / 32);
+    if (grid > kNumSMs) grid = kNumSMs;
+    if (grid < 1) grid = 1;
+#define LAUNCH(NZ, SM)                                                                                        \
+    do {                                                                                                      \
+        auto kern = router_fwd_kernel<EP, NZ, SM>;                                                            \
+        const size_t sh = SM ? wbytes : 0;                                                                    \
+        if (SM) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);             \
+        kern<<<grid, kRouterThreads, sh, stream>>>((const __nv_bfloat16*)x, wsw, wnsw, z, T, H, E, k,         \
+                                                   router_type, logits, gates, probs, noise_act, err_flag);   \
+    } while (0)
+    if (noise) {
+        if (smem_w) LAUNCH(true, true); else LAUNCH(true, false);
+    } else {
+        if (smem_w) LAUNCH(false, true); else LAUNCH(false, false);
+    }
+#undef LAUNCH
+    B200_CHECK_LAUNCH("router_fwd");
+    return B200MOE_OK;
+}
+
+template <int EP>
+int gate_impl(const float* logits, int T, int E, int k, int router_type, float* gates, float* probs,
+              uint8_t* topk, int32_t* err_flag, cudaStream_t stream) {
+    int grid = ceil_div(T, 256);
+    if (grid > 4 * kNumSMs) grid = 4 * kNumSMs;
+    if (grid < 1) grid = 1;
+    gate_from_logits_kernel<EP><<<grid, 256, 0, stream>>>(logits, T, E, k, router_type, gates, probs, topk,
+                                                           err_flag);
+    B200_CHECK_LAUNCH("gate_from_logits");
+    return B200MOE_OK;
+}
+
+int check_router_args(int T, int H, int E, int k, int router_type) {
+    B200_CHECK_ARG(T >= 1, B200MOE_ERR_CONFIG, "tokens_per_batch must be >= 1, got %d", T);
+    B200_CHECK_ARG(E >= 1 && E <= kMaxE, B200MOE_ERR_CONFIG, "n_experts must be in [1, %d], got %d", kMaxE, E);
+    B200_CHECK_ARG(k >= 1 && k <= E, B200MOE_ERR_CONFIG, "top-k out of range: k=%d, n=%d", k, E);
+    B200_CHECK_ARG(router_type == B200MOE_ROUTER_MIXTRAL || router_type == B200MOE_ROUTER_ST, B200MOE_ERR_CONFIG,
+                   "router_type %d", router_type);
+    B200_CHECK_ARG(H >= 4 && H % 4 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 4, got %d", H);
+    return B200MOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E,
+                       int k, int router_type, float* logits, float* gates, float* probs, float* noise_act,
+                       float* workspace, int32_t* err_flag, cudaStream_t stream) {
+    int rc = check_router_args(T, H, E, k, router_type);
+    if (rc) return rc;
+    B200_CHECK_ARG(z == nullptr || (w_noise != nullptr && noise_act != nullptr), B200MOE_ERR_CONFIG,
+                   "noise needs w_noise and noise_act");
+    if (E <= 4) return router_fwd_impl<4>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs, noise_act, workspace, err_flag, stream);
+    if (E <= 8) return router_fwd_impl<8>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs, noise_act, workspace, err_flag, stream);
+    if (E <= 16) return router_fwd_impl<16>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs, noise_act, workspace, err_flag, stream);
+    return router_fwd_impl<32>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs, noise_act, workspace, err_flag, stream);
+}
+
+int b200moe_gate_from_logits(const float* logits, int T, int E, int k, int router_type, float* gates, float* probs,
+                             uint8_t* topk_mask, int32_t* err_flag, cudaStream_t stream) {
+    int rc = check_router_args(T, 4, E, k, router_type);
+    if (rc) return rc;
+    if (E <= 4) return gate_impl<4>(logits, T, E, k, router_type, gates, probs, topk_mask, err_flag, stream);
+    if (E <= 8) return gate_impl<8>(logits, T, E, k, router_type, gates, probs, topk_mask, err_flag, stream);
+    if (E <= 16) return gate_impl<16>(logits, T, E, k, router_type, gates, probs, topk_mask, err_flag, stream);
+    return gate_impl<32>(logits, T, E, k, router_type, gates, probs, topk_mask, err_flag, stream);
+}
+
+int b200moe_dispatch(const float* gates, int T, int E, int capacity, int policy, int layout, int seg_stride,
+                     int32_t* slot_rank, int32_t* counts, int32_t* seg_base, float* gate_mass, float* importance,
+                     int64_t* stats, int32_t* workspace, cudaStream_t stream) {
+    B200_CHECK_ARG(T >= 1, B200MOE_ERR_CONFIG, "tokens_per_batch must be >= 1, got %d", T);
+    B200_CHECK_ARG(E >= 1 && E <= kMaxE, B200MOE_ERR_CONFIG, "n_experts %d", E);
+    B200_CHECK_ARG(policy == B200MOE_POLICY_POSITION || policy == B200MOE_POLICY_SCORE, B200MOE_ERR_CONFIG,
+                   "drop_policy must be one of ('position', 'score')");
+    B200_CHECK_ARG(layout == B200MOE_LAYOUT_COMPACT || (layout == B200MOE_LAYOUT_FIXED && seg_stride % kSegPad == 0),
+                   B200MOE_ERR_CONFIG, "fixed layout needs a segment stride multiple of %d", kSegPad);
+    dispatch_kernel<<<E, kDispThreads, 0, stream>>>(gates, T, E, capacity, policy, layout, seg_stride, slot_rank,
+                                                    counts, seg_base, gate_mass, importance, stats, workspace);
+    B200_CHECK_LAUNCH("dispatch");
+    return B200MOE_OK;
+}
+
+}  // extern "C"
