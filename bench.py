@@ -1,0 +1,302 @@
+"""Benchmark: E8T2 MoE-layer fwd+bwd tokens/s and MFU on B200 (BASELINE.json).
+
+Workload (BASELINE.json configs[1]): Llama-3-8B-shape E8T2 layer, hidden 4096,
+ffn 14336, 8 experts top-2, mixtral router, capacity factor 1.0 (reference
+formula ceil(T*CF/E)), position drop policy, 8192 tokens per GPU, bf16,
+upcycled weights (random-init dense FFN copied into the experts), synthetic
+inputs.  One step = moe_forward + importance aux loss + backward (all
+gradients), i.e. what a training step does for this layer.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun: expert parallelism (E/N experts per rank, NCCL
+all-to-all dispatch/combine), 8192 tokens per rank ("scaling": "weak").
+--impl reference times the CPU reference path (the oracle port of moefold's
+numpy implementation) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, F, E, K_TOP = 4096, 14336, 8, 2
+MEASURED = {"hbm_gbs": 6555.2, "bf16_tflops": 1692.0, "bf16_tflops_sustained": 1416.2}
+try:
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as _f:
+        MEASURED.update(json.load(_f))
+except OSError:
+    pass
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--tokens", type=int, default=8192)
+    p.add_argument("--cf", type=float, default=1.0)
+    p.add_argument("--router", default="mixtral")
+    p.add_argument("--policy", default="position")
+    p.add_argument("--cpu-tokens", type=int, default=512, help="bounded CPU sample (tokens per oracle step)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def cpu_sample(tokens: int, cf: float, router: str, policy: str, reps: int):
+    """Oracle (numpy port of moefold) fwd+bwd at the Llama shape on `tokens` tokens."""
+    import numpy as np  # noqa: F401
+    from oracle import moe_oracle as O
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    times = [O.time_fwd_bwd(tokens, H, F, E, K_TOP, cf, router, policy, reps=1) for _ in range(reps)]
+    return times, cores
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x100: "display_clock_setting"}
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                r = int(parts[2], 16)
+            except (ValueError, IndexError):
+                continue
+            sm.append(s)
+            mx = max(mx, m)
+            for bit, nm in names.items():
+                if r & bit and nm != "gpu_idle":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    reps = args.steps
+    for _ in range(args.warmup):
+        cpu_sample(args.cpu_tokens, args.cf, args.router, args.policy, 1)
+    times, cores = cpu_sample(args.cpu_tokens, args.cf, args.router, args.policy, reps)
+    tps = args.cpu_tokens * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 3),
+        "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"E8T2 layer fwd+bwd, H={H} F={F} E={E} k={K_TOP}, {args.router}, CF={args.cf}, "
+                               f"{args.policy}; CPU sample of {args.cpu_tokens} tokens per step",
+                   "tokens_per_step": args.cpu_tokens},
+        "cpu_baseline": {"value": round(tps, 3), "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.cpu_tokens} tokens/step at Llama-3 shape, numpy/OpenBLAS fp32, "
+                                   f"{cpu_model()}"},
+        "e2e": {"value": round(tps, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        from paper_2412_09952_b200.ep import run_ep_bench
+        run_ep_bench(args, rank, world, dev, MEASURED)
+        dist.destroy_process_group()
+        return
+    run_single(args, dev)
+
+
+def layer_flops(T: int, S: int) -> float:
+    """Algorithmic FLOPs of one fwd+bwd: 18*H*F per kept slot + router 6*T*H*E."""
+    return 18.0 * H * F * S + 6.0 * T * H * E
+
+
+def run_single(args, dev):
+    import torch
+    import paper_2412_09952_b200 as B
+    from paper_2412_09952_b200 import _lib
+    from paper_2412_09952_b200.upcycle import upcycle_experts, router_weights
+
+    T = args.tokens
+    torch.manual_seed(0)
+    # upcycled layer: one random-init dense SwiGLU FFN copied into 8 experts (K12)
+    w1 = (torch.randn(H, F, device=dev) * 0.02).to(torch.bfloat16)
+    w2 = (torch.randn(F, H, device=dev) * 0.02).to(torch.bfloat16)
+    w3 = (torch.randn(H, F, device=dev) * 0.02).to(torch.bfloat16)
+    W1, W2, W3 = (w.requires_grad_() for w in upcycle_experts(w1, w2, w3, E))
+    del w1, w2, w3
+    cfg_m = B.ModelConfig(vocab=32, hidden=H, layers=1, heads=32, kv_heads=8, ffn_hidden=F, seq_len=T)
+    wg, wn = router_weights(cfg_m, E, 0, 1, torch.float32, dev)
+    wg.requires_grad_()
+    wn.requires_grad_()
+    layer = B.MoELayer.from_stacked(B.RouterParams(wg, wn), W1, W2, W3)
+    gate = B.GateConfig(n_experts=E, top_k=K_TOP, router_type=args.router, capacity_factor=args.cf,
+                        drop_policy=args.policy)
+    x = torch.randn(T, H, device=dev).to(torch.bfloat16).requires_grad_()
+    dy = torch.randn(T, H, device=dev).to(torch.bfloat16)
+    lam = torch.tensor(0.01, device=dev)
+    params = [W1, W2, W3, wg, wn, x]
+
+    def step(xin, dyin):
+        for p in params:
+            p.grad = None
+        out = B.moe_forward(xin, layer, gate)
+        aux = B.importance_penalty(out.gates)
+        torch.autograd.backward([out.output, aux], [dyin, lam])
+        return out, aux
+
+    # warmup
+    for _ in range(max(args.warmup, 3)):
+        out, _ = step(x, dy)
+    torch.cuda.synchronize()
+    S = int(out.stats.assigned.sum())
+
+    # ---- timed region (device time, CUDA events on the launching stream)
+    prof = _lib.Profiler(events=True)
+    _lib.PROFILER = prof
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        s0.record()
+        for _ in range(args.steps):
+            step(x, dy)
+        s1.record()
+        torch.cuda.synchronize()
+    _lib.PROFILER = None
+    ms = s0.elapsed_time(s1) / args.steps
+    ktimes = prof.times_ms()
+    launches = prof.launches
+
+    gemm_names = [n for n in ktimes if n.startswith("b200moe_expert_")]
+    gemm_ms = sum(ktimes[n][0] for n in gemm_names) / args.steps
+    gemm_flops = 18.0 * H * F * S
+    achieved_tf = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    peak = MEASURED["bf16_tflops"]
+    flops = layer_flops(T, S)
+    tps = T / (ms * 1e-3)
+    mfu_measured = flops / (ms * 1e-3) / (peak * 1e12)
+    mfu_spec = flops / (ms * 1e-3) / 2.25e15
+
+    # ---- e2e: through the public API with pinned host buffers, H2D + D2H inside
+    e2e = None
+    if not args.no_e2e:
+        xh = x.detach().cpu().pin_memory()
+        dyh = dy.cpu().pin_memory()
+        res_h = torch.empty(2, dtype=torch.float32).pin_memory()
+        xd = torch.empty_like(x)
+        dyd = torch.empty_like(dy)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            dyd.copy_(dyh, non_blocking=True)
+            xin = xd.detach().requires_grad_()
+            out, aux = step(xin, dyd)
+            res_h[0:1].copy_(aux.detach().reshape(1), non_blocking=True)
+            return out
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": round(T / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
+               "h2d_bytes_per_step": xh.numel() * 2 + dyh.numel() * 2, "d2h_bytes_per_step": 4,
+               "ms_per_step": round(e2e_ms, 4)}
+
+    # ---- CPU baseline (oracle port) on a bounded sample, rank 0 / N=1 only
+    cpu = None
+    if not args.no_cpu_baseline:
+        times, cores = cpu_sample(args.cpu_tokens, args.cf, args.router, args.policy, 2)
+        cpu = {"value": round(args.cpu_tokens / min(times), 3), "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_tokens} tokens per fwd+bwd at the Llama-3 shape (best of 2), numpy/OpenBLAS "
+                         f"fp32 on {cores} threads, {cpu_model()}"}
+
+    clocks = clk.summary()
+    line = {
+        "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 1), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "Llama-3-8B-shape E8T2 MoE layer fwd+bwd (configs[1])", "hidden": H, "ffn": F,
+                   "experts": E, "top_k": K_TOP, "tokens": T, "capacity_factor": args.cf, "router": args.router,
+                   "drop_policy": args.policy, "kept_slots": S, "parallelism": "single GPU",
+                   "l2": "working set > L2: 2.8 GB of expert weights + 1.5 GB activations stream each step"},
+        "mfu": {"measured_peak": round(mfu_measured, 4), "spec_2250": round(mfu_spec, 4),
+                "flops_per_step": flops},
+        "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM, all 5 launches/step)", "bound": "tensor",
+                     "achieved": round(achieved_tf, 1), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved_tf / peak, 4), "traffic": None,
+                     "gemm_ms_per_step": round(gemm_ms, 4), "gemm_share_of_step": round(gemm_ms / ms, 4)},
+        "kernels_ms_per_step": {n.replace("b200moe_", ""): round(t / args.steps, 4) for n, (t, c) in ktimes.items()},
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -82,10 +82,60 @@ def exported_symbols() -> list[str]:
     return sorted(list(SIGNATURES) + ["b200moe_last_error"])
 
 
+# Kernel launches issued by each entry point (for the bench's gpu_launches).
+KERNELS_PER_CALL = {
+    "b200moe_router_fwd": 2, "b200moe_gate_from_logits": 1, "b200moe_dispatch": 1, "b200moe_permute": 1,
+    "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 2, "b200moe_router_wgrad": 2,
+    "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
+    "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_upcycle_copy": 3,
+}
+
+
+class Profiler:
+    """Optional per-entry-point accounting: launch counts and, with
+    `events=True`, CUDA events recorded on the current stream around each call
+    (the stream the kernels are launched on)."""
+
+    def __init__(self, events: bool = False):
+        self.events = events
+        self.launches = 0
+        self.calls: dict = {}
+        self._pending: list = []
+
+    def record(self, name, fn):
+        self.launches += KERNELS_PER_CALL.get(name, 0)
+        if not self.events:
+            return fn()
+        import torch
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        rc = fn()
+        b.record()
+        self._pending.append((name, a, b))
+        return rc
+
+    def times_ms(self) -> dict:
+        """Sum of event durations per entry point (synchronises)."""
+        out: dict = {}
+        for name, a, b in self._pending:
+            b.synchronize()
+            t, n = out.get(name, (0.0, 0))
+            out[name] = (t + a.elapsed_time(b), n + 1)
+        return out
+
+
+PROFILER: Profiler | None = None
+
+
 def call(name: str, *args) -> None:
     """Invoke a C entry point and map its status onto the reference exceptions."""
     lib = load()
-    rc = getattr(lib, name)(*args)
+    fn = getattr(lib, name)
+    if PROFILER is not None:
+        rc = PROFILER.record(name, lambda: fn(*args))
+    else:
+        rc = fn(*args)
     if rc == OK:
         return
     msg = (lib.b200moe_last_error() or b"").decode(errors="replace")

@@ -92,17 +92,17 @@ struct Sched {
         int r = t - prefix[s];
         ti.seg = s;
         if constexpr (kMode == kWgrad) {
-            const int tiles_w13 = (a.F / 256) * (a.H / 256);
+            const int tiles_w13 = (a.F / Cfg<kCG>::kTileM) * (a.H / kBN);
             if (r < 2 * tiles_w13) {
                 ti.sub = r / tiles_w13;
                 r -= ti.sub * tiles_w13;
-                const int nt = a.H / 256;
+                const int nt = a.H / kBN;
                 ti.m_tile = r / nt;
                 ti.n_tile = r % nt;
             } else {
                 ti.sub = 2;
                 r -= 2 * tiles_w13;
-                const int nt = a.F / 256;
+                const int nt = a.F / kBN;
                 ti.m_tile = r / nt;
                 ti.n_tile = r % nt;
             }
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
         int acc = 0;
         prefix[0] = 0;
         if constexpr (kMode == kWgrad) {
-            const int per_e = 2 * (a.F / 256) * (a.H / 256) + (a.H / 256) * (a.F / 256);
+            const int per_e = 2 * (a.F / C::kTileM) * (a.H / kBN) + (a.H / C::kTileM) * (a.F / kBN);
             for (int e = 0; e < a.E_local; ++e) {
                 acc += per_e;
                 prefix[e + 1] = acc;

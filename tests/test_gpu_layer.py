@@ -117,7 +117,9 @@ def test_small_layer(rt, pol, cf, noise):
 @pytest.mark.parametrize("cf", [1.0, 2.0, None])
 def test_cfg1_upcycled_layer(rt, cf):
     """Config 1: T=2048, H=256, F=512, E8T2, identical (upcycled) experts."""
-    run_and_compare(2048, 256, 512, 8, rt, "position", cf, False, identical=True, lam=0.01,
+    # lam=1: with identical experts the expert-path router gradient cancels
+    # exactly (sum of p*(dg - dg) = 0), so dW_g is carried by the aux term.
+    run_and_compare(2048, 256, 512, 8, rt, "position", cf, False, identical=True, lam=1.0,
                     wscale=(0.02, 0.0, 0.02))
 
 
