@@ -45,6 +45,7 @@ SIGNATURES = {
     "b200moe_expert_wgrad": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
     "b200moe_gemm_set_cta_group": [_I],
     "b200moe_gemm_set_max_ctas": [_I],
+    "b200moe_gemm_set_debug": [_I],
     "b200moe_upcycle_copy": [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P],
     "b200moe_version": [],
 }

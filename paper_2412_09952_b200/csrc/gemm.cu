@@ -23,8 +23,8 @@
 // (2 x 256 columns) so the epilogue of tile i overlaps the mainloop of i+1.
 // kCtaGroup == 1 is the single-SM variant (128 x 256 tile, 4 stages).
 //
-// Warp roles (192 threads): w0 TMA producer, w1 MMA issuer (leader CTA),
-// w2..w5 epilogue (TMEM lane quarter = warp % 4).
+// Warp roles (320 threads): w0 TMA producer, w1 MMA issuer (leader CTA),
+// w2..w9 epilogue (TMEM lane quarter = warp % 4, column half = (warp-2)/4).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -41,10 +41,12 @@ constexpr int kBK = 64;            // K per pipeline stage (128 B of bf16 = one 
 constexpr int kBN = 256;           // accumulator columns per tile
 constexpr int kRowsPerCta = 128;   // M rows per CTA
 constexpr int kMaxSeg = 64;
-constexpr int kNumThreads = 192;
+constexpr int kNumEpiWarps = 8;
+constexpr int kNumThreads = 64 + 32 * kNumEpiWarps;   // producer, MMA, 8 epilogue warps
 
 struct TmaSet {
-    CUtensorMap m[5];
+    CUtensorMap m[5];   // operand loads (SWIZZLE_128B)
+    CUtensorMap st[3];  // epilogue stores: 32 x 32 bf16 boxes (SWIZZLE_64B)
 };
 
 struct GemmArgs {
@@ -58,6 +60,7 @@ struct GemmArgs {
     __nv_bfloat16* out2;
     const __nv_bfloat16* in0;
     const __nv_bfloat16* in1;
+    int debug;  // bit 0: skip wgrad epilogue stores (diagnostics only)
 };
 
 template <int kCG>
@@ -68,7 +71,18 @@ struct Cfg {
     static constexpr int kBBytes = kBRows * kBK * 2;            // 16 KB (cg2) / 32 KB (cg1)
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTileM = kRowsPerCta * kCG;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + 4 * (kMaxSeg + 2);
+};
+
+// Per-(mode, cta-group) shared-memory plan: operand ring + per-epilogue-warp
+// staging (store ring of 2 x 2 KB; BWD2 on CTA pairs adds a TMA load ring of
+// 2 x (a, b) 2 KB chunks and trades two operand stages for it).
+template <int kMode, int kCG>
+struct Geo {
+    static constexpr bool kTmaEpiLoads = (kMode == kBwd2) && (kCG == 2);
+    static constexpr int kStages = kTmaEpiLoads ? 4 : Cfg<kCG>::kStages;
+    static constexpr int kEpiWarpBytes = kTmaEpiLoads ? 6 * 2048 : 2 * 2048;
+    static constexpr int kSmemBytes = kStages * Cfg<kCG>::kStageBytes + kNumEpiWarps * kEpiWarpBytes +
+                                      1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2);
 };
 
 // ------------------------------------------------------------------ tile map
@@ -217,37 +231,99 @@ __device__ __forceinline__ void produce_kblock(const TmaSet& tm, const GemmArgs&
 }
 
 // ------------------------------------------------------------------ epilogues
-__device__ __forceinline__ void store32(__nv_bfloat16* dst, const float* v) {
-    uint4* d = reinterpret_cast<uint4*>(dst);
+// Each epilogue warp owns a 2 x 2 KB staging ring in shared memory.  A 32-row
+// x 32-column bf16 chunk is written row-per-lane into the SWIZZLE_64B layout
+// (16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3): conflict-free)
+// and shipped with one TMA bulk tensor store, so global writes are full,
+// coalesced lines instead of 32 scattered 16-byte pieces per instruction.
+constexpr int kStageBufBytes = 2048;
+
+struct EpiRing {
+    uint8_t* base;  // this warp's two buffers
+    int idx;
+};
+
+__device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m, const float* v, int lane, int col,
+                                            int row0) {
+    uint8_t* buf = ring.base + ring.idx * kStageBufBytes;
+    if (lane == 0) ptx::bulk_wait_read<1>();  // the older store from this buffer has been read
+    __syncwarp();
+    uint4* rowp = reinterpret_cast<uint4*>(buf + lane * 64);
+    const int sw = (lane >> 1) & 3;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) d[i] = pack8(v + 8 * i);
+    for (int j = 0; j < 4; ++j) rowp[j ^ sw] = pack8(v + 8 * j);
+    ptx::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        ptx::tma_store_2d(m, buf, col, row0);
+        ptx::bulk_commit();
+    }
+    ring.idx ^= 1;
 }
 
-__device__ __forceinline__ void load32(const __nv_bfloat16* src, float* v) {
-    const uint4* s = reinterpret_cast<const uint4*>(src);
+// BWD2 load ring: two buffers, each holding a 32x32 chunk of the stored `a`
+// and `b` pre-activations (2 KB each, SWIZZLE_64B), filled by TMA and tracked
+// by one mbarrier per buffer.
+struct EpiLoads {
+    uint8_t* base;     // 2 x (a 2 KB, b 2 KB)
+    uint64_t* bar;     // 2 mbarriers
+    int idx;           // next buffer to fill
+    uint32_t phases;   // bit i = parity of bar[i]'s next completion
+};
+
+__device__ __forceinline__ void epi_load_issue(EpiLoads& ld, const CUtensorMap* ma, const CUtensorMap* mb, int col,
+                                               int row0, int lane) {
+    if (lane == 0) {
+        uint8_t* buf = ld.base + ld.idx * 2 * kStageBufBytes;
+        ptx::mbar_arrive_expect_tx(&ld.bar[ld.idx], 2 * kStageBufBytes);
+        ptx::tma_load_2d(ma, &ld.bar[ld.idx], buf, col, row0);
+        ptx::tma_load_2d(mb, &ld.bar[ld.idx], buf + kStageBufBytes, col, row0);
+    }
+    ld.idx ^= 1;
+}
+
+// Wait for buffer `i`, then unpack this lane's row of a and b.
+__device__ __forceinline__ void epi_load_take(EpiLoads& ld, int i, int lane, float* av, float* bv) {
+    ptx::mbar_wait(&ld.bar[i], (ld.phases >> i) & 1u);
+    ld.phases ^= 1u << i;
+    const uint8_t* buf = ld.base + i * 2 * kStageBufBytes;
+    const uint4* ra = reinterpret_cast<const uint4*>(buf + lane * 64);
+    const uint4* rb = reinterpret_cast<const uint4*>(buf + kStageBufBytes + lane * 64);
+    const int sw = (lane >> 1) & 3;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) unpack8(s[i], v + 8 * i);
+    for (int j = 0; j < 4; ++j) {
+        unpack8(ra[j ^ sw], av + 8 * j);
+        unpack8(rb[j ^ sw], bv + 8 * j);
+    }
+    __syncwarp();  // every lane has read buffer i before it can be refilled
 }
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
 
+// One epilogue warp: TMEM lane quarter q (rows q*32..q*32+31 of this CTA's
+// 128) and column half `half` of the 256-column accumulator.  Waits on the
+// accumulator itself (tfull) so that loads which do not depend on it (the
+// stored pre-activations in BWD2) are issued before the wait.  Segment rows
+// are padded to 128, so a warp's 32 rows are either all inside the padded
+// segment or all outside it.
 template <int kMode, int kCG>
-__device__ __forceinline__ void epilogue_tile(const GemmArgs& a, const TileInfo& ti, uint32_t tmem_acc, int q,
-                                              int lane, uint32_t rank, bool k_empty) {
+__device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& a, const TileInfo& ti,
+                                              uint32_t tmem_acc, int q, int half, int lane, uint32_t rank,
+                                              bool k_empty, uint64_t* tfull, uint32_t tphase, EpiRing& ring,
+                                              EpiLoads& ld) {
     using C = Cfg<kCG>;
     uint32_t r0[32], r1[32];
     float v0[32], v1[32], v2[32];
     const uint32_t lane_addr = tmem_acc + ((uint32_t)(q * 32) << 16);
     if constexpr (kMode == kWgrad) {
         const int e = ti.seg;
-        const int row = ti.m_tile * C::kTileM + rank * kRowsPerCta + q * 32 + lane;  // output row
-        int ncols;
-        __nv_bfloat16* out;
-        if (ti.sub == 2) { ncols = a.F; out = a.out1 + ((size_t)e * a.H + row) * a.F; }
-        else { ncols = a.H; out = (ti.sub == 0 ? a.out0 : a.out2) + ((size_t)e * a.F + row) * a.H; }
-        out += ti.n_tile * kBN;
-        (void)ncols;
-        for (int c = 0; c < kBN; c += 32) {
+        const int orow = ti.m_tile * C::kTileM + rank * kRowsPerCta + q * 32;  // first output row of the warp
+        const int smap = ti.sub == 0 ? 0 : (ti.sub == 1 ? 2 : 1);            // dW1, dW3, dW2
+        const int grow = (ti.sub == 2 ? e * a.H : e * a.F) + orow;
+        const int col0 = ti.n_tile * kBN;
+        ptx::mbar_wait(tfull, tphase);
+        ptx::tc_fence_after();
+        for (int c = half * 128; c < half * 128 + 128; c += 32) {
             if (!k_empty) {
                 ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
                 ptx::tmem_ld_wait();
@@ -257,19 +333,98 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, const TileInfo&
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v0[i] = 0.f;
             }
-            store32(out + c, v0);
+            if (!(a.debug & 1)) stage_store(ring, &tm.st[smap], v0, lane, col0 + c, grow);
         }
         return;
     } else {
         const int cnt = a.seg_count[ti.seg];
         const int rel = ti.m_tile * C::kTileM + rank * kRowsPerCta + q * 32;  // first row of this warp
         const int limit = round_up(cnt, kSegPad);
-        if (rel >= limit) return;  // whole warp outside the padded segment (warp-uniform)
-        const bool valid = (rel + lane) < limit;
-        const size_t row = (size_t)a.seg_base[ti.seg] + rel + lane;
+        const bool live = rel < limit;                                        // warp-uniform
+        const int row0 = a.seg_base[ti.seg] + rel;
+        if constexpr (Geo<kMode, kCG>::kTmaEpiLoads) {
+            // SwiGLU backward with the stored pre-activations (a, b) streamed by
+            // TMA one 32-column chunk ahead; chunk 0 is requested before the
+            // accumulator wait.
+            const int col0 = ti.n_tile * kBN + half * 128;
+            if (live) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0, row0, lane);
+            ptx::mbar_wait(tfull, tphase);
+            ptx::tc_fence_after();
+            if (!live) return;
+#pragma unroll 1
+            for (int cc = 0; cc < 4; ++cc) {
+                const int c = cc * 32;
+                const int cur = ld.idx ^ 1;  // buffer holding chunk cc
+                if (cc + 1 < 4) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0 + c + 32, row0, lane);
+                ptx::tmem_ld_32x32b_x32(lane_addr + half * 128 + c, r0);
+                epi_load_take(ld, cur, lane, v0, v1);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float dm = __uint_as_float(r0[i]);
+                    const float av = v0[i], bv = v1[i];
+                    const float sg = sigmoidf_(av);
+                    v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
+                    v1[i] = dm * (av * sg);
+                }
+                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
+                stage_store(ring, &tm.st[1], v1, lane, col0 + c, row0);
+            }
+            return;
+        } else if constexpr (kMode == kBwd2) {
+            // SwiGLU backward: prefetch the stored pre-activations (a, b) one
+            // 32-column chunk ahead; the first chunk is in flight before the
+            // accumulator wait.
+            const int col0 = ti.n_tile * kBN + half * 128;
+            const size_t off = (size_t)(row0 + lane) * a.F + col0;
+            uint4 pa[2][4], pb[2][4];
+            if (live) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    pa[0][i] = ld_nc_v4(a.in0 + off + 8 * i);
+                    pb[0][i] = ld_nc_v4(a.in1 + off + 8 * i);
+                }
+            }
+            ptx::mbar_wait(tfull, tphase);
+            ptx::tc_fence_after();
+            if (!live) return;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const int c = cc * 32;
+                const int cur = cc & 1;
+                if (cc + 1 < 4) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        pa[cur ^ 1][i] = ld_nc_v4(a.in0 + off + c + 32 + 8 * i);
+                        pb[cur ^ 1][i] = ld_nc_v4(a.in1 + off + c + 32 + 8 * i);
+                    }
+                }
+                ptx::tmem_ld_32x32b_x32(lane_addr + half * 128 + c, r0);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    unpack8(pa[cur][i], v0 + 8 * i);
+                    unpack8(pb[cur][i], v1 + 8 * i);
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float dm = __uint_as_float(r0[i]);
+                    const float av = v0[i], bv = v1[i];
+                    const float sg = sigmoidf_(av);
+                    v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
+                    v1[i] = dm * (av * sg);
+                }
+                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
+                stage_store(ring, &tm.st[1], v1, lane, col0 + c, row0);
+            }
+            return;
+        }
+        ptx::mbar_wait(tfull, tphase);
+        ptx::tc_fence_after();
+        if (!live) return;
         if constexpr (kMode == kFwd1) {
-            const size_t off = row * a.F + ti.n_tile * 128;
-            for (int c = 0; c < 128; c += 32) {
+            const int col0 = ti.n_tile * 128;
+            for (int c = half * 64; c < half * 64 + 64; c += 32) {
                 ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
                 ptx::tmem_ld_32x32b_x32(lane_addr + 128 + c, r1);
                 ptx::tmem_ld_wait();
@@ -281,44 +436,18 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, const TileInfo&
                     v1[i] = bv;
                     v2[i] = av * sigmoidf_(av) * bv;
                 }
-                if (valid) {
-                    store32(a.out0 + off + c, v0);
-                    store32(a.out1 + off + c, v1);
-                    store32(a.out2 + off + c, v2);
-                }
+                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
+                stage_store(ring, &tm.st[1], v1, lane, col0 + c, row0);
+                stage_store(ring, &tm.st[2], v2, lane, col0 + c, row0);
             }
-        } else if constexpr (kMode == kFwd2 || kMode == kBwd1) {
-            const size_t off = row * a.H + ti.n_tile * kBN;
-            for (int c = 0; c < kBN; c += 32) {
+        } else {  // kFwd2 / kBwd1: plain bf16 store
+            const int col0 = ti.n_tile * kBN;
+            for (int c = half * 128; c < half * 128 + 128; c += 32) {
                 ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]);
-                if (valid) store32(a.out0 + off + c, v0);
-            }
-        } else {  // kBwd2: SwiGLU backward from the stored pre-activations
-            const size_t off = row * a.F + ti.n_tile * kBN;
-            for (int c = 0; c < kBN; c += 32) {
-                ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
-                if (valid) {
-                    load32(a.in0 + off + c, v0);  // a
-                    load32(a.in1 + off + c, v1);  // b
-                }
-                ptx::tmem_ld_wait();
-                if (valid) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float dm = __uint_as_float(r0[i]);
-                        const float av = v0[i], bv = v1[i];
-                        const float sg = sigmoidf_(av);
-                        const float da = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
-                        const float db = dm * (av * sg);
-                        v0[i] = da;
-                        v1[i] = db;
-                    }
-                    store32(a.out0 + off + c, v0);
-                    store32(a.out1 + off + c, v1);
-                }
+                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
             }
         }
     }
@@ -330,14 +459,17 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& a, const TileInfo&
 template <int kMode, int kCG>
 __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_constant__ TmaSet tm, GemmArgs a) {
     using C = Cfg<kCG>;
+    using G = Geo<kMode, kCG>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stages = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-    uint64_t* empty = full + C::kStages;
-    uint64_t* tfull = empty + C::kStages;
+    uint8_t* staging = smem + G::kStages * C::kStageBytes;  // per-epilogue-warp rings
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + kNumEpiWarps * G::kEpiWarpBytes);
+    uint64_t* empty = full + G::kStages;
+    uint64_t* tfull = empty + G::kStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* ldbar = tempty + 2;  // 2 per epilogue warp (BWD2 TMA load ring)
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(ldbar + 2 * kNumEpiWarps);
     int* prefix = reinterpret_cast<int*>(tmem_base_slot + 1);
 
     const int warp = threadIdx.x / 32;
@@ -366,14 +498,16 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
     }
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 5; ++i) ptx::prefetch_tmap(&tm.m[i]);
-        for (int s = 0; s < C::kStages; ++s) {
+        for (int i = 0; i < 3; ++i) ptx::prefetch_tmap(&tm.st[i]);
+        for (int s = 0; s < G::kStages; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], kCG * 4);
+            ptx::mbar_init(&tempty[i], kCG * kNumEpiWarps);
         }
+        for (int i = 0; i < 2 * kNumEpiWarps; ++i) ptx::mbar_init(&ldbar[i], 1);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc<kCG>(tmem_base_slot, 512);
@@ -405,7 +539,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
                             uint8_t* sA = stages + stage * C::kStageBytes;
                             produce_kblock<kMode, kCG>(tm, a, ti, a.seg_base[s] + kb * kBK, 0, rank, &full[stage],
                                                        sA, sA + C::kABytes);
-                            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+                            if (++stage == G::kStages) { stage = 0; phase ^= 1; }
                         }
                     }
                 } else {
@@ -415,7 +549,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
                         if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes * kCG);
                         uint8_t* sA = stages + stage * C::kStageBytes;
                         produce_kblock<kMode, kCG>(tm, a, ti, kb, 0, rank, &full[stage], sA, sA + C::kABytes);
-                        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+                        if (++stage == G::kStages) { stage = 0; phase ^= 1; }
                     }
                 }
             }
@@ -451,7 +585,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
                         ptx::mma_commit<kCG>(&empty[stage], 0x3);
                     }
                     __syncwarp();
-                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+                    if (++stage == G::kStages) { stage = 0; phase ^= 1; }
                 }
                 if (ptx::elect_one()) ptx::mma_commit<kCG>(&tfull[acc], 0x3);
                 __syncwarp();
@@ -459,21 +593,25 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
             }
         }
     } else {
-        // ================= epilogue (warps 2..5)
+        // ================= epilogue (warps 2..9): lane quarter warp%4, column half
         const int q = warp % 4;
+        const int half = (warp - 2) / 4;
         int acc = 0;
         uint32_t acc_phase = 0;
+        EpiRing ring{staging + (warp - 2) * G::kEpiWarpBytes, 0};
+        EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + 2 * kStageBufBytes, ldbar + 2 * (warp - 2), 0, 0};
         for (int t = cid; t < sched.total; t += ncl) {
             const TileInfo ti = sched.decode(t, a);
             const bool k_empty = (kMode == kWgrad) ? (wgrad_k_blocks(a, ti.seg) == 0) : false;
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
-            epilogue_tile<kMode, kCG>(a, ti, tmem_base + acc * kBN, q, lane, rank, k_empty);
+            epilogue_tile<kMode, kCG>(tm, a, ti, tmem_base + acc * kBN, q, half, lane, rank, k_empty, &tfull[acc],
+                                      acc_phase, ring, ld);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(&tempty[acc], 0);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (lane == 0) ptx::bulk_wait<0>();  // all stores of this warp complete
+        __syncwarp();
     }
 
     ptx::tc_fence_before();
@@ -504,7 +642,8 @@ static EncodeTiledFn get_encode() {
 
 // 2-D bf16 tensor [outer, inner] (inner contiguous, row pitch `ld` elements).
 // K-major operands use box {64, 128}; MN-major operands box {64, 64}.
-static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, bool mn_major) {
+static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, bool mn_major,
+                    bool ptr_is_store_target = false) {
     EncodeTiledFn enc = get_encode();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable");
@@ -514,8 +653,14 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ou
     cuuint64_t strides[1] = {ld * 2};
     cuuint32_t box[2] = {64, mn_major ? 64u : 128u};
     cuuint32_t estr[2] = {1, 1};
+    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
+    if (ptr_is_store_target) {  // epilogue store map: 32 x 32 boxes, 64-byte swizzle
+        box[0] = 32;
+        box[1] = 32;
+        sw = CU_TENSOR_MAP_SWIZZLE_64B;
+    }
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d) inner=%llu outer=%llu ld=%llu", (int)r,
@@ -527,21 +672,23 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ou
 
 static int g_cta_group = 2;  // 2 = CTA-pair kernels (default), 1 = single-SM kernels
 static int g_max_ctas = kNumSMs;
+static int g_debug = 0;
 
 template <int kMode, int kCG>
 static int launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s) {
-    using C = Cfg<kCG>;
+    using G = Geo<kMode, kCG>;
+    static_assert(G::kSmemBytes <= 227 * 1024, "shared memory plan exceeds 227 KB");
     auto kern = moe_gemm_kernel<kMode, kCG>;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmemBytes);
         attr_done = true;
     }
     cudaLaunchConfig_t cfg = {};
     int grid = g_max_ctas - (g_max_ctas % kCG);
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kNumThreads);
-    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.dynamicSmemBytes = G::kSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -550,7 +697,9 @@ static int launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm, a);
+    GemmArgs args = a;
+    args.debug = g_debug;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm, args);
     if (e != cudaSuccess) {
         set_error("moe_gemm_kernel<%d,%d> launch: %s", kMode, kCG, cudaGetErrorString(e));
         return B200MOE_ERR_CUDA;
@@ -590,6 +739,11 @@ int b200moe_gemm_set_cta_group(int cg) {
     return B200MOE_OK;
 }
 
+int b200moe_gemm_set_debug(int flags) {
+    g_debug = flags;
+    return B200MOE_OK;
+}
+
 int b200moe_gemm_set_max_ctas(int n) {
     B200_CHECK_ARG(n >= 2 && n <= 4096, B200MOE_ERR_CONFIG, "max ctas %d", n);
     g_max_ctas = n;
@@ -606,6 +760,9 @@ int b200moe_expert_fwd1(const void* xp, const void* w1, const void* w3, const in
     B200_TRY(make_map(&tm.m[2], w3, H, (uint64_t)E_local * F, H, false));
     tm.m[3] = tm.m[0];
     tm.m[4] = tm.m[0];
+    B200_TRY(make_map(&tm.st[0], a_out, F, rows, F, false, true));
+    B200_TRY(make_map(&tm.st[1], b_out, F, rows, F, false, true));
+    B200_TRY(make_map(&tm.st[2], h_out, F, rows, F, false, true));
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)a_out, (__nv_bfloat16*)b_out, (__nv_bfloat16*)h_out, nullptr, nullptr};
     return dispatch_launch<kFwd1>(tm, a, stream);
@@ -619,6 +776,8 @@ int b200moe_expert_fwd2(const void* h, const void* w2, const int* seg_base, cons
     B200_TRY(make_map(&tm.m[0], h, F, rows, F, false));
     B200_TRY(make_map(&tm.m[1], w2, F, (uint64_t)E_local * H, F, false));
     tm.m[2] = tm.m[3] = tm.m[4] = tm.m[0];
+    B200_TRY(make_map(&tm.st[0], o_out, H, rows, H, false, true));
+    tm.st[1] = tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)o_out, nullptr, nullptr, nullptr, nullptr};
     return dispatch_launch<kFwd2>(tm, a, stream);
@@ -631,7 +790,12 @@ int b200moe_expert_bwd2(const void* dout, const void* w2, const void* a_pre, con
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], dout, H, rows, H, false));
     B200_TRY(make_map(&tm.m[1], w2, F, (uint64_t)E_local * H, F, true));
-    tm.m[2] = tm.m[3] = tm.m[4] = tm.m[0];
+    B200_TRY(make_map(&tm.m[2], a_pre, F, rows, F, false, true));  // epilogue loads: 32 x 32 boxes
+    B200_TRY(make_map(&tm.m[3], b_pre, F, rows, F, false, true));
+    tm.m[4] = tm.m[0];
+    B200_TRY(make_map(&tm.st[0], da_out, F, rows, F, false, true));
+    B200_TRY(make_map(&tm.st[1], db_out, F, rows, F, false, true));
+    tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)da_out, (__nv_bfloat16*)db_out, nullptr,
                   (const __nv_bfloat16*)a_pre, (const __nv_bfloat16*)b_pre};
@@ -648,6 +812,8 @@ int b200moe_expert_bwd1(const void* da, const void* db, const void* w1, const vo
     B200_TRY(make_map(&tm.m[2], w1, H, (uint64_t)E_local * F, H, true));
     B200_TRY(make_map(&tm.m[3], w3, H, (uint64_t)E_local * F, H, true));
     tm.m[4] = tm.m[0];
+    B200_TRY(make_map(&tm.st[0], dxp_out, H, rows, H, false, true));
+    tm.st[1] = tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dxp_out, nullptr, nullptr, nullptr, nullptr};
     return dispatch_launch<kBwd1>(tm, a, stream);
@@ -663,6 +829,9 @@ int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const 
     B200_TRY(make_map(&tm.m[2], da, F, rows, F, true));
     B200_TRY(make_map(&tm.m[3], xp, H, rows, H, true));
     B200_TRY(make_map(&tm.m[4], db, F, rows, F, true));
+    B200_TRY(make_map(&tm.st[0], dw1, H, (uint64_t)E_local * F, H, false, true));
+    B200_TRY(make_map(&tm.st[1], dw2, F, (uint64_t)E_local * H, F, false, true));
+    B200_TRY(make_map(&tm.st[2], dw3, H, (uint64_t)E_local * F, H, false, true));
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dw1, (__nv_bfloat16*)dw2, (__nv_bfloat16*)dw3, nullptr, nullptr};
     return dispatch_launch<kWgrad>(tm, a, stream);
