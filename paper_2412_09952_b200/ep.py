@@ -1,0 +1,359 @@
+"""Expert parallelism for the E8T2 layer: one process per GPU, E/R experts per
+rank, NCCL all-to-all dispatch / combine (reference ownership
+rule moefold/upcycle.py:207-208, byte model moefold/plan.py:246-247).
+
+Per rank r (T_local tokens, rank-local capacity, so routing equals the
+single-GPU oracle on that rank's batch):
+
+  forward   K1 router -> K1b dispatch (fixed layout: expert e's segment at
+            e * cap_pad) -> K2 permute into the send buffer [E, cap_pad, H]
+            -> all_to_all(counts[E]) and all_to_all(send) with equal splits
+            -> grouped GEMMs over R * E_local received segments
+            -> all_to_all back -> K5 combine
+  backward  K6 combine' -> all_to_all(dO) -> BWD2 / WGRAD / BWD1 over the
+            received segments -> all_to_all(dxp) back -> router' ->
+            all_reduce(dW_g, dW_noise)  (the router is replicated)
+
+Counts never leave the device: the GEMM kernels read the received counts
+directly, so no host synchronisation happens inside the layer.
+
+The data-movement plan (`EPPlan`) is plain torch and is exercised on CPU with
+the gloo backend in tests/test_ep_gloo.py; the compute runs only in the CUDA
+library.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .errors import ConfigError, ShapeError
+from .moe import (GateConfig, RoutingStats, SEG_PAD, _arange_i32, _dispatch_ws, _ep, _noise, expert_capacity)
+
+
+@dataclass
+class EPPlan:
+    """Static layout of one EP step (identical on every rank)."""
+
+    world: int
+    rank: int
+    n_experts: int
+    tokens: int          # T_local
+    capacity: int | None
+    cap_pad: int         # rows per (rank, expert) segment, multiple of 128
+
+    @classmethod
+    def make(cls, world: int, rank: int, n_experts: int, tokens: int, capacity_factor: float | None) -> "EPPlan":
+        if n_experts % world != 0:
+            raise ConfigError(f"n_experts ({n_experts}) not divisible by ep={world}")
+        cap = expert_capacity(tokens, n_experts, capacity_factor)
+        c = tokens if cap is None else min(cap, tokens)
+        cap_pad = max(SEG_PAD, (c + SEG_PAD - 1) // SEG_PAD * SEG_PAD)
+        return cls(world, rank, n_experts, tokens, cap, cap_pad)
+
+    @property
+    def e_local(self) -> int:
+        return self.n_experts // self.world
+
+    @property
+    def owned(self) -> range:
+        return range(self.rank * self.e_local, (self.rank + 1) * self.e_local)
+
+    @property
+    def send_rows(self) -> int:
+        return self.n_experts * self.cap_pad
+
+    def recv_segments(self, device):
+        """(base, expert) of the R * E_local received segments: segment
+        (src, el) starts at (src * E_local + el) * cap_pad."""
+        n = self.world * self.e_local
+        base = torch.arange(n, dtype=torch.int32, device=device) * self.cap_pad
+        expert = torch.arange(n, dtype=torch.int32, device=device) % self.e_local
+        return base, expert
+
+    def exchange_counts(self, counts: torch.Tensor, group=None) -> torch.Tensor:
+        """counts[E] (tokens this rank sends to each expert) -> recv[R * E_local]
+        (tokens each source rank sends to each of my experts)."""
+        recv = torch.empty(self.world * self.e_local, dtype=counts.dtype, device=counts.device)
+        dist.all_to_all_single(recv, counts.contiguous(), group=group)
+        return recv
+
+    def exchange_rows(self, out: torch.Tensor, inp: torch.Tensor, group=None) -> torch.Tensor:
+        """Equal-split all-to-all of [E * cap_pad, D] row blocks (expert-major)."""
+        dist.all_to_all_single(out, inp, group=group)
+        return out
+
+
+class _EPFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w_g, w_noise, W1, W2, W3, z, st):
+        cfg, plan, group = st["cfg"], st["plan"], st["group"]
+        T, H = x.shape
+        E = w_g.shape[1]
+        El = plan.e_local
+        F = W1.shape[1]
+        dev = x.device
+        s = _lib.stream_ptr()
+        f32 = dict(dtype=torch.float32, device=dev)
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        rt = _lib.ROUTER[cfg.router_type]
+
+        logits = torch.empty(T, E, **f32)
+        gates = torch.empty(T, E, **f32)
+        probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
+        noise_act = torch.empty(T, E, **f32) if z is not None else None
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws = torch.empty(2 * H * _ep(E), **f32)
+        _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
+                  cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),
+                  ws.data_ptr(), err.data_ptr(), s)
+        slot_rank = torch.empty(T, E, dtype=torch.int32, device=dev)
+        counts = torch.empty(E, dtype=torch.int32, device=dev)
+        seg_base = torch.empty(E, dtype=torch.int32, device=dev)
+        gate_mass = torch.empty(E, **f32)
+        imp = torch.empty(E, **f32)
+        stats = torch.empty(2, dtype=torch.int64, device=dev)
+        _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if plan.capacity is None else plan.capacity,
+                  _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_FIXED, plan.cap_pad, slot_rank.data_ptr(),
+                  counts.data_ptr(), seg_base.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),
+                  _dispatch_ws(dev).data_ptr(), s)
+        Rs = plan.send_rows
+        xs = torch.empty(Rs, H, **bf)
+        _lib.call("b200moe_permute", x.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), counts.data_ptr(), T,
+                  H, E, xs.data_ptr(), s)
+        rcounts = plan.exchange_counts(counts, group)
+        xr = plan.exchange_rows(torch.empty_like(xs), xs, group)
+        rbase, rexp = plan.recv_segments(dev)
+        nseg = plan.world * El
+        A = torch.empty(Rs, F, **bf)
+        B = torch.empty(Rs, F, **bf)
+        Hh = torch.empty(Rs, F, **bf)
+        _lib.call("b200moe_expert_fwd1", xr.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
+                  rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, A.data_ptr(), B.data_ptr(), Hh.data_ptr(), s)
+        Or = torch.empty(Rs, H, **bf)
+        _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
+                  rexp.data_ptr(), nseg, Rs, H, F, El, Or.data_ptr(), s)
+        Os = plan.exchange_rows(torch.empty_like(Or), Or, group)
+        y = torch.empty(T, H, **bf)
+        _lib.call("b200moe_combine", Os.data_ptr(), gates.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), T,
+                  H, E, y.data_ptr(), s)
+        st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_base,
+                             gate_mass=gate_mass, importance=imp, stats=stats, err=err, recv_counts=rcounts)
+        ctx.st = st
+        ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_base,
+                              rcounts, xr, A, B, Hh, Os)
+        return y, gates
+
+    @staticmethod
+    def backward(ctx, dy, dgates):
+        (x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_base, rcounts, xr, A, B,
+         Hh, Os) = ctx.saved_tensors
+        st = ctx.st
+        cfg, plan, group = st["cfg"], st["plan"], st["group"]
+        T, H = x.shape
+        E = w_g.shape[1]
+        El = plan.e_local
+        F = W1.shape[1]
+        Rs = plan.send_rows
+        dev = x.device
+        s = _lib.stream_ptr()
+        f32 = dict(dtype=torch.float32, device=dev)
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        nseg = plan.world * El
+        rbase, rexp = plan.recv_segments(dev)
+
+        dy = (torch.zeros(T, H, **bf) if dy is None else dy).to(torch.bfloat16).contiguous()
+        dOs = torch.empty(Rs, H, **bf)
+        dg = torch.empty(T, E, **f32)
+        _lib.call("b200moe_combine_bwd", dy.data_ptr(), Os.data_ptr(), gates.data_ptr(), slot_rank.data_ptr(),
+                  seg_base.data_ptr(), counts.data_ptr(), T, H, E, dOs.data_ptr(), dg.data_ptr(), s)
+        dOr = plan.exchange_rows(torch.empty_like(dOs), dOs, group)
+        dA = torch.empty(Rs, F, **bf)
+        dB = torch.empty(Rs, F, **bf)
+        _lib.call("b200moe_expert_bwd2", dOr.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(), rbase.data_ptr(),
+                  rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(), dB.data_ptr(), s)
+        dW1 = torch.empty_like(W1)
+        dW2 = torch.empty_like(W2)
+        dW3 = torch.empty_like(W3)
+        _lib.call("b200moe_expert_wgrad", xr.data_ptr(), Hh.data_ptr(), dOr.data_ptr(), dA.data_ptr(), dB.data_ptr(),
+                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dW1.data_ptr(),
+                  dW2.data_ptr(), dW3.data_ptr(), s)
+        dxr = torch.empty(Rs, H, **bf)
+        _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
+                  rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dxr.data_ptr(), s)
+        dxs = plan.exchange_rows(torch.empty_like(dxr), dxr, group)
+        dx = torch.empty(T, H, **bf)
+        dh = torch.empty(T, E, **f32)
+        dn = torch.empty(T, E, **f32) if z is not None else None
+        dgx, sx_t, sx_e = None, 0, 0
+        if dgates is not None:
+            dgx = dgates.to(torch.float32)
+            sx_t, sx_e = dgx.stride()
+        ws = torch.empty(2 * H * _ep(E), **f32)
+        _lib.call("b200moe_router_bwd", dxs.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), dg.data_ptr(),
+                  _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(), w_noise.data_ptr(),
+                  _lib.ptr(z), _lib.ptr(noise_act), T, H, E, _lib.ROUTER[cfg.router_type], dx.data_ptr(),
+                  dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
+        dwg = torch.empty(H, E, **f32)
+        dwn = torch.empty(H, E, **f32) if z is not None else None
+        wsw = torch.empty((T + 127) // 128 * H * E, **f32)
+        _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), _lib.ptr(dn), T, H, E, dwg.data_ptr(),
+                  _lib.ptr(dwn), wsw.data_ptr(), s)
+        if st.get("reduce_router", True):
+            dist.all_reduce(dwg, group=group)
+            if dwn is not None:
+                dist.all_reduce(dwn, group=group)
+        return dx, dwg, dwn, dW1, dW2, dW3, None, None
+
+
+class ExpertParallelMoE:
+    """EP-sharded E8T2 layer on this rank.  `w_g`, `w_noise`: replicated
+    router [H, E] fp32; W1, W3 [E_local, F, H], W2 [E_local, H, F] bf16: the
+    experts this rank owns (e.g. from upcycle_shard / upcycle_experts)."""
+
+    def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if cfg.n_experts % self.world != 0:
+            raise ConfigError(f"n_experts ({cfg.n_experts}) not divisible by ep={self.world}")
+        if W1.shape[0] != cfg.n_experts // self.world:
+            raise ShapeError(f"rank holds {W1.shape[0]} experts, expected {cfg.n_experts // self.world}")
+        if cfg.n_experts > 32:
+            raise ConfigError("the B200 router supports up to 32 experts")
+        self.w_g, self.w_noise, self.W1, self.W2, self.W3, self.cfg = w_g, w_noise, W1, W2, W3, cfg
+
+    def forward(self, x: torch.Tensor, rng=None, training: bool = False, noise=None, reduce_router: bool = True):
+        T, H = x.shape
+        if H % 256 or self.W1.shape[1] % 256:
+            raise ShapeError("the EP path needs hidden and ffn multiples of 256")
+        plan = EPPlan.make(self.world, self.rank, self.cfg.n_experts, T, self.cfg.capacity_factor)
+        z = _noise(T, self.cfg.n_experts, x.device, self.cfg.noise_enabled and training, rng, noise)
+        st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router)
+        y, gates = _EPFunction.apply(x.to(torch.bfloat16).contiguous(), self.w_g.to(torch.float32).contiguous(),
+                                     self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)
+        r = st["routing"]
+        from .moe import MoEForwardResult
+        out = MoEForwardResult(output=y, stats=RoutingStats(r["counts"], r["stats"], r["gate_mass"], plan.capacity,
+                                                            r["err"]), gates=gates)
+        out.routing = r
+        out.plan = plan
+        return out
+
+    __call__ = forward
+
+
+def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
+    """bench.py --gpus N under torchrun: weak scaling, T_local tokens per rank."""
+    import json
+    import bench as B
+    import paper_2412_09952_b200 as P
+    from .upcycle import router_weights, upcycle_experts
+
+    H, F, E, K = B.H, B.F, B.E, B.K_TOP
+    T = args.tokens
+    if E % world:
+        raise ConfigError(f"{E} experts cannot be split over {world} ranks")
+    torch.manual_seed(0)  # same dense FFN on every rank (upcycling is rank-local copying)
+    w1 = (torch.randn(H, F, device=dev) * 0.02).to(torch.bfloat16)
+    w2 = (torch.randn(F, H, device=dev) * 0.02).to(torch.bfloat16)
+    w3 = (torch.randn(H, F, device=dev) * 0.02).to(torch.bfloat16)
+    W1, W2, W3 = (w.requires_grad_() for w in upcycle_experts(w1, w2, w3, E // world))
+    del w1, w2, w3
+    cfg_m = P.ModelConfig(vocab=32, hidden=H, layers=1, heads=32, kv_heads=8, ffn_hidden=F, seq_len=T)
+    wg, wn = router_weights(cfg_m, E, 0, 1, torch.float32, dev)
+    wg.requires_grad_()
+    wn.requires_grad_()
+    gate = P.GateConfig(n_experts=E, top_k=K, router_type=args.router, capacity_factor=args.cf,
+                        drop_policy=args.policy)
+    layer = ExpertParallelMoE(wg, wn, W1, W2, W3, gate)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    x = torch.randn(T, H, device=dev, generator=g).to(torch.bfloat16).requires_grad_()
+    dy = torch.randn(T, H, device=dev, generator=g).to(torch.bfloat16)
+    lam = torch.tensor(0.01, device=dev)
+    params = [W1, W2, W3, wg, wn, x]
+
+    def step(xin, dyin):
+        for p in params:
+            p.grad = None
+        out = layer(xin)
+        aux = P.importance_penalty(out.gates)
+        torch.autograd.backward([out.output, aux], [dyin, lam])
+        return out
+
+    for _ in range(max(args.warmup, 3)):
+        out = step(x, dy)
+    torch.cuda.synchronize()
+    S = int(out.routing["recv_counts"].sum().item())
+    prof = _lib.Profiler(events=False)
+    _lib.PROFILER = prof
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with B.ClockSampler(dev.index) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            step(x, dy)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    _lib.PROFILER = None
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms, float(S)], device=dev, dtype=torch.float64)
+    tmax = t.clone()
+    dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+    ssum = t[1:].clone()
+    dist.all_reduce(ssum, op=dist.ReduceOp.SUM)
+    ms_max = float(tmax[0])
+    S_tot = float(ssum[0])
+
+    # e2e: host-resident x / dy copied in, aux loss read back, every step
+    xh = x.detach().cpu().pin_memory()
+    dyh = dy.cpu().pin_memory()
+    res_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    xd, dyd = torch.empty_like(x), torch.empty_like(dy)
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        dyd.copy_(dyh, non_blocking=True)
+        out = step(xd.detach().requires_grad_(), dyd)
+        res_h.copy_(P.importance_penalty(out.gates).detach().reshape(1), non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_t = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    clocks = clk.summary()
+    if rank == 0:
+        tps = world * T / (ms_max * 1e-3)
+        flops = 18.0 * H * F * S_tot + 6.0 * world * T * H * E
+        peak = measured["bf16_tflops"]
+        line = {
+            "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 1), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "Llama-3-8B-shape E8T2 MoE layer fwd+bwd, expert parallel (configs[2])",
+                       "hidden": H, "ffn": F, "experts": E, "top_k": K, "tokens_per_gpu": T,
+                       "capacity_factor": args.cf, "router": args.router, "drop_policy": args.policy,
+                       "kept_slots_total": int(S_tot), "parallelism": f"ep{world}",
+                       "comm": "NCCL all_to_all_single (equal splits, fixed capacity segments) + all_reduce(dW_g)",
+                       "l2": "working set > L2 (expert weights + activations)"},
+            "mfu": {"measured_peak": round(flops / (ms_max * 1e-3) / (world * peak * 1e12), 4),
+                    "spec_2250": round(flops / (ms_max * 1e-3) / (world * 2.25e15), 4)},
+            "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM)", "bound": "tensor", "achieved": None,
+                         "peak": peak, "unit": "TFLOP/s", "frac": None, "traffic": None},
+            "e2e": {"value": round(world * T / (float(e2e_t[0]) * 1e-3), 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": world * (xh.numel() + dyh.numel()) * 2, "d2h_bytes_per_step": 4 * world},
+            "cpu_baseline": None, "clocks": clocks, "gpu_launches": prof.launches,
+        }
+        print(json.dumps(line), flush=True)

@@ -1,0 +1,105 @@
+"""EP parity on N GPUs (torchrun --nproc-per-node N tools/ep_check.py).
+
+Every rank runs the expert-parallel layer (E/N experts, NCCL all-to-all) and
+the single-GPU layer holding all experts on the same local batch, and checks:
+routing bit-identical (gates, slot ranks), y and dx bit-identical (each row's
+math is the same kernel on the same data), expert / router gradients equal to
+the all-reduced single-GPU gradients within bf16 tolerance."""
+
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2412_09952_b200 as P  # noqa: E402
+from paper_2412_09952_b200.ep import ExpertParallelMoE  # noqa: E402
+
+
+def rel(a, b):
+    return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
+
+
+def case(rank, world, dev, T, H, F, router, policy, cf, noise):
+    E = 8
+    El = E // world
+    g = torch.Generator(device=dev).manual_seed(5)
+    W1 = (torch.randn(E, F, H, generator=g, device=dev) * 0.05).to(torch.bfloat16)
+    W2 = (torch.randn(E, H, F, generator=g, device=dev) * 0.05).to(torch.bfloat16)
+    W3 = (torch.randn(E, F, H, generator=g, device=dev) * 0.05).to(torch.bfloat16)
+    wg = torch.randn(H, E, generator=g, device=dev) * 0.05
+    wn = torch.randn(H, E, generator=g, device=dev) * 0.02
+    gx = torch.Generator(device=dev).manual_seed(100 + rank)
+    x = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
+    dy = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
+    z = torch.randn(T, E, generator=gx, device=dev) if noise else None
+    cfg = P.GateConfig(n_experts=E, top_k=2, router_type=router, noise_enabled=noise, capacity_factor=cf,
+                       drop_policy=policy)
+    own = slice(rank * El, (rank + 1) * El)
+
+    # ---- expert parallel
+    lw = [t.clone().requires_grad_() for t in (wg, wn, W1[own], W2[own], W3[own])]
+    ep = ExpertParallelMoE(*lw, cfg)
+    xe = x.clone().requires_grad_()
+    oe = ep(xe, training=True, noise=z)
+    loss = (oe.output.float() * dy.float()).sum() + 0.1 * P.importance_penalty(oe.gates)
+    loss.backward()
+
+    # ---- single GPU, all experts, same batch
+    rw = [t.clone().requires_grad_() for t in (wg, wn, W1, W2, W3)]
+    layer = P.MoELayer.from_stacked(P.RouterParams(rw[0], rw[1]), rw[2], rw[3], rw[4])
+    xr = x.clone().requires_grad_()
+    orf = P.moe_forward(xr, layer, cfg, training=True, noise=z)
+    loss = (orf.output.float() * dy.float()).sum() + 0.1 * P.importance_penalty(orf.gates)
+    loss.backward()
+    torch.cuda.synchronize()
+
+    ok = True
+    msgs = []
+    def check(name, cond):
+        nonlocal ok
+        if not cond:
+            ok = False
+            msgs.append(name)
+
+    check("gates", torch.equal(oe.gates, orf.gates))
+    check("slot_rank", torch.equal(oe.routing["slot_rank"], orf.routing["slot_rank"]))
+    check("y", torch.equal(oe.output, orf.output))
+    check("dx", rel(xe.grad, xr.grad) < 1e-2)
+    for i, name in ((2, "dW1"), (3, "dW2"), (4, "dW3")):
+        ref = rw[i].grad.float().clone()
+        dist.all_reduce(ref)
+        check(name, rel(lw[i].grad.float(), ref[own]) < 2e-2)
+    refg = rw[0].grad.clone()
+    dist.all_reduce(refg)
+    check("dW_g", rel(lw[0].grad, refg) < 2e-2)
+    if noise:
+        refn = rw[1].grad.clone()
+        dist.all_reduce(refn)
+        check("dW_noise", rel(lw[1].grad, refn) < 2e-2)
+    tag = f"T={T} H={H} F={F} {router} {policy} cf={cf} noise={noise}"
+    print(f"rank {rank}: {'PASS' if ok else 'FAIL ' + ','.join(msgs)} {tag}", flush=True)
+    return ok
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    ok = True
+    for args in [(1024, 512, 768, "mixtral", "position", 1.0, False),
+                 (1000, 512, 512, "st", "score", 2.0, True),
+                 (512, 256, 512, "mixtral", "position", None, False),
+                 (2048, 1024, 1024, "mixtral", "position", 0.5, False)]:
+        ok &= case(rank, world, dev, *args)
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    dist.destroy_process_group()
+    sys.exit(int(flag.item() != 0))
+
+
+if __name__ == "__main__":
+    main()
