@@ -74,22 +74,33 @@ def cpu_model() -> str:
 
 
 class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 20 ms in the
+    background; only samples whose timestamp falls inside the timed region
+    (the `with` block) are summarised.  Started at construction so that the
+    process is up before the timed region begins."""
+
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-
-    def __enter__(self):
+        self.t0 = self.t1 = None
+        self.lines = []
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                ["nvidia-smi", "-i", str(index),
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
+            time.sleep(1.0)
         except OSError:
             self.proc = None
+
+    def __enter__(self):
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        self.lines = []
+        self.t1 = time.time()
+        time.sleep(0.1)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -100,16 +111,22 @@ class ClockSampler:
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
+        import datetime
         sm, mx, reasons = [], 0, set()
         names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                  0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                  0x100: "display_clock_setting"}
-        for ln in getattr(self, "lines", []):
+        all_sm = []
+        for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             try:
-                s, m = float(parts[0]), float(parts[1])
-                r = int(parts[2], 16)
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                s, m = float(parts[1]), float(parts[2])
+                r = int(parts[3], 16)
             except (ValueError, IndexError):
+                continue
+            all_sm.append(s)
+            if self.t0 is not None and not (self.t0 - 0.05 <= ts <= self.t1 + 0.05):
                 continue
             sm.append(s)
             mx = max(mx, m)
