@@ -187,6 +187,56 @@ def layer_flops(T: int, S: int) -> float:
     return 18.0 * H * F * S + 6.0 * T * H * E
 
 
+def run_e2e(steps, T, x, dy, step):
+    """End-to-end through the public API: every step copies its inputs (x, dy)
+    from pinned host memory and reads the aux loss back.  The H2D copies of
+    step i+1 run on a copy stream while step i computes (double-buffered), as a
+    training loop's data prefetch would; every copy is inside the timed region."""
+    import torch
+    xh = x.detach().cpu().pin_memory()
+    dyh = dy.cpu().pin_memory()
+    res_h = torch.empty(steps + 2, dtype=torch.float32).pin_memory()
+    bufs = [(torch.empty_like(x), torch.empty_like(dy)) for _ in range(2)]
+    cs = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    for ev in consumed:
+        ev.record(main)
+
+    def prefetch(i):
+        b = i % 2
+        with torch.cuda.stream(cs):
+            cs.wait_event(consumed[b])
+            bufs[b][0].copy_(xh, non_blocking=True)
+            bufs[b][1].copy_(dyh, non_blocking=True)
+            copied[b].record(cs)
+
+    def run(n):
+        prefetch(0)
+        for i in range(n):
+            if i + 1 < n:
+                prefetch(i + 1)
+            b = i % 2
+            main.wait_event(copied[b])
+            out, aux = step(bufs[b][0].detach().requires_grad_(), bufs[b][1])
+            consumed[b].record(main)
+            res_h[i:i + 1].copy_(aux.detach().reshape(1), non_blocking=True)
+
+    run(2)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    run(steps)
+    e1.record(main)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / steps
+    return {"value": round(T / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
+            "h2d_bytes_per_step": xh.numel() * 2 + dyh.numel() * 2, "d2h_bytes_per_step": 4,
+            "ms_per_step": round(e2e_ms, 4), "h2d": "pinned host, copy stream double-buffered one step ahead"}
+
+
 def run_single(args, dev):
     import torch
     import paper_2412_09952_b200 as B
@@ -257,34 +307,7 @@ def run_single(args, dev):
     # ---- e2e: through the public API with pinned host buffers, H2D + D2H inside
     e2e = None
     if not args.no_e2e:
-        xh = x.detach().cpu().pin_memory()
-        dyh = dy.cpu().pin_memory()
-        res_h = torch.empty(2, dtype=torch.float32).pin_memory()
-        xd = torch.empty_like(x)
-        dyd = torch.empty_like(dy)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-
-        def e2e_step():
-            xd.copy_(xh, non_blocking=True)
-            dyd.copy_(dyh, non_blocking=True)
-            xin = xd.detach().requires_grad_()
-            out, aux = step(xin, dyd)
-            res_h[0:1].copy_(aux.detach().reshape(1), non_blocking=True)
-            return out
-
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record()
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / args.steps
-        e2e = {"value": round(T / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
-               "h2d_bytes_per_step": xh.numel() * 2 + dyh.numel() * 2, "d2h_bytes_per_step": 4,
-               "ms_per_step": round(e2e_ms, 4)}
+        e2e = run_e2e(args.steps, T, x, dy, step)
 
     # ---- CPU baseline (oracle port) on a bounded sample, rank 0 / N=1 only
     cpu = None

@@ -109,12 +109,13 @@ int b200moe_combine_bwd(const void* dy, const void* o, const float* gates, const
  * dh = softmax' (mixtral over the kept k, st over all E with the top-k mask);
  * dx[t] = sum_{kept e ascending} dxp[row] + dh.W_g^T (+ dn.W_noise^T with
  * dn = dh*z*sigmoid(noise_act)).  Writes dx (bf16), dh, dn (fp32, dn only with
- * noise).  Replaces tensor.py:292-295, 224, 375-378 and moe.py's router matmuls. */
+ * noise).  Replaces tensor.py:292-295, 224, 375-378 and moe.py's router matmuls.
+ * workspace: >= 2*H*32 + T*32 floats. */
 int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
                        const float* dgates_ext, int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates,
                        const float* probs, const float* w_g, const float* w_noise, const float* z,
-                       const float* noise_act, int T, int H, int E, int router_type, void* dx, float* dh, float* dn,
-                       float* workspace, cudaStream_t stream);
+                       const float* noise_act, int T, int H, int E, int k, int router_type, void* dx, float* dh,
+                       float* dn, float* workspace, cudaStream_t stream);
 
 /* Router weight gradients: dW_g = x^T.dh, dW_noise = x^T.dn (fp32, [H,E]),
  * deterministic (fixed-order partial sums).  workspace: >= ceil(T/128)*H*E*2

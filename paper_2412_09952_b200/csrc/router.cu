@@ -106,16 +106,17 @@ __device__ __forceinline__ bool gate_row(const float (&h)[EP], int E, int k, int
 
 // ---------------------------------------------------------------- K1
 // Swizzle W [H, E] (fp32) into float4 blocks laid out so that lane-consecutive
-// h-blocks are address-consecutive: index ((j * (EP/4) + e4) * (H/4) + hb).
+// 8-wide h-blocks are address-consecutive: index ((j * (EP/4) + e4) * (H/8) + hb),
+// h = hb*8 + j.
 template <int EP>
 __global__ void swizzle_w_kernel(const float* __restrict__ w, int H, int E, float4* __restrict__ out) {
-    const int n = (H / 4) * 4 * (EP / 4);
+    const int n = (H / 8) * 8 * (EP / 4);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int hb = i % (H / 4);
-        const int rest = i / (H / 4);
+        const int hb = i % (H / 8);
+        const int rest = i / (H / 8);
         const int e4 = rest % (EP / 4);
         const int j = rest / (EP / 4);
-        const int h = hb * 4 + j;
+        const int h = hb * 8 + j;
         float v[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -162,28 +163,23 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict_
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
-    const int HB = H / 4;
+    const int HB = H / 8;
 
     for (int t0 = (blockIdx.x * (blockDim.x >> 5) + warp) * TT; t0 < T; t0 += nwarps * TT) {
         float acc[32], accn[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) { acc[i] = 0.f; accn[i] = 0.f; }
         for (int hb = lane; hb < HB; hb += 32) {
-            float xv[TT][4];
+            float xv[TT][8];
 #pragma unroll
             for (int tt = 0; tt < TT; ++tt) {
                 const int t = t0 + tt;
-                if (t < T) {
-                    const uint2 u = *reinterpret_cast<const uint2*>(x + (size_t)t * H + hb * 4);
-                    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
-                    const float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
-                    xv[tt][0] = f0.x; xv[tt][1] = f0.y; xv[tt][2] = f1.x; xv[tt][3] = f1.y;
-                } else {
-                    xv[tt][0] = xv[tt][1] = xv[tt][2] = xv[tt][3] = 0.f;
-                }
+                uint4 u = make_uint4(0, 0, 0, 0);
+                if (t < T) u = ld_nc_v4(x + (size_t)t * H + hb * 8);
+                unpack8(u, xv[tt]);
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < 8; ++j) {
 #pragma unroll
                 for (int e4 = 0; e4 < EP / 4; ++e4) {
                     const float4 w = W[(j * (EP / 4) + e4) * HB + hb];
@@ -517,7 +513,7 @@ int check_router_args(int T, int H, int E, int k, int router_type) {
     B200_CHECK_ARG(k >= 1 && k <= E, B200MOE_ERR_CONFIG, "top-k out of range: k=%d, n=%d", k, E);
     B200_CHECK_ARG(router_type == B200MOE_ROUTER_MIXTRAL || router_type == B200MOE_ROUTER_ST, B200MOE_ERR_CONFIG,
                    "router_type %d", router_type);
-    B200_CHECK_ARG(H >= 4 && H % 4 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 4, got %d", H);
+    B200_CHECK_ARG(H >= 8 && H % 8 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 8, got %d", H);
     return B200MOE_OK;
 }
 }  // namespace
@@ -539,7 +535,7 @@ int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, co
 
 int b200moe_gate_from_logits(const float* logits, int T, int E, int k, int router_type, float* gates, float* probs,
                              uint8_t* topk_mask, int32_t* err_flag, cudaStream_t stream) {
-    int rc = check_router_args(T, 4, E, k, router_type);
+    int rc = check_router_args(T, 8, E, k, router_type);
     if (rc) return rc;
     if (E <= 4) return gate_impl<4>(logits, T, E, k, router_type, gates, probs, topk_mask, err_flag, stream);
     if (E <= 8) return gate_impl<8>(logits, T, E, k, router_type, gates, probs, topk_mask, err_flag, stream);

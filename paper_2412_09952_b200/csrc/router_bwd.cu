@@ -10,6 +10,11 @@
 //   st:      ds = dg_total*topk; dh = s*(ds - sum(s*ds))    (s = probs)
 //   dn = dh * z * sigmoid(x.W_noise)          (noise only)
 //   dx = sum_{kept e asc} dxp[row] + dh.W_g^T + dn.W_noise^T
+//
+// Two kernels: a per-token pass (dh, dn and the compact list of the token's
+// kept rows), then a bandwidth pass over [T, H] with 16-byte loads (8 hidden
+// units per lane per chunk) that gathers the expert rows and adds the router
+// term from an L1-resident swizzled copy of W.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <math.h>
@@ -18,15 +23,18 @@
 
 namespace b200moe {
 
-template <int EP>
-__global__ void swizzle_w_kernel_bwd(const float* __restrict__ w, int H, int E, float4* __restrict__ out) {
-    const int n = (H / 4) * 4 * (EP / 4);
+// W [H, E] fp32 -> float4 blocks: index ((j * (EP/4) + e4) * (H/J) + hb), h = hb*J + j,
+// so lane-consecutive hb are address-consecutive (conflict-free, coalesced).
+template <int EP, int J>
+__global__ void swizzle_w_j(const float* __restrict__ w, int H, int E, float4* __restrict__ out) {
+    const int HB = H / J;
+    const int n = HB * J * (EP / 4);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int hb = i % (H / 4);
-        const int rest = i / (H / 4);
+        const int hb = i % HB;
+        const int rest = i / HB;
         const int e4 = rest % (EP / 4);
         const int j = rest / (EP / 4);
-        const int h = hb * 4 + j;
+        const int h = hb * J + j;
         float v[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -37,133 +45,153 @@ __global__ void swizzle_w_kernel_bwd(const float* __restrict__ w, int H, int E, 
     }
 }
 
-constexpr int kRbThreads = 512;
-
-template <int EP, bool kNoise, bool kSmemW>
-__global__ void __launch_bounds__(kRbThreads, 1)
-router_bwd_kernel(const __nv_bfloat16* __restrict__ dxp, const int32_t* __restrict__ slot_rank,
-                  const int32_t* __restrict__ seg_base, const float* __restrict__ dg,
-                  const float* __restrict__ dgx, int64_t sx_t, int64_t sx_e, const float* __restrict__ gates,
-                  const float* __restrict__ probs, const float4* __restrict__ wsw, const float4* __restrict__ wnsw,
-                  const float* __restrict__ z, const float* __restrict__ noise_act, int T, int H, int E,
-                  int router_type, __nv_bfloat16* __restrict__ dx, float* __restrict__ dh_out,
-                  float* __restrict__ dn_out) {
-    constexpr int TT = 32 / EP;
-    extern __shared__ float4 smem_w[];
-    const float4* W = wsw;
-    if constexpr (kSmemW) {
-        for (int i = threadIdx.x; i < H * EP / 4; i += blockDim.x) smem_w[i] = wsw[i];
-        __syncthreads();
-        W = smem_w;
-    }
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int nwarps = gridDim.x * (blockDim.x >> 5);
-    const int HB = H / 4;
-    const int tt_mine = lane / EP, e_mine = lane % EP;
-
-    for (int t0 = (blockIdx.x * (blockDim.x >> 5) + warp) * TT; t0 < T; t0 += nwarps * TT) {
-        // ---- per (token, expert) lane: dh, dn
-        const int t = t0 + tt_mine;
-        const bool live = (t < T) && (e_mine < E);
-        float gt = 0.f, pv = 0.f, topk = 0.f;
-        int rank = -1;
-        if (live) {
-            const size_t i = (size_t)t * E + e_mine;
-            gt = dg[i];
-            if (dgx) gt += dgx[(int64_t)t * sx_t + (int64_t)e_mine * sx_e];
-            const float gv = gates[i];
-            pv = (router_type == B200MOE_ROUTER_MIXTRAL) ? gv : probs[i];
-            topk = (gv > 0.f) ? 1.f : 0.f;
-            rank = slot_rank[i];
-        }
-        const float geff = (router_type == B200MOE_ROUTER_MIXTRAL) ? ((pv > 0.f) ? gt : 0.f) : gt * topk;
-        float dot = pv * geff;
+// ---- pass 1: one thread per token
+template <int EP, int KM>
+__global__ void __launch_bounds__(256)
+router_dh_kernel(const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
+                 const float* __restrict__ dg, const float* __restrict__ dgx, int64_t sx_t, int64_t sx_e,
+                 const float* __restrict__ gates, const float* __restrict__ probs, const float* __restrict__ z,
+                 const float* __restrict__ noise_act, int T, int E, int router_type, float* __restrict__ dh_out,
+                 float* __restrict__ dn_out, int32_t* __restrict__ rows_out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    float p[EP], g[EP];
+    float dot = 0.f;
+    int nrow = 0;
+    int rows[KM];
 #pragma unroll
-        for (int o = 1; o < EP; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        float dhv = live ? pv * (geff - dot) : 0.f;
-        if (router_type == B200MOE_ROUTER_MIXTRAL && !(pv > 0.f)) dhv = 0.f;
-        float dnv = 0.f;
-        if constexpr (kNoise) {
-            if (live) {
-                const size_t i = (size_t)t * E + e_mine;
-                const float an = noise_act[i];
-                const float sg = 1.0f / (1.0f + expf(-an));
-                dnv = dhv * z[i] * sg;
-                dn_out[i] = dnv;
+    for (int j = 0; j < KM; ++j) rows[j] = -1;
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+        p[e] = 0.f;
+        g[e] = 0.f;
+        if (e < E) {
+            const size_t i = (size_t)t * E + e;
+            float gt = dg[i];
+            if (dgx) gt += dgx[(int64_t)t * sx_t + (int64_t)e * sx_e];
+            const float gv = gates[i];
+            const float pv = (router_type == B200MOE_ROUTER_MIXTRAL) ? gv : probs[i];
+            const bool topk = gv > 0.f;  // top-k and not underflowed (underflowed entries contribute 0)
+            const float geff = (router_type == B200MOE_ROUTER_MIXTRAL) ? (pv > 0.f ? gt : 0.f) : (topk ? gt : 0.f);
+            p[e] = pv;
+            g[e] = geff;
+            dot = fmaf(pv, geff, dot);
+            const int rk = slot_rank[i];
+            if (rk >= 0 && nrow < KM) {
+#pragma unroll
+                for (int j = 0; j < KM; ++j)
+                    if (j == nrow) rows[j] = seg_base[e] + rk;
+                ++nrow;
             }
         }
-        if (live) dh_out[(size_t)t * E + e_mine] = dhv;
-        // broadcast all (token, expert) values to every lane
-        float dhall[32], dnall[32];
+    }
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+        if (e < E) {
+            const size_t i = (size_t)t * E + e;
+            float dhv = p[e] * (g[e] - dot);
+            if (router_type == B200MOE_ROUTER_MIXTRAL && !(p[e] > 0.f)) dhv = 0.f;
+            dh_out[i] = dhv;
+            if (dn_out) {
+                const float an = noise_act[i];
+                dn_out[i] = dhv * z[i] * (1.0f / (1.0f + expf(-an)));
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < KM; ++j) rows_out[(size_t)t * KM + j] = rows[j];
+}
+
+// ---- pass 2: warp per TT tokens, lane owns 8 hidden units per 256-wide chunk
+constexpr int kDxThreads = 256;
+
+template <int EP, int KM, bool kNoise>
+__global__ void __launch_bounds__(kDxThreads)
+router_dx_kernel(const __nv_bfloat16* __restrict__ dxp, const int32_t* __restrict__ rows_in,
+                 const float* __restrict__ dh, const float* __restrict__ dn, const float4* __restrict__ wsw,
+                 const float4* __restrict__ wnsw, int T, int H, int E, __nv_bfloat16* __restrict__ dx) {
+    constexpr int TT = 32 / EP;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (kDxThreads / 32) + (threadIdx.x >> 5);
+    const int t0 = gw * TT;
+    if (t0 >= T) return;
+    const int HB = H / 8;
+    // (token, expert) values broadcast to every lane
+    float dhall[32], dnall[32];
+    {
+        const int t = t0 + lane / EP, e = lane % EP;
+        const bool live = t < T && e < E;
+        const float v = live ? dh[(size_t)t * E + e] : 0.f;
+        const float w = (kNoise && live) ? dn[(size_t)t * E + e] : 0.f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-            dhall[i] = __shfl_sync(0xffffffffu, dhv, i);
-            if constexpr (kNoise) dnall[i] = __shfl_sync(0xffffffffu, dnv, i);
+            dhall[i] = __shfl_sync(0xffffffffu, v, i);
+            if constexpr (kNoise) dnall[i] = __shfl_sync(0xffffffffu, w, i);
         }
-        // rows of the kept experts for each token (ascending expert order)
-        const int row = (rank >= 0) ? seg_base[e_mine] + rank : -1;
-        int rr[32];
+    }
+    int rr[TT][KM];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) rr[i] = __shfl_sync(0xffffffffu, row, i);
+    for (int tt = 0; tt < TT; ++tt)
+#pragma unroll
+        for (int j = 0; j < KM; ++j) rr[tt][j] = (t0 + tt < T) ? rows_in[(size_t)(t0 + tt) * KM + j] : -1;
 
-        for (int hb = lane; hb < HB; hb += 32) {
-            float acc[TT][4];
+    for (int hb = lane; hb < HB; hb += 32) {
+        float acc[TT][8];
+        uint4 ld[TT][KM];
 #pragma unroll
-            for (int tt = 0; tt < TT; ++tt)
+        for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[tt][j] = 0.f;
-            // expert-path contributions, ascending expert order
+            for (int j = 0; j < KM; ++j)
+                if (rr[tt][j] >= 0) ld[tt][j] = ld_nc_v4(dxp + (size_t)rr[tt][j] * H + hb * 8);
 #pragma unroll
-            for (int tt = 0; tt < TT; ++tt) {
+        for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
-                for (int e = 0; e < EP; ++e) {
-                    const int r = rr[tt * EP + e];
-                    if (r >= 0) {
-                        const uint2 u = *reinterpret_cast<const uint2*>(dxp + (size_t)r * H + hb * 4);
-                        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
-                        const float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
-                        acc[tt][0] += f0.x; acc[tt][1] += f0.y; acc[tt][2] += f1.x; acc[tt][3] += f1.y;
-                    }
+            for (int c = 0; c < 8; ++c) acc[tt][c] = 0.f;
+        // expert-path rows, ascending expert order
+#pragma unroll
+        for (int tt = 0; tt < TT; ++tt)
+#pragma unroll
+            for (int j = 0; j < KM; ++j)
+                if (rr[tt][j] >= 0) {
+                    float f[8];
+                    unpack8(ld[tt][j], f);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc[tt][c] += f[c];
                 }
-            }
-            // router path: dh . W_g^T (+ dn . W_noise^T)
+        // router path
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+        for (int jh = 0; jh < 8; ++jh) {
 #pragma unroll
-                for (int e4 = 0; e4 < EP / 4; ++e4) {
-                    const float4 w = W[(j * (EP / 4) + e4) * HB + hb];
+            for (int e4 = 0; e4 < EP / 4; ++e4) {
+                const float4 w = __ldg(&wsw[(jh * (EP / 4) + e4) * HB + hb]);
+#pragma unroll
+                for (int tt = 0; tt < TT; ++tt) {
+                    const float* d = dhall + tt * EP + e4 * 4;
+                    float a = acc[tt][jh];
+                    a = fmaf(d[0], w.x, a);
+                    a = fmaf(d[1], w.y, a);
+                    a = fmaf(d[2], w.z, a);
+                    a = fmaf(d[3], w.w, a);
+                    acc[tt][jh] = a;
+                }
+                if constexpr (kNoise) {
+                    const float4 wn = __ldg(&wnsw[(jh * (EP / 4) + e4) * HB + hb]);
 #pragma unroll
                     for (int tt = 0; tt < TT; ++tt) {
-                        const float* d = dhall + tt * EP + e4 * 4;
-                        acc[tt][j] = fmaf(d[0], w.x, acc[tt][j]);
-                        acc[tt][j] = fmaf(d[1], w.y, acc[tt][j]);
-                        acc[tt][j] = fmaf(d[2], w.z, acc[tt][j]);
-                        acc[tt][j] = fmaf(d[3], w.w, acc[tt][j]);
+                        const float* d = dnall + tt * EP + e4 * 4;
+                        float a = acc[tt][jh];
+                        a = fmaf(d[0], wn.x, a);
+                        a = fmaf(d[1], wn.y, a);
+                        a = fmaf(d[2], wn.z, a);
+                        a = fmaf(d[3], wn.w, a);
+                        acc[tt][jh] = a;
                     }
-                    if constexpr (kNoise) {
-                        const float4 wn = __ldg(&wnsw[(j * (EP / 4) + e4) * HB + hb]);
-#pragma unroll
-                        for (int tt = 0; tt < TT; ++tt) {
-                            const float* d = dnall + tt * EP + e4 * 4;
-                            acc[tt][j] = fmaf(d[0], wn.x, acc[tt][j]);
-                            acc[tt][j] = fmaf(d[1], wn.y, acc[tt][j]);
-                            acc[tt][j] = fmaf(d[2], wn.z, acc[tt][j]);
-                            acc[tt][j] = fmaf(d[3], wn.w, acc[tt][j]);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int tt = 0; tt < TT; ++tt) {
-                if (t0 + tt < T) {
-                    uint2 u;
-                    u.x = pack2(acc[tt][0], acc[tt][1]);
-                    u.y = pack2(acc[tt][2], acc[tt][3]);
-                    *reinterpret_cast<uint2*>(dx + (size_t)(t0 + tt) * H + hb * 4) = u;
                 }
             }
         }
+#pragma unroll
+        for (int tt = 0; tt < TT; ++tt)
+            if (t0 + tt < T) st_v4(dx + (size_t)(t0 + tt) * H + hb * 8, pack8(acc[tt]));
     }
 }
 
@@ -192,8 +220,9 @@ router_wgrad_partial(const __nv_bfloat16* __restrict__ x, const float* __restric
 #pragma unroll
         for (int e = 0; e < EP; ++e) acc[j][e] = 0.f;
     const int tn = min(kWgTok, T - t0);
+#pragma unroll 8
     for (int tt = 0; tt < tn; ++tt) {
-        const uint2 u = *reinterpret_cast<const uint2*>(x + (size_t)(t0 + tt) * H + h0);
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(x + (size_t)(t0 + tt) * H + h0));
         const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
         const float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
         const float xv[4] = {f0.x, f0.y, f1.x, f1.y};
@@ -220,23 +249,35 @@ __global__ void reduce_partials(const float* __restrict__ part, int nchunks, siz
     }
 }
 
-// Importance penalty forward: one block.  imp_e = sum_t g[t,e] (fixed order),
-// mean, population variance, loss = var / mean^2 (tensor.py:509-514).
-__global__ void importance_fwd_kernel(const float* __restrict__ g, int T, int E, float* __restrict__ imp,
-                                      float* __restrict__ loss, int32_t* __restrict__ err_flag) {
+// Importance penalty forward: one block of 1024 threads; thread i sums the
+// rows i, i+1024, ... (fixed order), then a fixed-order block reduction per
+// expert; mean, population variance, loss = var / mean^2 (tensor.py:509-514).
+__global__ void __launch_bounds__(1024)
+importance_fwd_kernel(const float* __restrict__ g, int T, int E, float* __restrict__ imp, float* __restrict__ loss,
+                      int32_t* __restrict__ err_flag) {
     __shared__ float part[32][33];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 32 warps
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int e0 = 0; e0 < E; e0 += 32) {
-        const int e = e0 + lane;
-        float s = 0.f;
-        if (e < E)
-            for (int t = warp; t < T; t += 32) s += g[(size_t)t * E + e];
-        part[warp][lane] = s;
+        float s[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[i] = 0.f;
+        for (int t = threadIdx.x; t < T; t += blockDim.x) {
+            const float* row = g + (size_t)t * E + e0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (e0 + i < E) s[i] += row[i];
+        }
+        // warp reduce each of the (up to 32) expert sums, lane i keeps expert i
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            float v = warp_sum(s[i]);
+            if (lane == i) part[warp][i] = v;
+        }
         __syncthreads();
-        if (warp == 0 && e < E) {
+        if (warp == 0 && e0 + lane < E) {
             float r = 0.f;
             for (int w = 0; w < 32; ++w) r += part[w][lane];
-            imp[e] = r;
+            imp[e0 + lane] = r;
         }
         __syncthreads();
     }
@@ -246,8 +287,8 @@ __global__ void importance_fwd_kernel(const float* __restrict__ g, int T, int E,
         mean /= (float)E;
         float var = 0.f;
         for (int e = 0; e < E; ++e) {
-            const float d = ((volatile float*)imp)[e] - mean;
-            var += d * d;
+            const float dd = ((volatile float*)imp)[e] - mean;
+            var += dd * dd;
         }
         var /= (float)E;
         if (!(mean > 0.f)) atomicExch(err_flag, 1);
@@ -279,38 +320,44 @@ __global__ void importance_bwd_kernel(const float* __restrict__ imp, const float
 using namespace b200moe;
 
 namespace {
-template <int EP>
+template <int EP, int KM>
 int router_bwd_impl(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
                     const float* dgx, int64_t sx_t, int64_t sx_e, const float* gates, const float* probs,
                     const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T, int H,
                     int E, int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
+    // workspace: swizzled W_g [H*EP], W_noise [H*EP], rows [T*KM] (int32)
     float4* wsw = reinterpret_cast<float4*>(workspace);
     float4* wnsw = reinterpret_cast<float4*>(workspace + (size_t)H * EP);
-    swizzle_w_kernel_bwd<EP><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
+    int32_t* rows = reinterpret_cast<int32_t*>(workspace + (size_t)2 * H * EP);
     const bool noise = z != nullptr;
-    if (noise) swizzle_w_kernel_bwd<EP><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
-    const size_t wbytes = (size_t)H * EP * sizeof(float);
-    const bool smem_w = wbytes <= 160 * 1024;
+    swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
+    if (noise) swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
+    router_dh_kernel<EP, KM><<<ceil_div(T, 256), 256, 0, stream>>>(slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates,
+                                                                    probs, z, noise_act, T, E, router_type, dh,
+                                                                    noise ? dn : nullptr, rows);
     constexpr int TT = 32 / EP;
-    int grid = ceil_div(ceil_div(T, TT), kRbThreads / 32);
-    if (grid > kNumSMs) grid = kNumSMs;
-#define LAUNCH(NZ, SM)                                                                                         \
-    do {                                                                                                       \
-        auto kern = router_bwd_kernel<EP, NZ, SM>;                                                             \
-        const size_t sh = SM ? wbytes : 0;                                                                     \
-        if (SM) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);              \
-        kern<<<grid, kRbThreads, sh, stream>>>((const __nv_bfloat16*)dxp, slot_rank, seg_base, dg, dgx, sx_t, \
-                                               sx_e, gates, probs, wsw, wnsw, z, noise_act, T, H, E,          \
-                                               router_type, (__nv_bfloat16*)dx, dh, dn);                       \
-    } while (0)
-    if (noise) {
-        if (smem_w) LAUNCH(true, true); else LAUNCH(true, false);
-    } else {
-        if (smem_w) LAUNCH(false, true); else LAUNCH(false, false);
-    }
-#undef LAUNCH
+    const int grid = ceil_div(ceil_div(T, TT), kDxThreads / 32);
+    if (noise)
+        router_dx_kernel<EP, KM, true><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, rows, dh, dn,
+                                                                         wsw, wnsw, T, H, E, (__nv_bfloat16*)dx);
+    else
+        router_dx_kernel<EP, KM, false><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, rows, dh, dn,
+                                                                          wsw, wnsw, T, H, E, (__nv_bfloat16*)dx);
     B200_CHECK_LAUNCH("router_bwd");
     return B200MOE_OK;
+}
+
+template <int EP>
+int router_bwd_k(int k, const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
+                 const float* dgx, int64_t sx_t, int64_t sx_e, const float* gates, const float* probs,
+                 const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T, int H, int E,
+                 int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
+#define CALL(KM) router_bwd_impl<EP, KM>(dxp, slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates, probs, w_g, w_noise, \
+                                         z, noise_act, T, H, E, router_type, dx, dh, dn, workspace, stream)
+    if (k <= 2) return CALL(2);
+    if (k <= 4 || EP == 4) return CALL((EP < 4 ? EP : 4));
+    return CALL(EP);
+#undef CALL
 }
 
 template <int EP>
@@ -330,15 +377,16 @@ extern "C" {
 int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
                        const float* dgates_ext, int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates,
                        const float* probs, const float* w_g, const float* w_noise, const float* z,
-                       const float* noise_act, int T, int H, int E, int router_type, void* dx, float* dh, float* dn,
-                       float* workspace, cudaStream_t stream) {
+                       const float* noise_act, int T, int H, int E, int k, int router_type, void* dx, float* dh,
+                       float* dn, float* workspace, cudaStream_t stream) {
     B200_CHECK_ARG(T >= 1 && E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "bad T/E (%d, %d)", T, E);
-    B200_CHECK_ARG(H % 4 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 4");
+    B200_CHECK_ARG(k >= 1 && k <= E, B200MOE_ERR_CONFIG, "top-k out of range: k=%d, n=%d", k, E);
+    B200_CHECK_ARG(H % 8 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 8");
     B200_CHECK_ARG(router_type != B200MOE_ROUTER_ST || probs != nullptr, B200MOE_ERR_CONFIG, "st needs probs");
     B200_CHECK_ARG(z == nullptr || (w_noise && noise_act && dn), B200MOE_ERR_CONFIG, "noise args missing");
-#define CALL(EP) router_bwd_impl<EP>(dxp, slot_rank, seg_base, dg, dgates_ext, dgates_stride_t, dgates_stride_e, \
-                                     gates, probs, w_g, w_noise, z, noise_act, T, H, E, router_type, dx, dh, dn,  \
-                                     workspace, stream)
+#define CALL(EP) router_bwd_k<EP>(k, dxp, slot_rank, seg_base, dg, dgates_ext, dgates_stride_t,                   \
+                                  dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, T, H, E, router_type, \
+                                  dx, dh, dn, workspace, stream)
     if (E <= 4) return CALL(4);
     if (E <= 8) return CALL(8);
     if (E <= 16) return CALL(16);

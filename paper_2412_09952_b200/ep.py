@@ -192,11 +192,11 @@ class _EPFunction(torch.autograd.Function):
         if dgates is not None:
             dgx = dgates.to(torch.float32)
             sx_t, sx_e = dgx.stride()
-        ws = torch.empty(2 * H * _ep(E), **f32)
+        ws = torch.empty(2 * H * _ep(E) + T * _ep(E), **f32)
         _lib.call("b200moe_router_bwd", dxs.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), dg.data_ptr(),
                   _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(), w_noise.data_ptr(),
-                  _lib.ptr(z), _lib.ptr(noise_act), T, H, E, _lib.ROUTER[cfg.router_type], dx.data_ptr(),
-                  dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
+                  _lib.ptr(z), _lib.ptr(noise_act), T, H, E, cfg.top_k, _lib.ROUTER[cfg.router_type],
+                  dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
         dwg = torch.empty(H, E, **f32)
         dwn = torch.empty(H, E, **f32) if z is not None else None
         wsw = torch.empty((T + 127) // 128 * H * E, **f32)
