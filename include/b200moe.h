@@ -130,6 +130,9 @@ int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T,
 int b200moe_importance_fwd(const float* gates, int T, int E, float* imp, float* loss, int32_t* err_flag,
                            cudaStream_t stream);
 int b200moe_importance_bwd(const float* imp, const float* gscale, int E, float* dimp, cudaStream_t stream);
+/* Loss only, from an importance vector already reduced by b200moe_dispatch
+ * (`importance` output) for the same gates. */
+int b200moe_importance_loss(const float* imp, int E, float* loss, int32_t* err_flag, cudaStream_t stream);
 
 /* Grouped expert GEMMs on tcgen05/TMEM/TMA (see gemm.cu).  `rows` = rows of
  * the permuted activation buffers.  H and F must be multiples of 256. */

@@ -79,8 +79,11 @@ struct Cfg {
 template <int kMode, int kCG>
 struct Geo {
     static constexpr bool kTmaEpiLoads = (kMode == kBwd2) && (kCG == 2);
+    // Store-ring depth per epilogue warp (4 buffers + 5 stages measured no
+    // better than 2 + 6 for WGRAD on B200).
+    static constexpr int kRing = 2;
     static constexpr int kStages = kTmaEpiLoads ? 4 : Cfg<kCG>::kStages;
-    static constexpr int kEpiWarpBytes = kTmaEpiLoads ? 6 * 2048 : 2 * 2048;
+    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? 4 * 2048 : 0) + kRing * 2048;
     static constexpr int kSmemBytes = kStages * Cfg<kCG>::kStageBytes + kNumEpiWarps * kEpiWarpBytes +
                                       1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2);
 };
@@ -231,22 +234,23 @@ __device__ __forceinline__ void produce_kblock(const TmaSet& tm, const GemmArgs&
 }
 
 // ------------------------------------------------------------------ epilogues
-// Each epilogue warp owns a 2 x 2 KB staging ring in shared memory.  A 32-row
-// x 32-column bf16 chunk is written row-per-lane into the SWIZZLE_64B layout
-// (16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3): conflict-free)
-// and shipped with one TMA bulk tensor store, so global writes are full,
-// coalesced lines instead of 32 scattered 16-byte pieces per instruction.
+// Each epilogue warp owns a ring of kRing x 2 KB staging buffers in shared
+// memory.  A 32-row x 32-column bf16 chunk is written row-per-lane into the
+// SWIZZLE_64B layout (16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3):
+// conflict-free) and shipped with one TMA bulk tensor store, so global writes
+// are full, coalesced lines instead of 32 scattered 16-byte pieces.
 constexpr int kStageBufBytes = 2048;
 
 struct EpiRing {
-    uint8_t* base;  // this warp's two buffers
+    uint8_t* base;  // this warp's buffers
     int idx;
 };
 
+template <int kRing>
 __device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m, const float* v, int lane, int col,
                                             int row0) {
     uint8_t* buf = ring.base + ring.idx * kStageBufBytes;
-    if (lane == 0) ptx::bulk_wait_read<1>();  // the older store from this buffer has been read
+    if (lane == 0) ptx::bulk_wait_read<kRing - 1>();  // the store that last used this buffer has read it
     __syncwarp();
     uint4* rowp = reinterpret_cast<uint4*>(buf + lane * 64);
     const int sw = (lane >> 1) & 3;
@@ -258,7 +262,7 @@ __device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m,
         ptx::tma_store_2d(m, buf, col, row0);
         ptx::bulk_commit();
     }
-    ring.idx ^= 1;
+    ring.idx = (ring.idx + 1 == kRing) ? 0 : ring.idx + 1;
 }
 
 // BWD2 load ring: two buffers, each holding a 32x32 chunk of the stored `a`
@@ -312,6 +316,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                                               bool k_empty, uint64_t* tfull, uint32_t tphase, EpiRing& ring,
                                               EpiLoads& ld) {
     using C = Cfg<kCG>;
+    constexpr int kRing = Geo<kMode, kCG>::kRing;
     uint32_t r0[32], r1[32];
     float v0[32], v1[32], v2[32];
     const uint32_t lane_addr = tmem_acc + ((uint32_t)(q * 32) << 16);
@@ -333,7 +338,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v0[i] = 0.f;
             }
-            if (!(a.debug & 1)) stage_store(ring, &tm.st[smap], v0, lane, col0 + c, grow);
+            if (!(a.debug & 1)) stage_store<kRing>(ring,&tm.st[smap], v0, lane, col0 + c, grow);
         }
         return;
     } else {
@@ -367,8 +372,8 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
                     v1[i] = dm * (av * sg);
                 }
-                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
-                stage_store(ring, &tm.st[1], v1, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[1], v1, lane, col0 + c, row0);
             }
             return;
         } else if constexpr (kMode == kBwd2) {
@@ -414,8 +419,8 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
                     v1[i] = dm * (av * sg);
                 }
-                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
-                stage_store(ring, &tm.st[1], v1, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[1], v1, lane, col0 + c, row0);
             }
             return;
         }
@@ -436,9 +441,9 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v1[i] = bv;
                     v2[i] = av * sigmoidf_(av) * bv;
                 }
-                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
-                stage_store(ring, &tm.st[1], v1, lane, col0 + c, row0);
-                stage_store(ring, &tm.st[2], v2, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[1], v1, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[2], v2, lane, col0 + c, row0);
             }
         } else {  // kFwd2 / kBwd1: plain bf16 store
             const int col0 = ti.n_tile * kBN;
@@ -447,7 +452,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]);
-                stage_store(ring, &tm.st[0], v0, lane, col0 + c, row0);
+                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
             }
         }
     }
@@ -599,7 +604,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
         int acc = 0;
         uint32_t acc_phase = 0;
         EpiRing ring{staging + (warp - 2) * G::kEpiWarpBytes, 0};
-        EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + 2 * kStageBufBytes, ldbar + 2 * (warp - 2), 0, 0};
+        EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + G::kRing * kStageBufBytes, ldbar + 2 * (warp - 2), 0,
+                    0};
         for (int t = cid; t < sched.total; t += ncl) {
             const TileInfo ti = sched.decode(t, a);
             const bool k_empty = (kMode == kWgrad) ? (wgrad_k_blocks(a, ti.seg) == 0) : false;

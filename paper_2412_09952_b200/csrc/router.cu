@@ -169,15 +169,25 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict_
         float acc[32], accn[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) { acc[i] = 0.f; accn[i] = 0.f; }
+        // software-pipelined: the next chunk's 16-byte loads are in flight while
+        // the current chunk is multiplied
+        uint4 cur[TT];
+#pragma unroll
+        for (int tt = 0; tt < TT; ++tt)
+            cur[tt] = (lane < HB && t0 + tt < T) ? ld_nc_v4(x + (size_t)(t0 + tt) * H + lane * 8)
+                                                 : make_uint4(0, 0, 0, 0);
         for (int hb = lane; hb < HB; hb += 32) {
+            uint4 nxt[TT];
+            const int hn = hb + 32;
+#pragma unroll
+            for (int tt = 0; tt < TT; ++tt)
+                nxt[tt] = (hn < HB && t0 + tt < T) ? ld_nc_v4(x + (size_t)(t0 + tt) * H + hn * 8)
+                                                   : make_uint4(0, 0, 0, 0);
             float xv[TT][8];
 #pragma unroll
-            for (int tt = 0; tt < TT; ++tt) {
-                const int t = t0 + tt;
-                uint4 u = make_uint4(0, 0, 0, 0);
-                if (t < T) u = ld_nc_v4(x + (size_t)t * H + hb * 8);
-                unpack8(u, xv[tt]);
-            }
+            for (int tt = 0; tt < TT; ++tt) unpack8(cur[tt], xv[tt]);
+#pragma unroll
+            for (int tt = 0; tt < TT; ++tt) cur[tt] = nxt[tt];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
 #pragma unroll

@@ -244,9 +244,35 @@ router_wgrad_partial(const __nv_bfloat16* __restrict__ x, const float* __restric
 __global__ void reduce_partials(const float* __restrict__ part, int nchunks, size_t n, float* __restrict__ out) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         float s = 0.f;
-        for (int c = 0; c < nchunks; ++c) s += part[(size_t)c * n + i];
+        int c = 0;
+        for (; c + 8 <= nchunks; c += 8) {  // 8 independent loads in flight, summed in chunk order
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = __ldg(&part[(size_t)(c + j) * n + i]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s += v[j];
+        }
+        for (; c < nchunks; ++c) s += part[(size_t)c * n + i];
         out[i] = s;
     }
+}
+
+// Loss only, from a precomputed importance vector (the dispatch kernel's
+// per-expert sum of the same gates): mean, population variance, var / mean^2.
+__global__ void importance_loss_kernel(const float* __restrict__ imp, int E, float* __restrict__ loss,
+                                       int32_t* __restrict__ err_flag) {
+    if (threadIdx.x != 0) return;
+    float mean = 0.f;
+    for (int e = 0; e < E; ++e) mean += imp[e];
+    mean /= (float)E;
+    float var = 0.f;
+    for (int e = 0; e < E; ++e) {
+        const float dd = imp[e] - mean;
+        var += dd * dd;
+    }
+    var /= (float)E;
+    if (!(mean > 0.f)) atomicExch(err_flag, 1);
+    loss[0] = var / (mean * mean);
 }
 
 // Importance penalty forward: one block of 1024 threads; thread i sums the
@@ -417,6 +443,13 @@ int b200moe_importance_fwd(const float* gates, int T, int E, float* imp, float* 
     B200_CHECK_ARG(T >= 1 && E >= 1, B200MOE_ERR_SHAPE, "importance penalty needs a [T, E] gate matrix");
     importance_fwd_kernel<<<1, 1024, 0, stream>>>(gates, T, E, imp, loss, err_flag);
     B200_CHECK_LAUNCH("importance_fwd");
+    return B200MOE_OK;
+}
+
+int b200moe_importance_loss(const float* imp, int E, float* loss, int32_t* err_flag, cudaStream_t stream) {
+    B200_CHECK_ARG(E >= 1, B200MOE_ERR_SHAPE, "E >= 1");
+    importance_loss_kernel<<<1, 32, 0, stream>>>(imp, E, loss, err_flag);
+    B200_CHECK_LAUNCH("importance_loss");
     return B200MOE_OK;
 }
 

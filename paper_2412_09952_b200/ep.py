@@ -237,6 +237,7 @@ class ExpertParallelMoE:
                                      self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)
         r = st["routing"]
         from .moe import MoEForwardResult
+        gates._b200_importance = (r["importance"], gates._version)
         out = MoEForwardResult(output=y, stats=RoutingStats(r["counts"], r["stats"], r["gate_mass"], plan.capacity,
                                                             r["err"]), gates=gates)
         out.routing = r

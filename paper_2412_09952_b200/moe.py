@@ -548,6 +548,7 @@ def moe_forward(x: torch.Tensor, layer: MoELayer, cfg: GateConfig, rng: Rng | No
     if Hp != H:
         y = y[:, :H]
     r = st.routing
+    gates._b200_importance = (r["importance"], gates._version)
     stats = RoutingStats(r["counts"], r["stats"], r["gate_mass"], r["capacity"], r["err"])
     out = MoEForwardResult(output=y, stats=stats, gates=gates)
     out.routing = r  # device-side routing tensors (slot_rank, counts, logits, ...) for inspection
@@ -594,12 +595,19 @@ class _ImportanceFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, gates):
         T, E = gates.shape
-        g = gates.detach().to(torch.float32).contiguous()
-        imp = torch.empty(E, dtype=torch.float32, device=g.device)
-        loss = torch.empty(1, dtype=torch.float32, device=g.device)
-        err = torch.zeros(1, dtype=torch.int32, device=g.device)
-        _lib.call("b200moe_importance_fwd", g.data_ptr(), T, E, imp.data_ptr(), loss.data_ptr(), err.data_ptr(),
-                  _lib.stream_ptr())
+        loss = torch.empty(1, dtype=torch.float32, device=gates.device)
+        err = torch.zeros(1, dtype=torch.int32, device=gates.device)
+        cached = getattr(gates, "_b200_importance", None)
+        if cached is not None and cached[1] == gates._version:
+            # gates straight from moe_forward: the dispatch kernel already reduced them
+            imp = cached[0]
+            _lib.call("b200moe_importance_loss", imp.data_ptr(), E, loss.data_ptr(), err.data_ptr(),
+                      _lib.stream_ptr())
+        else:
+            g = gates.detach().to(torch.float32).contiguous()
+            imp = torch.empty(E, dtype=torch.float32, device=g.device)
+            _lib.call("b200moe_importance_fwd", g.data_ptr(), T, E, imp.data_ptr(), loss.data_ptr(), err.data_ptr(),
+                      _lib.stream_ptr())
         ctx.save_for_backward(imp)
         ctx.shape = (T, E)
         ctx.err = err
