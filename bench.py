@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--cpu-tokens", type=int, default=512, help="bounded CPU sample (tokens per oracle step)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                   help="EP exchange: fused NVLink peer-memory kernels (default) or NCCL all-to-all")
     return p.parse_args()
 
 

@@ -117,6 +117,32 @@ int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t*
                        const float* noise_act, int T, int H, int E, int k, int router_type, void* dx, float* dh,
                        float* dn, float* workspace, cudaStream_t stream);
 
+/* ---- Expert parallelism fused with the exchange (NVLink peer memory) ----
+ * The *_peer variants address expert e's rows in the buffer of its owner rank
+ * d = e / e_per_rank: `*_bufs` is a DEVICE array of the per-rank base pointers
+ * (symmetric memory mapped into this process), and seg_base[e] is the row of
+ * this rank's segment inside the owner's receive buffer.  permute_peer writes
+ * every kept token straight into its owner's buffer (+ zero pads) and publishes
+ * counts[e] into the owner's receive table count_bufs[d][rank*e_per_rank + e%e_per_rank];
+ * combine_peer / combine_bwd_peer / router_bwd_peer read expert outputs (and
+ * write combine gradients) in the owners' buffers.  The caller orders ranks
+ * with a device barrier between producer and consumer kernels.  These replace
+ * the NCCL all-to-alls of the dispatch / combine exchange. */
+int b200moe_permute_peer(const void* x, const int32_t* slot_rank, const int32_t* seg_base, const int32_t* counts,
+                         int T, int H, int E, int e_per_rank, int rank, const uint64_t* xp_bufs,
+                         const uint64_t* count_bufs, cudaStream_t stream);
+int b200moe_combine_peer(const uint64_t* o_bufs, int e_per_rank, const float* gates, const int32_t* slot_rank,
+                         const int32_t* seg_base, int T, int H, int E, void* y, cudaStream_t stream);
+int b200moe_combine_bwd_peer(const void* dy, const uint64_t* o_bufs, const float* gates, const int32_t* slot_rank,
+                             const int32_t* seg_base, const int32_t* counts, int T, int H, int E, int e_per_rank,
+                             const uint64_t* dout_bufs, float* dg, cudaStream_t stream);
+int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
+                            const int32_t* seg_base, const float* dg, const float* dgates_ext,
+                            int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates, const float* probs,
+                            const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T,
+                            int H, int E, int k, int router_type, void* dx, float* dh, float* dn, float* workspace,
+                            cudaStream_t stream);
+
 /* Router weight gradients: dW_g = x^T.dh, dW_noise = x^T.dn (fp32, [H,E]),
  * deterministic (fixed-order partial sums).  workspace: >= ceil(T/128)*H*E*2
  * floats. */

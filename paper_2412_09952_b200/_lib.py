@@ -36,6 +36,11 @@ SIGNATURES = {
     "b200moe_router_bwd": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P,
                            _P, _P, _P],
     "b200moe_router_wgrad": [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P],
+    "b200moe_permute_peer": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P],
+    "b200moe_combine_peer": [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P],
+    "b200moe_combine_bwd_peer": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P],
+    "b200moe_router_bwd_peer": [_P, _I, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P,
+                                _P, _P, _P, _P],
     "b200moe_importance_fwd": [_P, _I, _I, _P, _P, _P, _P],
     "b200moe_importance_bwd": [_P, _P, _I, _P, _P],
     "b200moe_importance_loss": [_P, _I, _P, _P, _P],
@@ -90,6 +95,7 @@ KERNELS_PER_CALL = {
     "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 3, "b200moe_router_wgrad": 2,
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_upcycle_copy": 3,
+    "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 3,
 }
 
 

@@ -1,10 +1,19 @@
-// Token permute (K2), weighted combine (K5) and combine backward (K6).
+// Token permute (K2), weighted combine (K5) and combine backward (K6), local
+// or fused with the expert-parallel exchange over NVLink peer memory.
 //
 // Reference: moefold/moe.py:272-282 (per expert: take_rows, ffn, multiply by the
 // gate column, put_rows, add in expert order) and the backward closures
 // tensor.py:185 (mul), :389 (put_rows), :375 (take_rows).  Every kernel is a
 // warp per token with 128-bit loads/stores; the per-token sum over its kept
 // experts runs in ascending expert order (deterministic, no atomics).
+//
+// Row addressing: expert e's rows live in buffer bufs[e / e_per_rank] at row
+// seg_base[e] + slot_rank[t, e].  Single GPU: one local buffer.  Expert
+// parallel (kPeer): bufs[d] is rank d's symmetric-memory buffer mapped into this
+// process, so the permute writes each token straight into its expert owner's
+// receive buffer and the combine reads expert outputs straight from the owner:
+// the all-to-all happens inside these kernels, overlapped with their own
+// loads and arithmetic, with no staging copies.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -14,6 +23,18 @@ namespace b200moe {
 
 constexpr int kPermThreads = 256;  // 8 warps
 constexpr int kVecPerLane = 8;     // uint4 per lane per pass (4 KB per warp pass)
+
+struct Rows {
+    __nv_bfloat16* local;   // single-GPU buffer (or nullptr)
+    const uint64_t* bufs;   // per-rank buffer bases (device array) when kPeer
+    int e_per_rank;
+
+    template <bool kPeer>
+    __device__ __forceinline__ __nv_bfloat16* base(int e) const {
+        if constexpr (kPeer) return reinterpret_cast<__nv_bfloat16*>(bufs[e / e_per_rank]);
+        else return local;
+    }
+};
 
 // Kept experts of token t (ascending) -> rows; returns the count.
 __device__ __forceinline__ int token_rows(const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
@@ -49,12 +70,18 @@ __device__ __forceinline__ void zero_pad_rows(__nv_bfloat16* buf, const int32_t*
     for (size_t i = threadIdx.x; i < nvec; i += blockDim.x) p[i] = zero;
 }
 
+template <bool kPeer>
 __global__ void __launch_bounds__(kPermThreads)
 permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ slot_rank,
                const int32_t* __restrict__ seg_base, const int32_t* __restrict__ counts, int T, int H, int E,
-               int token_blocks, __nv_bfloat16* __restrict__ xp) {
+               int token_blocks, Rows out, const uint64_t* __restrict__ count_bufs, int rank) {
     if ((int)blockIdx.x >= token_blocks) {
-        zero_pad_rows(xp, seg_base, counts, blockIdx.x - token_blocks, H);
+        const int e = blockIdx.x - token_blocks;
+        zero_pad_rows(out.base<kPeer>(e), seg_base, counts, e, H);
+        if (kPeer && threadIdx.x == 0) {  // publish this rank's count into the owner's receive table
+            const int el = e % out.e_per_rank;
+            reinterpret_cast<int32_t*>(count_bufs[e / out.e_per_rank])[rank * out.e_per_rank + el] = counts[e];
+        }
         return;
     }
     const int lane = threadIdx.x & 31;
@@ -73,7 +100,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
             if (j < nvec) v[i] = ld_nc_v4(src + j);
         }
         for (int r = 0; r < n; ++r) {
-            uint4* dst = reinterpret_cast<uint4*>(xp + (size_t)rows[r] * H);
+            uint4* dst = reinterpret_cast<uint4*>(out.base<kPeer>(experts[r]) + (size_t)rows[r] * H);
 #pragma unroll
             for (int i = 0; i < kVecPerLane; ++i) {
                 const int j = base + i * 32 + lane;
@@ -83,10 +110,10 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
     }
 }
 
+template <bool kPeer>
 __global__ void __launch_bounds__(kPermThreads)
-combine_kernel(const __nv_bfloat16* __restrict__ o, const float* __restrict__ gates,
-               const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base, int T, int H, int E,
-               __nv_bfloat16* __restrict__ y) {
+combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restrict__ slot_rank,
+               const int32_t* __restrict__ seg_base, int T, int H, int E, __nv_bfloat16* __restrict__ y) {
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * (kPermThreads / 32) + (threadIdx.x >> 5);
     if (t >= T) return;
@@ -103,12 +130,12 @@ combine_kernel(const __nv_bfloat16* __restrict__ o, const float* __restrict__ ga
 #pragma unroll
             for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
         for (int r = 0; r < n; ++r) {
-            const uint4* src = reinterpret_cast<const uint4*>(o + (size_t)rows[r] * H);
+            const uint4* src = reinterpret_cast<const uint4*>(o.base<kPeer>(experts[r]) + (size_t)rows[r] * H);
             uint4 v[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int j = base + i * 32 + lane;
-                if (j < nvec) v[i] = ld_nc_v4(src + j);
+                if (j < nvec) v[i] = kPeer ? src[j] : ld_nc_v4(src + j);
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -126,13 +153,15 @@ combine_kernel(const __nv_bfloat16* __restrict__ o, const float* __restrict__ ga
     }
 }
 
+template <bool kPeer>
 __global__ void __launch_bounds__(kPermThreads)
-combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ o,
-                   const float* __restrict__ gates, const int32_t* __restrict__ slot_rank,
-                   const int32_t* __restrict__ seg_base, const int32_t* __restrict__ counts, int T, int H, int E,
-                   int token_blocks, __nv_bfloat16* __restrict__ dout, float* __restrict__ dg) {
+combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __restrict__ gates,
+                   const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
+                   const int32_t* __restrict__ counts, int T, int H, int E, int token_blocks, Rows dout,
+                   float* __restrict__ dg) {
     if ((int)blockIdx.x >= token_blocks) {
-        zero_pad_rows(dout, seg_base, counts, blockIdx.x - token_blocks, H);
+        const int e = blockIdx.x - token_blocks;
+        zero_pad_rows(dout.base<kPeer>(e), seg_base, counts, e, H);
         return;
     }
     const int lane = threadIdx.x & 31;
@@ -157,15 +186,15 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __
             unpack8(v, d[i]);
         }
         for (int r = 0; r < n; ++r) {
-            const uint4* os = reinterpret_cast<const uint4*>(o + (size_t)rows[r] * H);
-            uint4* ds = reinterpret_cast<uint4*>(dout + (size_t)rows[r] * H);
+            const uint4* os = reinterpret_cast<const uint4*>(o.base<kPeer>(experts[r]) + (size_t)rows[r] * H);
+            uint4* ds = reinterpret_cast<uint4*>(dout.base<kPeer>(experts[r]) + (size_t)rows[r] * H);
             float s = 0.f;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int j = base + i * 32 + lane;
                 if (j < nvec) {
                     float f[8], w[8];
-                    unpack8(ld_nc_v4(os + j), f);
+                    unpack8(kPeer ? os[j] : ld_nc_v4(os + j), f);
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                         s = fmaf(d[i][c], f[c], s);
@@ -197,6 +226,13 @@ int check_perm(int T, int H, int E) {
     B200_CHECK_ARG(H % 8 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 8, got %d", H);
     return B200MOE_OK;
 }
+int check_peer(int E, int e_per_rank) {
+    B200_CHECK_ARG(e_per_rank >= 1 && E % e_per_rank == 0, B200MOE_ERR_CONFIG,
+                   "n_experts (%d) not divisible by experts per rank (%d)", E, e_per_rank);
+    return B200MOE_OK;
+}
+Rows local_rows(void* p, int E) { return Rows{(__nv_bfloat16*)p, nullptr, E}; }
+Rows peer_rows(const uint64_t* bufs, int epr) { return Rows{nullptr, bufs, epr}; }
 }  // namespace
 
 extern "C" {
@@ -206,9 +242,23 @@ int b200moe_permute(const void* x, const int32_t* slot_rank, const int32_t* seg_
     int rc = check_perm(T, H, E);
     if (rc) return rc;
     const int tb = ceil_div(T, kPermThreads / 32);
-    permute_kernel<<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts, T, H,
-                                                         E, tb, (__nv_bfloat16*)xp);
+    permute_kernel<false><<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts,
+                                                                T, H, E, tb, local_rows(xp, E), nullptr, 0);
     B200_CHECK_LAUNCH("permute");
+    return B200MOE_OK;
+}
+
+int b200moe_permute_peer(const void* x, const int32_t* slot_rank, const int32_t* seg_base, const int32_t* counts,
+                         int T, int H, int E, int e_per_rank, int rank, const uint64_t* xp_bufs,
+                         const uint64_t* count_bufs, cudaStream_t stream) {
+    int rc = check_perm(T, H, E);
+    if (rc) return rc;
+    if ((rc = check_peer(E, e_per_rank))) return rc;
+    const int tb = ceil_div(T, kPermThreads / 32);
+    permute_kernel<true><<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts,
+                                                               T, H, E, tb, peer_rows(xp_bufs, e_per_rank),
+                                                               count_bufs, rank);
+    B200_CHECK_LAUNCH("permute_peer");
     return B200MOE_OK;
 }
 
@@ -217,9 +267,21 @@ int b200moe_combine(const void* o, const float* gates, const int32_t* slot_rank,
     int rc = check_perm(T, H, E);
     if (rc) return rc;
     const int tb = ceil_div(T, kPermThreads / 32);
-    combine_kernel<<<tb, kPermThreads, 0, stream>>>((const __nv_bfloat16*)o, gates, slot_rank, seg_base, T, H, E,
-                                                     (__nv_bfloat16*)y);
+    combine_kernel<false><<<tb, kPermThreads, 0, stream>>>(local_rows((void*)o, E), gates, slot_rank, seg_base, T, H,
+                                                            E, (__nv_bfloat16*)y);
     B200_CHECK_LAUNCH("combine");
+    return B200MOE_OK;
+}
+
+int b200moe_combine_peer(const uint64_t* o_bufs, int e_per_rank, const float* gates, const int32_t* slot_rank,
+                         const int32_t* seg_base, int T, int H, int E, void* y, cudaStream_t stream) {
+    int rc = check_perm(T, H, E);
+    if (rc) return rc;
+    if ((rc = check_peer(E, e_per_rank))) return rc;
+    const int tb = ceil_div(T, kPermThreads / 32);
+    combine_kernel<true><<<tb, kPermThreads, 0, stream>>>(peer_rows(o_bufs, e_per_rank), gates, slot_rank, seg_base,
+                                                           T, H, E, (__nv_bfloat16*)y);
+    B200_CHECK_LAUNCH("combine_peer");
     return B200MOE_OK;
 }
 
@@ -229,10 +291,24 @@ int b200moe_combine_bwd(const void* dy, const void* o, const float* gates, const
     int rc = check_perm(T, H, E);
     if (rc) return rc;
     const int tb = ceil_div(T, kPermThreads / 32);
-    combine_bwd_kernel<<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)o,
-                                                             gates, slot_rank, seg_base, counts, T, H, E, tb,
-                                                             (__nv_bfloat16*)dout, dg);
+    combine_bwd_kernel<false><<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)dy, local_rows((void*)o, E),
+                                                                    gates, slot_rank, seg_base, counts, T, H, E, tb,
+                                                                    local_rows(dout, E), dg);
     B200_CHECK_LAUNCH("combine_bwd");
+    return B200MOE_OK;
+}
+
+int b200moe_combine_bwd_peer(const void* dy, const uint64_t* o_bufs, const float* gates, const int32_t* slot_rank,
+                             const int32_t* seg_base, const int32_t* counts, int T, int H, int E, int e_per_rank,
+                             const uint64_t* dout_bufs, float* dg, cudaStream_t stream) {
+    int rc = check_perm(T, H, E);
+    if (rc) return rc;
+    if ((rc = check_peer(E, e_per_rank))) return rc;
+    const int tb = ceil_div(T, kPermThreads / 32);
+    combine_bwd_kernel<true><<<tb + E, kPermThreads, 0, stream>>>(
+        (const __nv_bfloat16*)dy, peer_rows(o_bufs, e_per_rank), gates, slot_rank, seg_base, counts, T, H, E, tb,
+        peer_rows(dout_bufs, e_per_rank), dg);
+    B200_CHECK_LAUNCH("combine_bwd_peer");
     return B200MOE_OK;
 }
 

@@ -46,13 +46,17 @@ __global__ void swizzle_w_j(const float* __restrict__ w, int H, int E, float4* _
 }
 
 // ---- pass 1: one thread per token
+// Row handles: row index in the owner's buffer, with the owner rank in bits
+// 26..30 (expert parallel: owner = e / e_per_rank; single GPU: owner 0).
+constexpr int kRowBits = 26;
+
 template <int EP, int KM>
 __global__ void __launch_bounds__(256)
 router_dh_kernel(const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
                  const float* __restrict__ dg, const float* __restrict__ dgx, int64_t sx_t, int64_t sx_e,
                  const float* __restrict__ gates, const float* __restrict__ probs, const float* __restrict__ z,
                  const float* __restrict__ noise_act, int T, int E, int router_type, float* __restrict__ dh_out,
-                 float* __restrict__ dn_out, int32_t* __restrict__ rows_out) {
+                 float* __restrict__ dn_out, int32_t* __restrict__ rows_out, int e_per_rank) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
     float p[EP], g[EP];
@@ -80,7 +84,7 @@ router_dh_kernel(const int32_t* __restrict__ slot_rank, const int32_t* __restric
             if (rk >= 0 && nrow < KM) {
 #pragma unroll
                 for (int j = 0; j < KM; ++j)
-                    if (j == nrow) rows[j] = seg_base[e] + rk;
+                    if (j == nrow) rows[j] = ((e / e_per_rank) << kRowBits) | (seg_base[e] + rk);
                 ++nrow;
             }
         }
@@ -107,7 +111,8 @@ constexpr int kDxThreads = 256;
 
 template <int EP, int KM, bool kNoise>
 __global__ void __launch_bounds__(kDxThreads)
-router_dx_kernel(const __nv_bfloat16* __restrict__ dxp, const int32_t* __restrict__ rows_in,
+router_dx_kernel(const __nv_bfloat16* __restrict__ dxp_local, const uint64_t* __restrict__ dxp_bufs,
+                 const int32_t* __restrict__ rows_in,
                  const float* __restrict__ dh, const float* __restrict__ dn, const float4* __restrict__ wsw,
                  const float4* __restrict__ wnsw, int T, int H, int E, __nv_bfloat16* __restrict__ dx) {
     constexpr int TT = 32 / EP;
@@ -142,7 +147,16 @@ router_dx_kernel(const __nv_bfloat16* __restrict__ dxp, const int32_t* __restric
         for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
             for (int j = 0; j < KM; ++j)
-                if (rr[tt][j] >= 0) ld[tt][j] = ld_nc_v4(dxp + (size_t)rr[tt][j] * H + hb * 8);
+                if (rr[tt][j] >= 0) {
+                    const int h = rr[tt][j];
+                    const size_t row = (size_t)(h & ((1 << kRowBits) - 1));
+                    if (dxp_bufs) {  // expert parallel: the owner's buffer, over NVLink
+                        const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(dxp_bufs[h >> kRowBits]);
+                        ld[tt][j] = *reinterpret_cast<const uint4*>(src + row * H + hb * 8);
+                    } else {
+                        ld[tt][j] = ld_nc_v4(dxp_local + row * H + hb * 8);
+                    }
+                }
 #pragma unroll
         for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
@@ -347,7 +361,8 @@ using namespace b200moe;
 
 namespace {
 template <int EP, int KM>
-int router_bwd_impl(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
+int router_bwd_impl(const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
+                    const int32_t* seg_base, const float* dg,
                     const float* dgx, int64_t sx_t, int64_t sx_e, const float* gates, const float* probs,
                     const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T, int H,
                     int E, int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
@@ -360,26 +375,30 @@ int router_bwd_impl(const void* dxp, const int32_t* slot_rank, const int32_t* se
     if (noise) swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
     router_dh_kernel<EP, KM><<<ceil_div(T, 256), 256, 0, stream>>>(slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates,
                                                                     probs, z, noise_act, T, E, router_type, dh,
-                                                                    noise ? dn : nullptr, rows);
+                                                                    noise ? dn : nullptr, rows, e_per_rank);
     constexpr int TT = 32 / EP;
     const int grid = ceil_div(ceil_div(T, TT), kDxThreads / 32);
     if (noise)
-        router_dx_kernel<EP, KM, true><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, rows, dh, dn,
-                                                                         wsw, wnsw, T, H, E, (__nv_bfloat16*)dx);
+        router_dx_kernel<EP, KM, true><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, dxp_bufs, rows,
+                                                                         dh, dn, wsw, wnsw, T, H, E,
+                                                                         (__nv_bfloat16*)dx);
     else
-        router_dx_kernel<EP, KM, false><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, rows, dh, dn,
-                                                                          wsw, wnsw, T, H, E, (__nv_bfloat16*)dx);
+        router_dx_kernel<EP, KM, false><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, dxp_bufs, rows,
+                                                                          dh, dn, wsw, wnsw, T, H, E,
+                                                                          (__nv_bfloat16*)dx);
     B200_CHECK_LAUNCH("router_bwd");
     return B200MOE_OK;
 }
 
 template <int EP>
-int router_bwd_k(int k, const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
+int router_bwd_k(int k, const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
+                 const int32_t* seg_base, const float* dg,
                  const float* dgx, int64_t sx_t, int64_t sx_e, const float* gates, const float* probs,
                  const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T, int H, int E,
                  int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
-#define CALL(KM) router_bwd_impl<EP, KM>(dxp, slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates, probs, w_g, w_noise, \
-                                         z, noise_act, T, H, E, router_type, dx, dh, dn, workspace, stream)
+#define CALL(KM) router_bwd_impl<EP, KM>(dxp, dxp_bufs, e_per_rank, slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates, \
+                                         probs, w_g, w_noise, z, noise_act, T, H, E, router_type, dx, dh, dn,        \
+                                         workspace, stream)
     if (k <= 2) return CALL(2);
     if (k <= 4 || EP == 4) return CALL((EP < 4 ? EP : 4));
     return CALL(EP);
@@ -400,24 +419,48 @@ int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, f
 
 extern "C" {
 
-int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
-                       const float* dgates_ext, int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates,
-                       const float* probs, const float* w_g, const float* w_noise, const float* z,
-                       const float* noise_act, int T, int H, int E, int k, int router_type, void* dx, float* dh,
-                       float* dn, float* workspace, cudaStream_t stream) {
+static int router_bwd_any(const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
+                          const int32_t* seg_base, const float* dg, const float* dgates_ext, int64_t dgates_stride_t,
+                          int64_t dgates_stride_e, const float* gates, const float* probs, const float* w_g,
+                          const float* w_noise, const float* z, const float* noise_act, int T, int H, int E, int k,
+                          int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
     B200_CHECK_ARG(T >= 1 && E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "bad T/E (%d, %d)", T, E);
     B200_CHECK_ARG(k >= 1 && k <= E, B200MOE_ERR_CONFIG, "top-k out of range: k=%d, n=%d", k, E);
     B200_CHECK_ARG(H % 8 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 8");
     B200_CHECK_ARG(router_type != B200MOE_ROUTER_ST || probs != nullptr, B200MOE_ERR_CONFIG, "st needs probs");
     B200_CHECK_ARG(z == nullptr || (w_noise && noise_act && dn), B200MOE_ERR_CONFIG, "noise args missing");
-#define CALL(EP) router_bwd_k<EP>(k, dxp, slot_rank, seg_base, dg, dgates_ext, dgates_stride_t,                   \
-                                  dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, T, H, E, router_type, \
-                                  dx, dh, dn, workspace, stream)
+    B200_CHECK_ARG(e_per_rank >= 1 && E % e_per_rank == 0 && E / e_per_rank <= 32, B200MOE_ERR_CONFIG,
+                   "experts per rank %d does not divide %d", e_per_rank, E);
+#define CALL(EP) router_bwd_k<EP>(k, dxp, dxp_bufs, e_per_rank, slot_rank, seg_base, dg, dgates_ext,              \
+                                  dgates_stride_t, dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, T, H, \
+                                  E, router_type, dx, dh, dn, workspace, stream)
     if (E <= 4) return CALL(4);
     if (E <= 8) return CALL(8);
     if (E <= 16) return CALL(16);
     return CALL(32);
 #undef CALL
+}
+
+int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
+                       const float* dgates_ext, int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates,
+                       const float* probs, const float* w_g, const float* w_noise, const float* z,
+                       const float* noise_act, int T, int H, int E, int k, int router_type, void* dx, float* dh,
+                       float* dn, float* workspace, cudaStream_t stream) {
+    return router_bwd_any(dxp, nullptr, E, slot_rank, seg_base, dg, dgates_ext, dgates_stride_t, dgates_stride_e,
+                          gates, probs, w_g, w_noise, z, noise_act, T, H, E, k, router_type, dx, dh, dn, workspace,
+                          stream);
+}
+
+int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
+                            const int32_t* seg_base, const float* dg, const float* dgates_ext,
+                            int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates, const float* probs,
+                            const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T,
+                            int H, int E, int k, int router_type, void* dx, float* dh, float* dn, float* workspace,
+                            cudaStream_t stream) {
+    B200_CHECK_ARG(dxp_bufs != nullptr, B200MOE_ERR_CONFIG, "peer buffers required");
+    return router_bwd_any(nullptr, dxp_bufs, e_per_rank, slot_rank, seg_base, dg, dgates_ext, dgates_stride_t,
+                          dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, T, H, E, k, router_type, dx, dh,
+                          dn, workspace, stream);
 }
 
 int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T, int H, int E, float* dw_g,

@@ -74,6 +74,12 @@ class EPPlan:
         expert = torch.arange(n, dtype=torch.int32, device=device) % self.e_local
         return base, expert
 
+    def peer_seg_base(self, device) -> torch.Tensor:
+        """[E] row of (this rank, expert e) inside expert e's owner receive buffer:
+        (rank * E_local + e % E_local) * cap_pad."""
+        e = torch.arange(self.n_experts, dtype=torch.int32, device=device)
+        return ((self.rank * self.e_local + e % self.e_local) * self.cap_pad).to(torch.int32)
+
     def exchange_counts(self, counts: torch.Tensor, group=None) -> torch.Tensor:
         """counts[E] (tokens this rank sends to each expert) -> recv[R * E_local]
         (tokens each source rank sends to each of my experts)."""
@@ -209,12 +215,200 @@ class _EPFunction(torch.autograd.Function):
         return dx, dwg, dwn, dW1, dW2, dW3, None, None
 
 
+class _PeerBuffers:
+    """One symmetric-memory allocation per (receive rows, hidden, group) holding
+    this rank's receive-side buffers -- xr (tokens in), O (expert outputs), dO,
+    dxp, each [R*E_local*cap_pad, H] bf16 -- plus the int32 receive-count table.
+    Peers address them through device arrays of per-rank base pointers."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, rows: int, H: int, n_counts: int, group, device):
+        grp = group if group is not None else dist.group.WORLD
+        key = (rows, H, n_counts, grp.group_name, device.index)
+        b = cls._cache.get(key)
+        if b is None:
+            b = cls(rows, H, n_counts, grp, device)
+            cls._cache[key] = b
+        return b
+
+    def __init__(self, rows, H, n_counts, grp, device):
+        import torch.distributed._symmetric_memory as symm
+        plane = rows * H * 2
+        cnt_off = 4 * plane
+        total = cnt_off + ((n_counts * 4 + 255) // 256) * 256
+        self.raw = symm.empty(total, dtype=torch.uint8, device=device)
+        self.handle = symm.rendezvous(self.raw, grp.group_name)
+        self.views = [self.raw[i * plane:(i + 1) * plane].view(torch.bfloat16).view(rows, H) for i in range(4)]
+        self.counts = self.raw[cnt_off:cnt_off + n_counts * 4].view(torch.int32)
+        ptrs = list(self.handle.buffer_ptrs)
+        mk = lambda off: torch.tensor([p + off for p in ptrs], dtype=torch.int64, device=device)  # noqa: E731
+        self.peer = [mk(i * plane) for i in range(4)]   # xr, O, dO, dxp base pointers on every rank
+        self.peer_counts = mk(cnt_off)
+
+    def barrier(self):
+        self.handle.barrier(channel=0)
+
+    @property
+    def xr(self):
+        return self.views[0]
+
+    @property
+    def o(self):
+        return self.views[1]
+
+    @property
+    def do(self):
+        return self.views[2]
+
+    @property
+    def dxp(self):
+        return self.views[3]
+
+
+class _EPPeerFunction(torch.autograd.Function):
+    """Expert parallelism with the dispatch / combine exchange fused into the
+    permute / combine kernels over NVLink peer memory (no NCCL all-to-all)."""
+
+    @staticmethod
+    def forward(ctx, x, w_g, w_noise, W1, W2, W3, z, st):
+        cfg, plan, group = st["cfg"], st["plan"], st["group"]
+        T, H = x.shape
+        E = w_g.shape[1]
+        El = plan.e_local
+        F = W1.shape[1]
+        dev = x.device
+        s = _lib.stream_ptr()
+        f32 = dict(dtype=torch.float32, device=dev)
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        rt = _lib.ROUTER[cfg.router_type]
+        Rs = plan.send_rows
+        pb = _PeerBuffers.get(Rs, H, plan.world * El, group, dev)
+
+        logits = torch.empty(T, E, **f32)
+        gates = torch.empty(T, E, **f32)
+        probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
+        noise_act = torch.empty(T, E, **f32) if z is not None else None
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws = torch.empty(2 * H * _ep(E), **f32)
+        _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
+                  cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),
+                  ws.data_ptr(), err.data_ptr(), s)
+        slot_rank = torch.empty(T, E, dtype=torch.int32, device=dev)
+        counts = torch.empty(E, dtype=torch.int32, device=dev)
+        seg_local = torch.empty(E, dtype=torch.int32, device=dev)
+        gate_mass = torch.empty(E, **f32)
+        imp = torch.empty(E, **f32)
+        stats = torch.empty(2, dtype=torch.int64, device=dev)
+        _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if plan.capacity is None else plan.capacity,
+                  _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_FIXED, plan.cap_pad, slot_rank.data_ptr(),
+                  counts.data_ptr(), seg_local.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),
+                  _dispatch_ws(dev).data_ptr(), s)
+        seg_peer = plan.peer_seg_base(dev)      # row of (this rank, expert e) in e's owner buffer
+        pb.barrier()                            # every rank is done with the previous use of the buffers
+        _lib.call("b200moe_permute_peer", x.data_ptr(), slot_rank.data_ptr(), seg_peer.data_ptr(),
+                  counts.data_ptr(), T, H, E, El, plan.rank, pb.peer[0].data_ptr(), pb.peer_counts.data_ptr(), s)
+        pb.barrier()                            # all tokens and counts have landed
+        rbase, rexp = plan.recv_segments(dev)
+        nseg = plan.world * El
+        rcounts = pb.counts
+        A = torch.empty(Rs, F, **bf)
+        B = torch.empty(Rs, F, **bf)
+        Hh = torch.empty(Rs, F, **bf)
+        _lib.call("b200moe_expert_fwd1", pb.xr.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
+                  rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, A.data_ptr(), B.data_ptr(), Hh.data_ptr(), s)
+        _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
+                  rexp.data_ptr(), nseg, Rs, H, F, El, pb.o.data_ptr(), s)
+        pb.barrier()                            # all expert outputs are ready
+        y = torch.empty(T, H, **bf)
+        _lib.call("b200moe_combine_peer", pb.peer[1].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
+                  seg_peer.data_ptr(), T, H, E, y.data_ptr(), s)
+        st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_peer,
+                             gate_mass=gate_mass, importance=imp, stats=stats, err=err, recv_counts=rcounts.clone())
+        ctx.st = st
+        ctx.pb = pb
+        ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer,
+                              A, B, Hh)
+        return y, gates
+
+    @staticmethod
+    def backward(ctx, dy, dgates):
+        (x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer, A, B,
+         Hh) = ctx.saved_tensors
+        st, pb = ctx.st, ctx.pb
+        cfg, plan, group = st["cfg"], st["plan"], st["group"]
+        T, H = x.shape
+        E = w_g.shape[1]
+        El = plan.e_local
+        F = W1.shape[1]
+        Rs = plan.send_rows
+        dev = x.device
+        s = _lib.stream_ptr()
+        f32 = dict(dtype=torch.float32, device=dev)
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        nseg = plan.world * El
+        rbase, rexp = plan.recv_segments(dev)
+        rcounts = pb.counts
+
+        dy = (torch.zeros(T, H, **bf) if dy is None else dy).to(torch.bfloat16).contiguous()
+        dg = torch.empty(T, E, **f32)
+        _lib.call("b200moe_combine_bwd_peer", dy.data_ptr(), pb.peer[1].data_ptr(), gates.data_ptr(),
+                  slot_rank.data_ptr(), seg_peer.data_ptr(), counts.data_ptr(), T, H, E, El, pb.peer[2].data_ptr(),
+                  dg.data_ptr(), s)
+        pb.barrier()                            # all output gradients have landed
+        dA = torch.empty(Rs, F, **bf)
+        dB = torch.empty(Rs, F, **bf)
+        _lib.call("b200moe_expert_bwd2", pb.do.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
+                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(),
+                  dB.data_ptr(), s)
+        dW1 = torch.empty_like(W1)
+        dW2 = torch.empty_like(W2)
+        dW3 = torch.empty_like(W3)
+        _lib.call("b200moe_expert_wgrad", pb.xr.data_ptr(), Hh.data_ptr(), pb.do.data_ptr(), dA.data_ptr(),
+                  dB.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El,
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
+        _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
+                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, pb.dxp.data_ptr(), s)
+        pb.barrier()                            # all input gradients are ready
+        dx = torch.empty(T, H, **bf)
+        dh = torch.empty(T, E, **f32)
+        dn = torch.empty(T, E, **f32) if z is not None else None
+        dgx, sx_t, sx_e = None, 0, 0
+        if dgates is not None:
+            dgx = dgates.to(torch.float32)
+            sx_t, sx_e = dgx.stride()
+        ws = torch.empty(2 * H * _ep(E) + T * _ep(E), **f32)
+        _lib.call("b200moe_router_bwd_peer", pb.peer[3].data_ptr(), El, slot_rank.data_ptr(), seg_peer.data_ptr(),
+                  dg.data_ptr(), _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(),
+                  w_noise.data_ptr(), _lib.ptr(z), _lib.ptr(noise_act), T, H, E, cfg.top_k,
+                  _lib.ROUTER[cfg.router_type], dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
+        dwg = torch.empty(H, E, **f32)
+        dwn = torch.empty(H, E, **f32) if z is not None else None
+        wsw = torch.empty((T + 127) // 128 * H * E, **f32)
+        _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), _lib.ptr(dn), T, H, E, dwg.data_ptr(),
+                  _lib.ptr(dwn), wsw.data_ptr(), s)
+        if st.get("reduce_router", True):
+            dist.all_reduce(dwg, group=group)
+            if dwn is not None:
+                dist.all_reduce(dwn, group=group)
+        return dx, dwg, dwn, dW1, dW2, dW3, None, None
+
+
 class ExpertParallelMoE:
     """EP-sharded E8T2 layer on this rank.  `w_g`, `w_noise`: replicated
     router [H, E] fp32; W1, W3 [E_local, F, H], W2 [E_local, H, F] bf16: the
     experts this rank owns (e.g. from upcycle_shard / upcycle_experts)."""
 
-    def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None):
+    TRANSPORTS = ("p2p", "nccl")
+
+    def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None, transport: str = "p2p"):
+        """transport: "p2p" (default) fuses the dispatch/combine exchange into the
+        permute/combine kernels over NVLink symmetric memory; "nccl" uses
+        all_to_all_single between separate kernels (the comparison baseline)."""
+        if transport not in self.TRANSPORTS:
+            raise ConfigError(f"transport must be one of {self.TRANSPORTS}, got {transport!r}")
+        self.transport = transport
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -233,8 +427,9 @@ class ExpertParallelMoE:
         plan = EPPlan.make(self.world, self.rank, self.cfg.n_experts, T, self.cfg.capacity_factor)
         z = _noise(T, self.cfg.n_experts, x.device, self.cfg.noise_enabled and training, rng, noise)
         st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router)
-        y, gates = _EPFunction.apply(x.to(torch.bfloat16).contiguous(), self.w_g.to(torch.float32).contiguous(),
-                                     self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)
+        fn = _EPPeerFunction if self.transport == "p2p" else _EPFunction
+        y, gates = fn.apply(x.to(torch.bfloat16).contiguous(), self.w_g.to(torch.float32).contiguous(),
+                            self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)
         r = st["routing"]
         from .moe import MoEForwardResult
         gates._b200_importance = (r["importance"], gates._version)
@@ -270,7 +465,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     wn.requires_grad_()
     gate = P.GateConfig(n_experts=E, top_k=K, router_type=args.router, capacity_factor=args.cf,
                         drop_policy=args.policy)
-    layer = ExpertParallelMoE(wg, wn, W1, W2, W3, gate)
+    layer = ExpertParallelMoE(wg, wn, W1, W2, W3, gate, transport=args.transport)
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     x = torch.randn(T, H, device=dev, generator=g).to(torch.bfloat16).requires_grad_()
     dy = torch.randn(T, H, device=dev, generator=g).to(torch.bfloat16)
@@ -283,10 +478,10 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
         out = layer(xin)
         aux = P.importance_penalty(out.gates)
         torch.autograd.backward([out.output, aux], [dyin, lam])
-        return out
+        return out, aux
 
     for _ in range(max(args.warmup, 3)):
-        out = step(x, dy)
+        out, _ = step(x, dy)
     torch.cuda.synchronize()
     S = int(out.routing["recv_counts"].sum().item())
     prof = _lib.Profiler(events=False)
@@ -311,28 +506,10 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     ms_max = float(tmax[0])
     S_tot = float(ssum[0])
 
-    # e2e: host-resident x / dy copied in, aux loss read back, every step
-    xh = x.detach().cpu().pin_memory()
-    dyh = dy.cpu().pin_memory()
-    res_h = torch.empty(1, dtype=torch.float32).pin_memory()
-    xd, dyd = torch.empty_like(x), torch.empty_like(dy)
-
-    def e2e_step():
-        xd.copy_(xh, non_blocking=True)
-        dyd.copy_(dyh, non_blocking=True)
-        out = step(xd.detach().requires_grad_(), dyd)
-        res_h.copy_(P.importance_penalty(out.gates).detach().reshape(1), non_blocking=True)
-
-    e2e_step()
-    torch.cuda.synchronize()
+    # e2e: host-resident x / dy copied in (copy stream, one step ahead), aux loss read back, every step
     dist.barrier()
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a0.record()
-    for _ in range(args.steps):
-        e2e_step()
-    a1.record()
-    torch.cuda.synchronize()
-    e2e_t = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev, dtype=torch.float64)
+    e2e_rank = B.run_e2e(args.steps, T, x, dy, step)
+    e2e_t = torch.tensor([e2e_rank["ms_per_step"]], device=dev, dtype=torch.float64)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     clocks = clk.summary()
     if rank == 0:
@@ -347,14 +524,18 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                        "hidden": H, "ffn": F, "experts": E, "top_k": K, "tokens_per_gpu": T,
                        "capacity_factor": args.cf, "router": args.router, "drop_policy": args.policy,
                        "kept_slots_total": int(S_tot), "parallelism": f"ep{world}",
-                       "comm": "NCCL all_to_all_single (equal splits, fixed capacity segments) + all_reduce(dW_g)",
+                       "comm": ("dispatch/combine fused into permute/combine kernels over NVLink symmetric memory "
+                                "(device barriers) + NCCL all_reduce(dW_g)" if args.transport == "p2p" else
+                                "NCCL all_to_all_single (equal splits, fixed capacity segments) + all_reduce(dW_g)"),
+                       "transport": args.transport,
                        "l2": "working set > L2 (expert weights + activations)"},
             "mfu": {"measured_peak": round(flops / (ms_max * 1e-3) / (world * peak * 1e12), 4),
                     "spec_2250": round(flops / (ms_max * 1e-3) / (world * 2.25e15), 4)},
             "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM)", "bound": "tensor", "achieved": None,
                          "peak": peak, "unit": "TFLOP/s", "frac": None, "traffic": None},
             "e2e": {"value": round(world * T / (float(e2e_t[0]) * 1e-3), 1), "unit": "tokens/s",
-                    "h2d_bytes_per_step": world * (xh.numel() + dyh.numel()) * 2, "d2h_bytes_per_step": 4 * world},
+                    "h2d_bytes_per_step": world * e2e_rank["h2d_bytes_per_step"], "d2h_bytes_per_step": 4 * world,
+                    "h2d": e2e_rank["h2d"]},
             "cpu_baseline": None, "clocks": clocks, "gpu_launches": prof.launches,
         }
         print(json.dumps(line), flush=True)

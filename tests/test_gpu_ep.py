@@ -23,4 +23,4 @@ def test_ep_matches_single_gpu_per_rank():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
-    assert r.stdout.count("PASS") == 4 * n
+    assert r.stdout.count("PASS") == 8 * n   # 4 cases x {p2p, nccl} per rank

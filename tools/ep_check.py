@@ -21,7 +21,7 @@ def rel(a, b):
     return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
 
 
-def case(rank, world, dev, T, H, F, router, policy, cf, noise):
+def case(rank, world, dev, T, H, F, router, policy, cf, noise, transport):
     E = 8
     El = E // world
     g = torch.Generator(device=dev).manual_seed(5)
@@ -40,7 +40,7 @@ def case(rank, world, dev, T, H, F, router, policy, cf, noise):
 
     # ---- expert parallel
     lw = [t.clone().requires_grad_() for t in (wg, wn, W1[own], W2[own], W3[own])]
-    ep = ExpertParallelMoE(*lw, cfg)
+    ep = ExpertParallelMoE(*lw, cfg, transport=transport)
     xe = x.clone().requires_grad_()
     oe = ep(xe, training=True, noise=z)
     loss = (oe.output.float() * dy.float()).sum() + 0.1 * P.importance_penalty(oe.gates)
@@ -78,7 +78,7 @@ def case(rank, world, dev, T, H, F, router, policy, cf, noise):
         refn = rw[1].grad.clone()
         dist.all_reduce(refn)
         check("dW_noise", rel(lw[1].grad, refn) < 2e-2)
-    tag = f"T={T} H={H} F={F} {router} {policy} cf={cf} noise={noise}"
+    tag = f"[{transport}] T={T} H={H} F={F} {router} {policy} cf={cf} noise={noise}"
     print(f"rank {rank}: {'PASS' if ok else 'FAIL ' + ','.join(msgs)} {tag}", flush=True)
     return ok
 
@@ -90,11 +90,12 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     rank, world = dist.get_rank(), dist.get_world_size()
     ok = True
-    for args in [(1024, 512, 768, "mixtral", "position", 1.0, False),
-                 (1000, 512, 512, "st", "score", 2.0, True),
-                 (512, 256, 512, "mixtral", "position", None, False),
-                 (2048, 1024, 1024, "mixtral", "position", 0.5, False)]:
-        ok &= case(rank, world, dev, *args)
+    for transport in ("p2p", "nccl"):
+        for args in [(1024, 512, 768, "mixtral", "position", 1.0, False),
+                     (1000, 512, 512, "st", "score", 2.0, True),
+                     (512, 256, 512, "mixtral", "position", None, False),
+                     (2048, 1024, 1024, "mixtral", "position", 0.5, False)]:
+            ok &= case(rank, world, dev, *args, transport)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     dist.destroy_process_group()
