@@ -42,6 +42,7 @@ constexpr int kBN = 256;           // accumulator columns per tile
 constexpr int kRowsPerCta = 128;   // M rows per CTA
 constexpr int kMaxSeg = 64;
 constexpr int kNumEpiWarps = 8;
+constexpr bool kWideStores = false;  // see Geo::kWide
 constexpr int kNumThreads = 64 + 32 * kNumEpiWarps;   // producer, MMA, 8 epilogue warps
 
 struct TmaSet {
@@ -82,8 +83,15 @@ struct Geo {
     // Store-ring depth per epilogue warp (4 buffers + 5 stages measured no
     // better than 2 + 6 for WGRAD on B200).
     static constexpr int kRing = 2;
-    static constexpr int kStages = kTmaEpiLoads ? 4 : Cfg<kCG>::kStages;
-    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? 4 * 2048 : 0) + kRing * 2048;
+    // Wide stores: 32 x 64 bf16 boxes (128-byte rows, SWIZZLE_128B) halve the
+    // TMA row requests of the plain-store epilogues, but cost one operand stage
+    // of shared memory.  Measured on B200: WGRAD 2.12-2.27 ms -> 2.33-2.42 ms
+    // (its operand loads are latency-bound, in-flight bytes matter more), BWD1
+    // and FWD2 within noise -- so disabled; kept for the next tile-shape study.
+    static constexpr bool kWide = kWideStores && (kCG == 2) && (kMode == kFwd2 || kMode == kBwd1 || kMode == kWgrad);
+    static constexpr int kStoreBytes = kWide ? 4096 : 2048;
+    static constexpr int kStages = kTmaEpiLoads ? 4 : (kWide ? 5 : Cfg<kCG>::kStages);
+    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? 4 * 2048 : 0) + kRing * kStoreBytes;
     static constexpr int kSmemBytes = kStages * Cfg<kCG>::kStageBytes + kNumEpiWarps * kEpiWarpBytes +
                                       1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2);
 };
@@ -265,6 +273,26 @@ __device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m,
     ring.idx = (ring.idx + 1 == kRing) ? 0 : ring.idx + 1;
 }
 
+// 32 rows x 64 columns (128-byte rows, SWIZZLE_128B: chunk j of row r at j ^ (r & 7)).
+template <int kRing>
+__device__ __forceinline__ void stage_store64(EpiRing& ring, const CUtensorMap* m, const float* v, int lane, int col,
+                                              int row0) {
+    uint8_t* buf = ring.base + ring.idx * 4096;
+    if (lane == 0) ptx::bulk_wait_read<kRing - 1>();
+    __syncwarp();
+    uint4* rowp = reinterpret_cast<uint4*>(buf + lane * 128);
+    const int sw = lane & 7;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) rowp[j ^ sw] = pack8(v + 8 * j);
+    ptx::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        ptx::tma_store_2d(m, buf, col, row0);
+        ptx::bulk_commit();
+    }
+    ring.idx = (ring.idx + 1 == kRing) ? 0 : ring.idx + 1;
+}
+
 // BWD2 load ring: two buffers, each holding a 32x32 chunk of the stored `a`
 // and `b` pre-activations (2 KB each, SWIZZLE_64B), filled by TMA and tracked
 // by one mbarrier per buffer.
@@ -328,17 +356,37 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
         const int col0 = ti.n_tile * kBN;
         ptx::mbar_wait(tfull, tphase);
         ptx::tc_fence_after();
-        for (int c = half * 128; c < half * 128 + 128; c += 32) {
-            if (!k_empty) {
-                ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
-                ptx::tmem_ld_wait();
+        if constexpr (Geo<kMode, kCG>::kWide) {
+            float w[64];
+            for (int c = half * 128; c < half * 128 + 128; c += 64) {
+                if (!k_empty) {
+                    ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
+                    ptx::tmem_ld_32x32b_x32(lane_addr + c + 32, r1);
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]);
-            } else {
+                    for (int i = 0; i < 32; ++i) {
+                        w[i] = __uint_as_float(r0[i]);
+                        w[32 + i] = __uint_as_float(r1[i]);
+                    }
+                } else {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v0[i] = 0.f;
+                    for (int i = 0; i < 64; ++i) w[i] = 0.f;
+                }
+                if (!(a.debug & 1)) stage_store64<kRing>(ring, &tm.st[smap], w, lane, col0 + c, grow);
             }
-            if (!(a.debug & 1)) stage_store<kRing>(ring,&tm.st[smap], v0, lane, col0 + c, grow);
+        } else {
+            for (int c = half * 128; c < half * 128 + 128; c += 32) {
+                if (!k_empty) {
+                    ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v0[i] = 0.f;
+                }
+                if (!(a.debug & 1)) stage_store<kRing>(ring, &tm.st[smap], v0, lane, col0 + c, grow);
+            }
         }
         return;
     } else {
@@ -445,6 +493,20 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                 stage_store<kRing>(ring,&tm.st[1], v1, lane, col0 + c, row0);
                 stage_store<kRing>(ring,&tm.st[2], v2, lane, col0 + c, row0);
             }
+        } else if constexpr (Geo<kMode, kCG>::kWide) {  // kFwd2 / kBwd1, 64-column stores
+            const int col0 = ti.n_tile * kBN;
+            float w[64];
+            for (int c = half * 128; c < half * 128 + 128; c += 64) {
+                ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
+                ptx::tmem_ld_32x32b_x32(lane_addr + c + 32, r1);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    w[i] = __uint_as_float(r0[i]);
+                    w[32 + i] = __uint_as_float(r1[i]);
+                }
+                stage_store64<kRing>(ring, &tm.st[0], w, lane, col0 + c, row0);
+            }
         } else {  // kFwd2 / kBwd1: plain bf16 store
             const int col0 = ti.n_tile * kBN;
             for (int c = half * 128; c < half * 128 + 128; c += 32) {
@@ -452,7 +514,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]);
-                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
+                stage_store<kRing>(ring, &tm.st[0], v0, lane, col0 + c, row0);
             }
         }
     }
@@ -604,7 +666,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
         int acc = 0;
         uint32_t acc_phase = 0;
         EpiRing ring{staging + (warp - 2) * G::kEpiWarpBytes, 0};
-        EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + G::kRing * kStageBufBytes, ldbar + 2 * (warp - 2), 0,
+        EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + G::kRing * G::kStoreBytes, ldbar + 2 * (warp - 2), 0,
                     0};
         for (int t = cid; t < sched.total; t += ncl) {
             const TileInfo ti = sched.decode(t, a);
@@ -649,7 +711,7 @@ static EncodeTiledFn get_encode() {
 // 2-D bf16 tensor [outer, inner] (inner contiguous, row pitch `ld` elements).
 // K-major operands use box {64, 128}; MN-major operands box {64, 64}.
 static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, bool mn_major,
-                    bool ptr_is_store_target = false) {
+                    bool ptr_is_store_target = false, bool wide = false) {
     EncodeTiledFn enc = get_encode();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable");
@@ -660,10 +722,10 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ou
     cuuint32_t box[2] = {64, mn_major ? 64u : 128u};
     cuuint32_t estr[2] = {1, 1};
     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
-    if (ptr_is_store_target) {  // epilogue store map: 32 x 32 boxes, 64-byte swizzle
-        box[0] = 32;
+    if (ptr_is_store_target) {  // epilogue map: 32 x 32 boxes (64-byte swizzle) or 32 x 64 (128-byte)
+        box[0] = wide ? 64 : 32;
         box[1] = 32;
-        sw = CU_TENSOR_MAP_SWIZZLE_64B;
+        sw = wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     }
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -782,7 +844,7 @@ int b200moe_expert_fwd2(const void* h, const void* w2, const int* seg_base, cons
     B200_TRY(make_map(&tm.m[0], h, F, rows, F, false));
     B200_TRY(make_map(&tm.m[1], w2, F, (uint64_t)E_local * H, F, false));
     tm.m[2] = tm.m[3] = tm.m[4] = tm.m[0];
-    B200_TRY(make_map(&tm.st[0], o_out, H, rows, H, false, true));
+    B200_TRY(make_map(&tm.st[0], o_out, H, rows, H, false, true, kWideStores && g_cta_group == 2));
     tm.st[1] = tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)o_out, nullptr, nullptr, nullptr, nullptr};
@@ -818,7 +880,7 @@ int b200moe_expert_bwd1(const void* da, const void* db, const void* w1, const vo
     B200_TRY(make_map(&tm.m[2], w1, H, (uint64_t)E_local * F, H, true));
     B200_TRY(make_map(&tm.m[3], w3, H, (uint64_t)E_local * F, H, true));
     tm.m[4] = tm.m[0];
-    B200_TRY(make_map(&tm.st[0], dxp_out, H, rows, H, false, true));
+    B200_TRY(make_map(&tm.st[0], dxp_out, H, rows, H, false, true, kWideStores && g_cta_group == 2));
     tm.st[1] = tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dxp_out, nullptr, nullptr, nullptr, nullptr};
@@ -835,9 +897,10 @@ int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const 
     B200_TRY(make_map(&tm.m[2], da, F, rows, F, true));
     B200_TRY(make_map(&tm.m[3], xp, H, rows, H, true));
     B200_TRY(make_map(&tm.m[4], db, F, rows, F, true));
-    B200_TRY(make_map(&tm.st[0], dw1, H, (uint64_t)E_local * F, H, false, true));
-    B200_TRY(make_map(&tm.st[1], dw2, F, (uint64_t)E_local * H, F, false, true));
-    B200_TRY(make_map(&tm.st[2], dw3, H, (uint64_t)E_local * F, H, false, true));
+    const bool wide = kWideStores && g_cta_group == 2;
+    B200_TRY(make_map(&tm.st[0], dw1, H, (uint64_t)E_local * F, H, false, true, wide));
+    B200_TRY(make_map(&tm.st[1], dw2, F, (uint64_t)E_local * H, F, false, true, wide));
+    B200_TRY(make_map(&tm.st[2], dw3, H, (uint64_t)E_local * F, H, false, true, wide));
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dw1, (__nv_bfloat16*)dw2, (__nv_bfloat16*)dw3, nullptr, nullptr};
     return dispatch_launch<kWgrad>(tm, a, stream);
