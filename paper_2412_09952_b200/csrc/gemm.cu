@@ -43,6 +43,7 @@ constexpr int kRowsPerCta = 128;   // M rows per CTA
 constexpr int kMaxSeg = 64;
 constexpr int kNumEpiWarps = 8;
 constexpr bool kWideStores = false;  // see Geo::kWide
+constexpr bool kLsuStores = true;    // see emit32
 constexpr int kNumThreads = 64 + 32 * kNumEpiWarps;   // producer, MMA, 8 epilogue warps
 
 struct TmaSet {
@@ -273,6 +274,40 @@ __device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m,
     ring.idx = (ring.idx + 1 == kRing) ? 0 : ring.idx + 1;
 }
 
+// Same 32 x 32 chunk, written back through the LSU instead of TMA: after the
+// row-per-lane swizzled smem write, each lane re-reads (row i*8 + lane/4,
+// 16-byte chunk lane%4) so every st.global instruction writes eight complete
+// 64-byte row segments.  Keeps the TMA engine free for operand loads.
+__device__ __forceinline__ void stage_store_lsu(uint8_t* buf, __nv_bfloat16* gdst, size_t ld, const float* v,
+                                                int lane) {
+    uint4* rowp = reinterpret_cast<uint4*>(buf + lane * 64);
+    const int sw = (lane >> 1) & 3;
+    __syncwarp();  // previous chunk's readers are done with buf
+#pragma unroll
+    for (int j = 0; j < 4; ++j) rowp[j ^ sw] = pack8(v + 8 * j);
+    __syncwarp();
+    const int cj = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = i * 8 + (lane >> 2);
+        const uint4 val = *reinterpret_cast<const uint4*>(buf + r * 64 + ((cj ^ ((r >> 1) & 3)) << 4));
+        *reinterpret_cast<uint4*>(gdst + (size_t)r * ld + cj * 8) = val;
+    }
+}
+
+// Epilogue store of one 32x32 chunk: LSU write-back or TMA bulk store.  A/B on
+// one B200 (interleaved runs): LSU is faster for WGRAD (2.10 vs 2.17-2.42 ms),
+// slower for BWD1 (+6%) and neutral for FWD1/BWD2, so only WGRAD uses it
+// (kLsuStores); debug bits 4 / 8 force TMA / LSU for experiments.
+// GemmArgs.debug bit 2 (4) forces TMA stores, bit 3 (8) forces LSU stores.
+template <int kRing, bool kLsuDefault = false>
+__device__ __forceinline__ void emit32(EpiRing& ring, const CUtensorMap* m, __nv_bfloat16* gbase, size_t ld,
+                                       const float* v, int lane, int col, int row0, int debug) {
+    const bool lsu = (debug & 4) ? false : ((debug & 8) ? true : kLsuDefault);
+    if (lsu) stage_store_lsu(ring.base, gbase + (size_t)row0 * ld + col, ld, v, lane);
+    else stage_store<kRing>(ring, m, v, lane, col, row0);
+}
+
 // 32 rows x 64 columns (128-byte rows, SWIZZLE_128B: chunk j of row r at j ^ (r & 7)).
 template <int kRing>
 __device__ __forceinline__ void stage_store64(EpiRing& ring, const CUtensorMap* m, const float* v, int lane, int col,
@@ -385,7 +420,11 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v0[i] = 0.f;
                 }
-                if (!(a.debug & 1)) stage_store<kRing>(ring, &tm.st[smap], v0, lane, col0 + c, grow);
+                if (!(a.debug & 1)) {
+                    __nv_bfloat16* base = ti.sub == 2 ? a.out1 : (ti.sub == 0 ? a.out0 : a.out2);
+                    emit32<kRing, kLsuStores>(ring, &tm.st[smap], base, ti.sub == 2 ? a.F : a.H, v0, lane,
+                                              col0 + c, grow, a.debug);
+                }
             }
         }
         return;
@@ -420,8 +459,8 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
                     v1[i] = dm * (av * sg);
                 }
-                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
-                stage_store<kRing>(ring,&tm.st[1], v1, lane, col0 + c, row0);
+                emit32<kRing>(ring, &tm.st[0], a.out0, a.F, v0, lane, col0 + c, row0, a.debug);
+                emit32<kRing>(ring, &tm.st[1], a.out1, a.F, v1, lane, col0 + c, row0, a.debug);
             }
             return;
         } else if constexpr (kMode == kBwd2) {
@@ -467,8 +506,8 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
                     v1[i] = dm * (av * sg);
                 }
-                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
-                stage_store<kRing>(ring,&tm.st[1], v1, lane, col0 + c, row0);
+                emit32<kRing>(ring, &tm.st[0], a.out0, a.F, v0, lane, col0 + c, row0, a.debug);
+                emit32<kRing>(ring, &tm.st[1], a.out1, a.F, v1, lane, col0 + c, row0, a.debug);
             }
             return;
         }
@@ -489,9 +528,9 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v1[i] = bv;
                     v2[i] = av * sigmoidf_(av) * bv;
                 }
-                stage_store<kRing>(ring,&tm.st[0], v0, lane, col0 + c, row0);
-                stage_store<kRing>(ring,&tm.st[1], v1, lane, col0 + c, row0);
-                stage_store<kRing>(ring,&tm.st[2], v2, lane, col0 + c, row0);
+                emit32<kRing>(ring, &tm.st[0], a.out0, a.F, v0, lane, col0 + c, row0, a.debug);
+                emit32<kRing>(ring, &tm.st[1], a.out1, a.F, v1, lane, col0 + c, row0, a.debug);
+                emit32<kRing>(ring, &tm.st[2], a.out2, a.F, v2, lane, col0 + c, row0, a.debug);
             }
         } else if constexpr (Geo<kMode, kCG>::kWide) {  // kFwd2 / kBwd1, 64-column stores
             const int col0 = ti.n_tile * kBN;
@@ -505,7 +544,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     w[i] = __uint_as_float(r0[i]);
                     w[32 + i] = __uint_as_float(r1[i]);
                 }
-                stage_store64<kRing>(ring, &tm.st[0], w, lane, col0 + c, row0);
+                stage_store64<kRing>(ring, &tm.st[0], w, lane, col0 + c, row0, a.debug);
             }
         } else {  // kFwd2 / kBwd1: plain bf16 store
             const int col0 = ti.n_tile * kBN;
@@ -514,7 +553,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]);
-                stage_store<kRing>(ring, &tm.st[0], v0, lane, col0 + c, row0);
+                emit32<kRing>(ring, &tm.st[0], a.out0, a.H, v0, lane, col0 + c, row0, a.debug);
             }
         }
     }
