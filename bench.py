@@ -184,6 +184,30 @@ def main():
     run_single(args, dev)
 
 
+def gemm_traffic():
+    """DRAM bytes (read + write) of one step's five grouped-GEMM launches from
+    the committed ncu --set full capture (tools/ncu_traffic.py), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gemm_traffic.json")))
+    if not files:
+        return None
+    try:
+        return json.load(open(files[-1]))["dram_bytes_per_step"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def gemm_min_bytes(S: int) -> int:
+    """Compulsory DRAM bytes of the five GEMM launches at S kept slots (bf16):
+    every weight read twice (forward + dgrad) and its gradient written once;
+    [S, F] activations: a, b (write + read), h, da, db (write + 2 reads) = 13
+    transfers; [S, H]: xp (2 reads), o (write), do (2 reads), dxp (write) = 6."""
+    w = 3 * E * H * F * 2                 # W1, W3, W2 (all experts)
+    act_h = S * H * 2
+    act_f = S * F * 2
+    return int(3 * w + 13 * act_f + 6 * act_h)
+
+
 def layer_flops(T: int, S: int) -> float:
     """Algorithmic FLOPs of one fwd+bwd: 18*H*F per kept slot + router 6*T*H*E."""
     return 18.0 * H * F * S + 6.0 * T * H * E
@@ -332,7 +356,9 @@ def run_single(args, dev):
                 "flops_per_step": flops},
         "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM, all 5 launches/step)", "bound": "tensor",
                      "achieved": round(achieved_tf, 1), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved_tf / peak, 4), "traffic": None,
+                     "frac": round(achieved_tf / peak, 4), "traffic": gemm_traffic(),
+                     "traffic_unit": "DRAM bytes per step (5 launches), ncu --set full capture, profiles/",
+                     "algorithmic_dram_bytes_per_step": gemm_min_bytes(S),
                      "gemm_ms_per_step": round(gemm_ms, 4), "gemm_share_of_step": round(gemm_ms / ms, 4)},
         "kernels_ms_per_step": {n.replace("b200moe_", ""): round(t / args.steps, 4) for n, (t, c) in ktimes.items()},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,

@@ -135,8 +135,13 @@ struct Sched {
         } else {
             const int mt = (prefix[s + 1] - prefix[s]) / n_tiles;
             ti.sub = 0;
-            ti.n_tile = r / mt;
-            ti.m_tile = r % mt;
+            if (a.debug & 16) {  // experiment: n fastest
+                ti.m_tile = r / n_tiles;
+                ti.n_tile = r % n_tiles;
+            } else {             // m fastest: concurrent clusters share weight tiles in L2
+                ti.n_tile = r / mt;
+                ti.m_tile = r % mt;
+            }
         }
         return ti;
     }
