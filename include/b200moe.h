@@ -144,7 +144,7 @@ int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int3
                             cudaStream_t stream);
 
 /* Router weight gradients: dW_g = x^T.dh, dW_noise = x^T.dn (fp32, [H,E]),
- * deterministic (fixed-order partial sums).  workspace: >= ceil(T/128)*H*E*2
+ * deterministic (fixed-order partial sums).  workspace: >= ceil(T/64)*H*E
  * floats. */
 int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T, int H, int E, float* dw_g,
                          float* dw_noise, float* workspace, cudaStream_t stream);

@@ -108,6 +108,9 @@ router_dh_kernel(const int32_t* __restrict__ slot_rank, const int32_t* __restric
 
 // ---- pass 2: warp per TT tokens, lane owns 8 hidden units per 256-wide chunk
 constexpr int kDxThreads = 256;
+// 32/EP tokens per warp (4 at E=8).  Two tokens per warp cut registers from 128
+// to 80 but measured slower in the bench (0.062 -> 0.088 ms: W traffic doubles).
+__host__ __device__ constexpr int dx_tokens_per_warp(int ep) { return 32 / ep; }
 
 template <int EP, int KM, bool kNoise>
 __global__ void __launch_bounds__(kDxThreads)
@@ -115,21 +118,21 @@ router_dx_kernel(const __nv_bfloat16* __restrict__ dxp_local, const uint64_t* __
                  const int32_t* __restrict__ rows_in,
                  const float* __restrict__ dh, const float* __restrict__ dn, const float4* __restrict__ wsw,
                  const float4* __restrict__ wnsw, int T, int H, int E, __nv_bfloat16* __restrict__ dx) {
-    constexpr int TT = 32 / EP;
+    constexpr int TT = dx_tokens_per_warp(EP);
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (kDxThreads / 32) + (threadIdx.x >> 5);
     const int t0 = gw * TT;
     if (t0 >= T) return;
     const int HB = H / 8;
     // (token, expert) values broadcast to every lane
-    float dhall[32], dnall[32];
+    float dhall[TT * EP], dnall[TT * EP];
     {
         const int t = t0 + lane / EP, e = lane % EP;
-        const bool live = t < T && e < E;
+        const bool live = lane < TT * EP && t < T && e < E;
         const float v = live ? dh[(size_t)t * E + e] : 0.f;
         const float w = (kNoise && live) ? dn[(size_t)t * E + e] : 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < TT * EP; ++i) {
             dhall[i] = __shfl_sync(0xffffffffu, v, i);
             if constexpr (kNoise) dnall[i] = __shfl_sync(0xffffffffu, w, i);
         }
@@ -210,7 +213,8 @@ router_dx_kernel(const __nv_bfloat16* __restrict__ dxp_local, const uint64_t* __
 }
 
 // dW[h, e] = sum_t x[t, h] * d[t, e]: per (H/1024 block, 128-token chunk) partials,
-// then a fixed-order reduction over chunks.
+// then a fixed-order reduction over chunks (64-token chunks measured slower:
+// the doubled partial traffic outweighs the occupancy gain).
 constexpr int kWgTok = 128;
 
 template <int EP>
@@ -376,7 +380,7 @@ int router_bwd_impl(const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, c
     router_dh_kernel<EP, KM><<<ceil_div(T, 256), 256, 0, stream>>>(slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates,
                                                                     probs, z, noise_act, T, E, router_type, dh,
                                                                     noise ? dn : nullptr, rows, e_per_rank);
-    constexpr int TT = 32 / EP;
+    constexpr int TT = dx_tokens_per_warp(EP);
     const int grid = ceil_div(ceil_div(T, TT), kDxThreads / 32);
     if (noise)
         router_dx_kernel<EP, KM, true><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, dxp_bufs, rows,

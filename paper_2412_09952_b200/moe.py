@@ -500,7 +500,7 @@ class _MoEFunction(torch.autograd.Function):
                   dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
         dwg = torch.empty(H, E, **f32)
         dwn = torch.empty(H, E, **f32) if z is not None else None
-        wsw = torch.empty((T + 127) // 128 * H * E, **f32)
+        wsw = torch.empty((T + 63) // 64 * H * E, **f32)
         _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), _lib.ptr(dn), T, H, E, dwg.data_ptr(),
                   _lib.ptr(dwn), wsw.data_ptr(), s)
         return dx, dwg, dwn, dW1, dW2, dW3, None, None
