@@ -259,6 +259,72 @@ router_wgrad_partial(const __nv_bfloat16* __restrict__ x, const float* __restric
             if (e < E) p[(size_t)(h0 + j) * E + e] = acc[j][e];
 }
 
+// E <= 8 variant with much more memory-level parallelism: a CTA owns a
+// 256-wide h slice and a 128-token chunk; each of its 8 warps sweeps 16 tokens
+// with all 16-byte loads issued up front (lane = 8 consecutive h), then the 8
+// warp partials are summed in fixed warp order through shared memory.
+constexpr int kWg2Warps = 8;
+constexpr int kWg2Tok = 16;  // tokens per warp
+
+template <int EP>
+__global__ void __launch_bounds__(256)
+router_wgrad_partial2(const __nv_bfloat16* __restrict__ x, const float* __restrict__ d, int T, int H, int E,
+                      float* __restrict__ part) {
+    extern __shared__ float sm[];
+    float* ds = sm;                                  // [128][EP]
+    float* red = sm + kWgTok * EP;                   // [8 warps][256 h][EP]
+    const int chunk = blockIdx.y;
+    const int t0 = chunk * kWgTok;
+    const int h0 = blockIdx.x * 256;
+    for (int i = threadIdx.x; i < kWgTok * EP; i += blockDim.x) {
+        const int tt = i / EP, e = i % EP;
+        const int t = t0 + tt;
+        ds[i] = (t < T && e < E) ? d[(size_t)t * E + e] : 0.f;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hl = lane * 8;  // local h of this lane
+    uint4 u[kWg2Tok];
+#pragma unroll
+    for (int i = 0; i < kWg2Tok; ++i) {
+        const int t = t0 + warp * kWg2Tok + i;
+        u[i] = (t < T && h0 + hl < H) ? ld_nc_v4(x + (size_t)t * H + h0 + hl) : make_uint4(0, 0, 0, 0);
+    }
+    float acc[8][EP];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < EP; ++e) acc[j][e] = 0.f;
+#pragma unroll
+    for (int i = 0; i < kWg2Tok; ++i) {
+        float xv[8];
+        unpack8(u[i], xv);
+        const float* dr = ds + (warp * kWg2Tok + i) * EP;
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+            const float dv = dr[e];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j][e] = fmaf(xv[j], dv, acc[j][e]);
+        }
+    }
+    float* rw = red + (size_t)warp * 256 * EP;  // [(j * EP + e) * 32 + lane]: conflict-free
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < EP; ++e) rw[(j * EP + e) * 32 + lane] = acc[j][e];
+    __syncthreads();
+    float* p = part + (size_t)chunk * H * E;
+    for (int i = threadIdx.x; i < 256 * EP; i += blockDim.x) {
+        const int l = i % 32, je = i / 32;
+        const int j = je / EP, e = je % EP;
+        const int hh = l * 8 + j;
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWg2Warps; ++w) s += red[(size_t)w * 256 * EP + i];
+        if (e < E && h0 + hh < H) p[(size_t)(h0 + hh) * E + e] = s;
+    }
+}
+
 __global__ void reduce_partials(const float* __restrict__ part, int nchunks, size_t n, float* __restrict__ out) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         float s = 0.f;
@@ -412,8 +478,17 @@ int router_bwd_k(int k, const void* dxp, const uint64_t* dxp_bufs, int e_per_ran
 template <int EP>
 int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, float* part, cudaStream_t stream) {
     const int nch = ceil_div(T, kWgTok);
-    dim3 grid(ceil_div(H, 1024), nch);
-    router_wgrad_partial<EP><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, d, T, H, E, part);
+    if constexpr (EP <= 8) {
+        static_assert(kWg2Warps * kWg2Tok == kWgTok, "token tiling");
+        const size_t sh = (size_t)(kWgTok * EP + kWg2Warps * 256 * EP) * sizeof(float);
+        auto kern = router_wgrad_partial2<EP>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+        dim3 grid(ceil_div(H, 256), nch);
+        kern<<<grid, 256, sh, stream>>>((const __nv_bfloat16*)x, d, T, H, E, part);
+    } else {
+        dim3 grid(ceil_div(H, 1024), nch);
+        router_wgrad_partial<EP><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, d, T, H, E, part);
+    }
     const size_t n = (size_t)H * E;
     reduce_partials<<<(int)((n + 255) / 256), 256, 0, stream>>>(part, nch, n, out);
     B200_CHECK_LAUNCH("router_wgrad");
