@@ -154,28 +154,36 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict_
     constexpr int TT = 32 / EP;  // tokens per warp iteration
     extern __shared__ float4 smem_w[];
     const int nvec = H * EP / 4;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int HB = H / 8;
+    const int tfirst = (blockIdx.x * (blockDim.x >> 5) + warp) * TT;
+    // first x chunk in flight before the W staging below
+    uint4 cur[TT];
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt)
+        cur[tt] = (lane < HB && tfirst + tt < T) ? ld_nc_v4(x + (size_t)(tfirst + tt) * H + lane * 8)
+                                                 : make_uint4(0, 0, 0, 0);
     const float4* W = wsw;
     if constexpr (kSmemW) {
         for (int i = threadIdx.x; i < nvec; i += blockDim.x) smem_w[i] = wsw[i];
         __syncthreads();
         W = smem_w;
     }
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int nwarps = gridDim.x * (blockDim.x >> 5);
-    const int HB = H / 8;
 
-    for (int t0 = (blockIdx.x * (blockDim.x >> 5) + warp) * TT; t0 < T; t0 += nwarps * TT) {
+    for (int t0 = tfirst; t0 < T; t0 += nwarps * TT) {
         float acc[32], accn[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) { acc[i] = 0.f; accn[i] = 0.f; }
         // software-pipelined: the next chunk's 16-byte loads are in flight while
         // the current chunk is multiplied
-        uint4 cur[TT];
+        if (t0 != tfirst) {
 #pragma unroll
-        for (int tt = 0; tt < TT; ++tt)
-            cur[tt] = (lane < HB && t0 + tt < T) ? ld_nc_v4(x + (size_t)(t0 + tt) * H + lane * 8)
-                                                 : make_uint4(0, 0, 0, 0);
+            for (int tt = 0; tt < TT; ++tt)
+                cur[tt] = (lane < HB && t0 + tt < T) ? ld_nc_v4(x + (size_t)(t0 + tt) * H + lane * 8)
+                                                     : make_uint4(0, 0, 0, 0);
+        }
         for (int hb = lane; hb < HB; hb += 32) {
             uint4 nxt[TT];
             const int hn = hb + 32;

@@ -276,20 +276,20 @@ router_wgrad_partial2(const __nv_bfloat16* __restrict__ x, const float* __restri
     const int chunk = blockIdx.y;
     const int t0 = chunk * kWgTok;
     const int h0 = blockIdx.x * 256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hl = lane * 8;  // local h of this lane
+    uint4 u[kWg2Tok];         // x loads first: their latency overlaps the dh staging below
+#pragma unroll
+    for (int i = 0; i < kWg2Tok; ++i) {
+        const int t = t0 + warp * kWg2Tok + i;
+        u[i] = (t < T && h0 + hl < H) ? ld_nc_v4(x + (size_t)t * H + h0 + hl) : make_uint4(0, 0, 0, 0);
+    }
     for (int i = threadIdx.x; i < kWgTok * EP; i += blockDim.x) {
         const int tt = i / EP, e = i % EP;
         const int t = t0 + tt;
         ds[i] = (t < T && e < E) ? d[(size_t)t * E + e] : 0.f;
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int hl = lane * 8;  // local h of this lane
-    uint4 u[kWg2Tok];
-#pragma unroll
-    for (int i = 0; i < kWg2Tok; ++i) {
-        const int t = t0 + warp * kWg2Tok + i;
-        u[i] = (t < T && h0 + hl < H) ? ld_nc_v4(x + (size_t)t * H + h0 + hl) : make_uint4(0, 0, 0, 0);
-    }
     float acc[8][EP];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
