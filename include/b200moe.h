@@ -189,6 +189,67 @@ int b200moe_gemm_set_debug(int flags);         /* diagnostics: bit 0 skips wgrad
 int b200moe_upcycle_copy(const void* w1, const void* w2, const void* w3, int src_is_fp32, int H, int F, int E_local,
                          void* W1, void* W2, void* W3, cudaStream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * The transformer step around the MoE layer (model.cu).
+ * Residual stream fp32 [T, H]; normalised activations bf16 [T, H].
+ * ------------------------------------------------------------------------- */
+
+/* x_out = x + delta (delta bf16, optional: NULL = no add, x_out unused);
+ * y = rmsnorm(x_out) * gain (bf16); rstd[T] = (mean(x_out^2) + eps)^-1/2.
+ * Replaces moefold/tensor.py:307-313 (rmsnorm forward) fused with the block's
+ * residual add (moefold/model.py:151,156). */
+int b200moe_rmsnorm_fwd(const float* x, const void* delta, const float* gain, int T, int H, float eps, float* x_out,
+                        void* y, float* rstd, cudaStream_t stream);
+/* dx = rmsnorm'(dy) + dres (dres optional), written as fp32 (dx) and/or bf16
+ * (dx_bf16); dgain[H] = sum_t dy*x*rstd.  workspace >= ceil(T/32) * H floats.
+ * Replaces moefold/tensor.py:314-319. */
+int b200moe_rmsnorm_bwd(const void* dy, const float* x, const float* rstd, const float* gain, const float* dres, int T,
+                        int H, float* dx, void* dx_bf16, float* dgain, float* workspace, cudaStream_t stream);
+/* out[t] = table[ids[t]] (fp32); ids outside [0, V) set *err_flag = 1.
+ * Replaces moefold/tensor.py:324-331. */
+int b200moe_embedding_fwd(const float* table, const int64_t* ids, int T, int H, int V, float* out, int* err_flag,
+                          cudaStream_t stream);
+/* grad[seg_id[s]] = sum over i in [seg_start[s], seg_start[s+1]) of g[order[i]]
+ * in order (order = stable argsort of the ids); other rows untouched.
+ * Replaces the np.add.at of moefold/tensor.py:333-336. */
+int b200moe_embedding_bwd(const float* g, const int* order, const int* seg_start, const int* seg_id, int n_seg, int H,
+                          float* grad, cudaStream_t stream);
+/* nll[t] = logsumexp(logits[t]) - logits[t, targets[t]], lse[t], loss[0] =
+ * mean(nll); logits bf16 [T, V].  Replaces moefold/tensor.py:340-359. */
+int b200moe_cross_entropy_fwd(const void* logits, const int64_t* targets, int T, int V, float* nll, float* lse,
+                              float* loss, int* err_flag, cudaStream_t stream);
+/* dlogits = (softmax(logits) - onehot(targets)) * dloss[0] / T (bf16).
+ * Replaces moefold/tensor.py:361-364. */
+int b200moe_cross_entropy_bwd(const void* logits, const int64_t* targets, const float* lse, const float* dloss, int T,
+                              int V, void* dlogits, cudaStream_t stream);
+
+#define B200MOE_OPT_ADAM 0 /* moefold/train.py:161-171 */
+#define B200MOE_OPT_SGD 1  /* moefold/train.py:172-176 */
+
+/* One optimizer tensor: fp32 master `param`, moments m (and v for Adam),
+ * gradient (fp32 or bf16), optional bf16 compute copy refreshed in place. */
+typedef struct {
+    float* param;
+    float* m;
+    float* v;
+    const void* grad;
+    void* shadow;
+    long long n;
+    int grad_bf16;
+    int reserved;
+} b200moe_opt_tensor;
+
+/* Elements per chunk of the optimizer's work list. */
+int b200moe_optimizer_chunk(void);
+/* One step over every tensor of `tensors` (device array); the work list is
+ * n_chunks (tensor index, element offset) pairs of b200moe_optimizer_chunk()
+ * elements.  Scalars are the float32-rounded constants of the reference's
+ * expressions (1-beta, 1-beta^t).  Replaces moefold/train.py:_Optimizer.step. */
+int b200moe_optimizer_step(const b200moe_opt_tensor* tensors, const int* chunk_tensor, const long long* chunk_off,
+                           int n_chunks, int kind, float lr, float beta1, float one_minus_beta1, float beta2,
+                           float one_minus_beta2, float eps, float bias_corr1, float bias_corr2, float momentum,
+                           cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

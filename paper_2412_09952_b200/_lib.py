@@ -24,6 +24,7 @@ LAYOUT_COMPACT, LAYOUT_FIXED = 0, 1
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _I64 = ctypes.c_int64
+_F = ctypes.c_float
 
 # name -> argtypes (every function returns int status)
 SIGNATURES = {
@@ -54,6 +55,14 @@ SIGNATURES = {
     "b200moe_gemm_set_debug": [_I],
     "b200moe_upcycle_copy": [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P],
     "b200moe_version": [],
+    "b200moe_rmsnorm_fwd": [_P, _P, _P, _I, _I, _F, _P, _P, _P, _P],
+    "b200moe_rmsnorm_bwd": [_P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P],
+    "b200moe_embedding_fwd": [_P, _P, _I, _I, _I, _P, _P, _P],
+    "b200moe_embedding_bwd": [_P, _P, _P, _P, _I, _I, _P, _P],
+    "b200moe_cross_entropy_fwd": [_P, _P, _I, _I, _P, _P, _P, _P, _P],
+    "b200moe_cross_entropy_bwd": [_P, _P, _P, _P, _I, _I, _P, _P],
+    "b200moe_optimizer_chunk": [],
+    "b200moe_optimizer_step": [_P, _P, _P, _I, _I, _F, _F, _F, _F, _F, _F, _F, _F, _F, _P],
 }
 
 _lib = None
@@ -96,6 +105,8 @@ KERNELS_PER_CALL = {
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_upcycle_copy": 3,
     "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 3,
+    "b200moe_rmsnorm_fwd": 1, "b200moe_rmsnorm_bwd": 2, "b200moe_embedding_fwd": 1, "b200moe_embedding_bwd": 1,
+    "b200moe_cross_entropy_fwd": 2, "b200moe_cross_entropy_bwd": 1, "b200moe_optimizer_step": 1,
 }
 
 

@@ -1,0 +1,203 @@
+"""GPU parity for SURVEY 8(f) row 1 (the transformer step around the MoE layer):
+the model.cu kernels against the oracle / reference goldens, and the whole
+2-layer model (dense FFN layer + E4T2 MoE layer) forward, backward and a
+5-step training run against the reference's own numbers."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import model_oracle as MO
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+OPS = os.path.join(GOLDEN, "model_ops.npz")
+TINY = os.path.join(GOLDEN, "model_tiny.npz")
+
+
+def rel(a, b):
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def ops():
+    return np.load(OPS)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return np.load(TINY)
+
+
+def cuda(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def test_rmsnorm_fwd_bwd(ops):
+    from paper_2412_09952_b200.tensor import rmsnorm
+    x = cuda(ops["rms_x"]).requires_grad_(True)
+    g = cuda(ops["rms_gain"]).requires_grad_(True)
+    y = rmsnorm(x, g)
+    assert y.dtype == torch.bfloat16
+    y.backward(cuda(ops["rms_dy"], torch.bfloat16))
+    assert rel(y.float().cpu(), ops["rms_y"]) < 4e-3          # bf16 output rounding
+    assert rel(x.grad.cpu(), ops["rms_dx"]) < 1e-5
+    assert rel(g.grad.cpu(), ops["rms_dgain"]) < 1e-5
+
+
+def test_add_rmsnorm_matches_oracle():
+    from paper_2412_09952_b200.tensor import add_rmsnorm
+    r = np.random.default_rng(3)
+    x = r.standard_normal((300, 512)).astype(np.float32)
+    d = r.standard_normal((300, 512)).astype(np.float32)
+    gain = (1 + 0.1 * r.standard_normal(512)).astype(np.float32)
+    dt = cuda(d, torch.bfloat16)
+    xs = x + dt.float().cpu().numpy()
+    xt = cuda(x).requires_grad_(True)
+    dtt = dt.clone().requires_grad_(True)
+    gt = cuda(gain).requires_grad_(True)
+    xo, y = add_rmsnorm(xt, dtt, gt)
+    dy = r.standard_normal((300, 512)).astype(np.float32)
+    dxo = r.standard_normal((300, 512)).astype(np.float32)
+    dyt = cuda(dy, torch.bfloat16)
+    torch.autograd.backward([xo, y], [cuda(dxo), dyt])
+    ry, rr = MO.rmsnorm_fwd(xs, gain)
+    rdx, rdg = MO.rmsnorm_bwd(xs, gain, rr, dyt.float().cpu().numpy())
+    np.testing.assert_array_equal(xo.detach().cpu().numpy(), xs)
+    assert rel(y.float().cpu(), ry) < 4e-3
+    assert rel(xt.grad.cpu(), rdx + dxo) < 1e-5
+    assert rel(dtt.grad.float().cpu(), rdx + dxo) < 4e-3
+    assert rel(gt.grad.cpu(), rdg) < 1e-5
+
+
+def test_cross_entropy_fwd_bwd(ops):
+    from paper_2412_09952_b200.tensor import cross_entropy
+    lg = cuda(ops["ce_logits"], torch.bfloat16).requires_grad_(True)   # bf16-exact values
+    loss = cross_entropy(lg, ops["ce_targets"])
+    loss.backward()
+    assert abs(float(loss.detach()) - float(ops["ce_loss"])) <= 1e-5 * abs(float(ops["ce_loss"]))
+    assert rel(lg.grad.float().cpu(), ops["ce_dlogits"]) < 4e-3
+
+
+def test_cross_entropy_large_vocab_matches_oracle():
+    from paper_2412_09952_b200.tensor import cross_entropy
+    r = np.random.default_rng(5)
+    T, V = 64, 128256
+    lg = cuda(4 * r.standard_normal((T, V)).astype(np.float32), torch.bfloat16).requires_grad_(True)
+    tg = r.integers(0, V, T)
+    loss = cross_entropy(lg, tg)
+    loss.backward()
+    ref_loss, p = MO.cross_entropy_fwd(lg.detach().float().cpu().numpy(), tg)
+    assert abs(float(loss) - float(ref_loss)) <= 1e-5 * abs(float(ref_loss))
+    assert rel(lg.grad.float().cpu(), MO.cross_entropy_bwd(p, tg)) < 4e-3
+
+
+def test_embedding_fwd_bwd_bit_exact(ops):
+    from paper_2412_09952_b200.tensor import embedding
+    table = cuda(ops["emb_table"]).requires_grad_(True)
+    out = embedding(table, ops["emb_ids"])
+    out.backward(cuda(ops["emb_g"]))
+    np.testing.assert_array_equal(out.detach().cpu().numpy(), ops["emb_out"])
+    np.testing.assert_array_equal(table.grad.cpu().numpy(), ops["emb_dtable"])   # token-order sums, like np.add.at
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_optimizer_kernel_bit_exact(ops, kind):
+    from paper_2412_09952_b200.train import Optimizer
+    params = {n: cuda(ops[f"opt_{kind}_{n}_p0"]) for n in ("a", "b")}
+    opt = Optimizer(kind, params)
+    for step in range(3):
+        for n in params:
+            params[n].grad = cuda(ops[f"opt_{kind}_{n}_grads"][step])
+        opt.step(1e-3 * (step + 1))
+        for n in params:
+            np.testing.assert_array_equal(params[n].cpu().numpy(), ops[f"opt_{kind}_{n}_traj"][step])
+
+
+def test_optimizer_bf16_shadow_and_bf16_grads():
+    from paper_2412_09952_b200.train import Optimizer
+    r = np.random.default_rng(9)
+    w = cuda(r.standard_normal((3, 1000)).astype(np.float32), torch.bfloat16)
+    master = w.float().cpu().numpy()
+    opt = Optimizer("adam", {"w": w})
+    m, v = np.zeros_like(master), np.zeros_like(master)
+    for t in range(1, 4):
+        g = cuda(r.standard_normal((3, 1000)).astype(np.float32), torch.bfloat16)
+        w.grad = g
+        opt.step(1e-2)
+        MO.adam_step(master, m, v, g.float().cpu().numpy(), np.float32(1e-2), t)
+        np.testing.assert_array_equal(opt.master["w"].cpu().numpy(), master)
+        assert torch.equal(w.cpu(), torch.from_numpy(master).to(torch.bfloat16))
+
+
+def _tiny_moe(cfg):
+    import paper_2412_09952_b200 as P
+    m = P.ModelConfig(**cfg["model"])
+    g = cfg["gate"]
+    dense = P.init_dense(m, seed=3)
+    return P.upcycle_full(dense, g["n_experts"], g["top_k"], moe_layers=tuple(g["moe_layers"]),
+                          router_seed=g["router_seed"], capacity_factor=g["capacity_factor"])
+
+
+def test_tiny_model_forward_backward_matches_reference(tiny):
+    import paper_2412_09952_b200 as P
+    from paper_2412_09952_b200.train import prepare_for_training, trainable_leaves
+    cfg = json.loads(str(tiny["config"]))
+    moe = _tiny_moe(cfg)
+    prepare_for_training(moe)
+    tokens = tiny["tokens"]
+    inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
+    fwd = P.forward_with_stats(moe, inputs, training=True)
+    loss = P.cross_entropy(fwd.logits, targets)
+    for g in fwd.gates:
+        loss = loss + (cfg["train"]["aux"] / len(fwd.gates)) * P.importance_penalty(g)
+    loss.backward()
+    assert rel(fwd.logits.float().cpu(), tiny["logits"]) < 2e-2
+    assert abs(float(loss) - float(tiny["loss"])) < 2e-3 * float(tiny["loss"])
+    st = fwd.stats[0]
+    assert int(np.abs(st.assigned - tiny["assigned"]).sum()) <= 8     # a few near-tie routing flips allowed
+    leaves = trainable_leaves(moe)
+    E = cfg["gate"]["n_experts"]
+    checked = 0
+    for name, t in moe.tensors.items():
+        ref = tiny[f"grad/{name}"]
+        if ".experts." in name:
+            li, e, w = name.split(".")[1], int(name.split(".")[4]), name.split(".")[5]
+            W = leaves[f"layers.{li}.moe.experts.{w.upper()}"]
+            got = W.grad[e].t().float().cpu()
+        else:
+            g = leaves[name].grad
+            got = np.zeros(ref.shape) if g is None else g.float().cpu()
+        tol = 5e-2 if ("experts" in name or "router" in name) else 3e-2
+        assert rel(got, ref) < tol, (name, rel(got, ref))
+        checked += 1
+    assert checked == len(moe.tensors) and E == 4
+
+
+def test_tiny_model_training_run_tracks_reference(tiny, tmp_path):
+    import paper_2412_09952_b200 as P
+    cfg = json.loads(str(tiny["config"]))
+    t = cfg["train"]
+    moe = _tiny_moe(cfg)
+    spec = P.BlendSpec(tuple(tuple(s) for s in t["blend"][0]), t["blend"][1])
+    lo, hi, wu, tot = t["lr"]
+    tc = P.TrainConfig(steps=t["steps"], schedule=P.Schedule(lo, hi, wu, tot), blend=spec,
+                       batch_size=t["batch_size"], seq_len=t["seq_len"], aux_loss_coeff=t["aux"])
+    m = P.train(moe, tc, run_id="tiny")
+    np.testing.assert_array_equal(m.lr, tiny["train_lr"])
+    np.testing.assert_allclose(m.loss, tiny["train_loss"], rtol=3e-3)
+    np.testing.assert_allclose(m.load_entropy, tiny["train_entropy"], atol=2e-2)
+    m.write_routing_csv(str(tmp_path / "r.csv"), cfg["gate"]["n_experts"])
+    m.write_metrics_csv(str(tmp_path / "m.csv"))
+    got = (tmp_path / "r.csv").read_text().splitlines()
+    ref = str(tiny["routing_csv"]).splitlines()
+    assert got[0] == ref[0] and len(got) == len(ref)
+    assert (tmp_path / "m.csv").read_text().splitlines()[0] == str(tiny["metrics_csv"]).splitlines()[0]

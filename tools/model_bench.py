@@ -1,0 +1,133 @@
+"""Model-level training-step benchmark:
+a Llama-3-8B-shape E8T2 model with `--layers` transformer blocks (all MoE),
+one full step = forward + cross-entropy + aux loss + backward + Adam over every
+parameter, on one GPU.  Weights are random-init on the device (synthetic), the
+batch is one sequence of `--seq` random token ids.
+
+Prints one JSON line: tokens/s, ms/step, model MFU with the reference's
+forward_flops(..., "6P") convention (plan.py:195-215) with the expert term
+counted on kept slots, and a per-phase split measured with CUDA events.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2412_09952_b200 as P  # noqa: E402
+from paper_2412_09952_b200.train import Optimizer, prepare_for_training  # noqa: E402
+
+
+def model_flops(cfg, gate, tokens: int, kept_slots: int) -> float:
+    """6 x matmul MACs of plan.py:forward_flops with S (kept slots) in place of
+    tokens * top_k for the expert FFNs."""
+    H, F, E = cfg.hidden, cfg.ffn_hidden, gate.n_experts
+    attn = 2 * H * H + 2 * H * cfg.kv_width
+    per_layer = tokens * (attn + H * E) + kept_slots * 3 * H * F
+    macs = tokens * H * cfg.vocab + cfg.layers * per_layer
+    macs += cfg.layers * 2 * tokens * min(tokens, cfg.seq_len) * H
+    return 6.0 * macs
+
+
+def random_dense(cfg, device):
+    g = torch.Generator(device=device)
+    g.manual_seed(0)
+    tensors = {}
+    for name, shape in sorted(P.dense_schema(cfg).items()):
+        if name.endswith("norm"):
+            tensors[name] = torch.ones(shape, dtype=torch.float32, device=device)
+        else:
+            tensors[name] = torch.randn(shape, generator=g, dtype=torch.float32, device=device) * 0.02
+    return P.DenseCheckpoint(config=cfg, tensors=tensors)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=2)
+    ap.add_argument("--seq", type=int, default=8192)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--cf", type=float, default=1.0)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--small", action="store_true", help="tiny shape for a smoke run")
+    a = ap.parse_args()
+    dev = torch.device("cuda")
+    if a.small:
+        cfg = P.ModelConfig(vocab=1024, hidden=512, layers=a.layers, heads=8, kv_heads=2, ffn_hidden=1024,
+                            seq_len=a.seq)
+    else:
+        cfg = P.ModelConfig(vocab=128256, hidden=4096, layers=a.layers, heads=32, kv_heads=8, ffn_hidden=14336,
+                            seq_len=a.seq)
+    dense = random_dense(cfg, dev)
+    moe = P.upcycle_full(dense, 8, 2, router_seed=1, capacity_factor=a.cf)
+    del dense
+    opt = Optimizer("adam", prepare_for_training(moe))
+    rng = np.random.default_rng(0)
+    tokens = rng.integers(0, cfg.vocab, (a.batch, a.seq + 1))
+    inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
+    T = a.batch * a.seq
+    aux = 0.01
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record()
+        fwd = P.forward_with_stats(moe, inputs, training=True)
+        loss = P.cross_entropy(fwd.logits, targets)
+        for g in fwd.gates:
+            loss = loss + (aux / len(fwd.gates)) * P.importance_penalty(g)
+        if ev is not None:
+            ev[1].record()
+        for p in opt.params.values():
+            p.grad = None
+        loss.backward()
+        if ev is not None:
+            ev[2].record()
+        opt.step(1e-4)
+        if ev is not None:
+            ev[3].record()
+        return loss, fwd.stats
+
+    for _ in range(a.warmup):
+        loss, stats = step()
+    torch.cuda.synchronize()
+    kept = sum(int(s.assigned.sum()) for s in stats) // cfg.layers
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
+    t0 = time.perf_counter()
+    for i in range(a.steps):
+        loss, _ = step(evs[i])
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / a.steps
+    ms = float(np.median([e[0].elapsed_time(e[3]) for e in evs]))
+    split = {k: round(float(np.median([e[i].elapsed_time(e[i + 1]) for e in evs])), 3)
+             for i, k in enumerate(("forward", "backward", "optimizer"))}
+    flops = model_flops(cfg, moe.gate, T, kept)
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))
+    n_params = sum(t.numel() for t in opt.params.values())
+    out = {
+        "metric": f"Llama-3-8B-shape E8T2 {cfg.layers}-layer training step tokens/s",
+        "value": round(T / (ms * 1e-3), 1), "unit": "tokens/s", "ms_per_step": round(ms, 3),
+        "wall_ms_per_step": round(wall * 1e3, 3), "phases_ms": split,
+        "mfu": {"measured_peak": round(flops / (ms * 1e-3) / (peaks["bf16_tflops"] * 1e12), 4),
+                "spec_2250": round(flops / (ms * 1e-3) / 2250e12, 4), "flops_per_step": flops,
+                "convention": "6P (plan.py:forward_flops) with kept slots for the expert FFNs"},
+        "loss": float(loss.detach()), "kept_slots_per_layer": kept, "params": n_params,
+        "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
+        "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
+                   "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": 8,
+                   "top_k": 2, "capacity_factor": a.cf, "optimizer": "adam (fp32 masters)"},
+        "data": "synthetic (random token ids, random-init weights)",
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
