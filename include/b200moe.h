@@ -250,6 +250,18 @@ int b200moe_optimizer_step(const b200moe_opt_tensor* tensors, const int* chunk_t
                            float one_minus_beta2, float eps, float bias_corr1, float bias_corr2, float momentum,
                            cudaStream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Checkpoint payload checksums (crc32c.cu).
+ * ------------------------------------------------------------------------- */
+
+/* Bytes of device workspace b200moe_crc32c needs. */
+long long b200moe_crc32c_workspace_bytes(void);
+/* *out (device uint32) = CRC32C (Castagnoli, init/xorout 0xFFFFFFFF) of the
+ * nbytes at `data` (device, 16-byte aligned).  Replaces the pure-Python
+ * slicing-by-8 crc32c of moefold/checkpoint.py:60-78 used on every tensor
+ * payload by save/load (checkpoint.py:108-118, 215-216). */
+int b200moe_crc32c(const void* data, long long nbytes, unsigned int* out, void* workspace, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,13 +80,14 @@ def _npexp_lib():
 
 
 def build_oracle() -> str:
-    """Compile oracle/npexp.c (the checker) into oracle/build/libnpexp.so."""
+    """Compile oracle/npexp.c and oracle/crc32c.c (the checkers) into
+    oracle/build/libnpexp.so."""
     import subprocess
     here = os.path.dirname(os.path.abspath(__file__))
     os.makedirs(os.path.join(here, "build"), exist_ok=True)
     out = os.path.join(here, "build", "libnpexp.so")
     subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
-                           os.path.join(here, "npexp.c"), "-o", out, "-lm"])
+                           os.path.join(here, "npexp.c"), os.path.join(here, "crc32c.c"), "-o", out, "-lm"])
     return out
 
 
