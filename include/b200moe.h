@@ -254,10 +254,13 @@ int b200moe_optimizer_step(const b200moe_opt_tensor* tensors, const int* chunk_t
  * Checkpoint payload checksums (crc32c.cu).
  * ------------------------------------------------------------------------- */
 
-/* Bytes of device workspace b200moe_crc32c needs. */
+/* Bytes of device workspace b200moe_crc32c needs (accumulator + tables). */
 long long b200moe_crc32c_workspace_bytes(void);
+/* Build the fixed lookup tables into a workspace (once per workspace). */
+int b200moe_crc32c_init(void* workspace, cudaStream_t stream);
 /* *out (device uint32) = CRC32C (Castagnoli, init/xorout 0xFFFFFFFF) of the
- * nbytes at `data` (device, 16-byte aligned).  Replaces the pure-Python
+ * nbytes at `data` (device, 16-byte aligned), using a workspace prepared by
+ * b200moe_crc32c_init; calls sharing a workspace must be stream-ordered.  Replaces the pure-Python
  * slicing-by-8 crc32c of moefold/checkpoint.py:60-78 used on every tensor
  * payload by save/load (checkpoint.py:108-118, 215-216). */
 int b200moe_crc32c(const void* data, long long nbytes, unsigned int* out, void* workspace, cudaStream_t stream);

@@ -64,6 +64,7 @@ SIGNATURES = {
     "b200moe_optimizer_chunk": [],
     "b200moe_optimizer_step": [_P, _P, _P, _I, _I, _F, _F, _F, _F, _F, _F, _F, _F, _F, _P],
     "b200moe_crc32c_workspace_bytes": [],
+    "b200moe_crc32c_init": [_P, _P],
     "b200moe_crc32c": [_P, _I64, _P, _P, _P],
 }
 
@@ -110,7 +111,7 @@ KERNELS_PER_CALL = {
     "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 3,
     "b200moe_rmsnorm_fwd": 1, "b200moe_rmsnorm_bwd": 2, "b200moe_embedding_fwd": 1, "b200moe_embedding_bwd": 1,
     "b200moe_cross_entropy_fwd": 2, "b200moe_cross_entropy_bwd": 1, "b200moe_optimizer_step": 1,
-    "b200moe_crc32c": 2,
+    "b200moe_crc32c": 2, "b200moe_crc32c_init": 1,
 }
 
 

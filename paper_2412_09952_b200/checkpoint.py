@@ -84,12 +84,29 @@ def _as_bytes_tensor(data) -> torch.Tensor:
     return t
 
 
+_WS: dict = {}
+
+
+def _crc_workspace(device) -> torch.Tensor:
+    """Per-device, per-stream workspace holding the kernel's lookup tables."""
+    dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = torch.empty(_lib.load().b200moe_crc32c_workspace_bytes(), dtype=torch.uint8, device=dev)
+        _lib.call("b200moe_crc32c_init", ws.data_ptr(), _lib.stream_ptr())
+        _WS[key] = ws
+    return ws
+
+
 class _CRC:
     """Batches device CRCs: one uint32 slot per payload, one D2H at the end."""
 
     def __init__(self, n: int, device="cuda"):
         self.out = torch.zeros(max(n, 1), dtype=torch.int64, device=device)
-        self._ws = torch.empty(_lib.load().b200moe_crc32c_workspace_bytes(), dtype=torch.uint8, device=device)
+        self._ws = _crc_workspace(device)
         self._keep = []
 
     def add(self, i: int, t: torch.Tensor) -> None:

@@ -2,22 +2,30 @@
 // (moefold/checkpoint.py:40-78: crc32c of every tensor payload, check value
 // crc32c("123456789") = 0xE3069283).  SURVEY 8(f) row 3.
 //
-// A CRC without init/xorout ("raw") is linear over GF(2), and
-// raw(A || B) = shift(raw(A), |B|) ^ raw(B), where shift(c, L) runs the
-// register over L zero bytes -- a fixed 32x32 bit matrix per L.  Leading zero
-// bytes leave a raw CRC of 0 unchanged, so the buffer is treated as if
-// front-padded with zeros to a whole number of equal blocks, and the standard
-// init 0xFFFFFFFF is folded in by inverting the first 4 data bytes.
+// A CRC without init/xorout ("raw") is linear over GF(2):
+//   raw(A || B) = shift(raw(A), |B|) ^ raw(B)
+// where shift(c, L) runs the register over L zero bytes (a 32x32 bit matrix).
+// Leading zero bytes leave a raw CRC of 0 unchanged, so the buffer is treated
+// as front-padded with zeros to a whole number of equal per-warp ranges, and
+// the standard init 0xFFFFFFFF is folded in by inverting the first 4 bytes.
 //
-//   crc_blocks  grid of blocks, each owning a contiguous run of 16 KB tiles.
-//               A tile is loaded coalesced into shared memory (segment stride
-//               17 words: conflict-free), each of the 256 threads computes the
-//               raw CRC of its 64-byte segment (slicing-by-4 tables in shared
-//               memory), a 8-level tree of shift matrices folds the 256
-//               segment CRCs into the tile CRC, and the block folds its tiles.
-//   crc_finish  one thread folds the block CRCs, runs the (<16 byte) tail
-//               byte-wise and applies the final xor.
-// HBM-bound: every byte is read once.
+//   crc_warp_kernel  each warp owns a contiguous range and walks it in 2 KB
+//                    steps of eight 512-byte rows (the next step's loads in
+//                    flight while the current one is hashed); every load is a fully
+//                    coalesced 16 bytes per lane (lane j takes bytes
+//                    [16j, 16j+16) of each row).  A lane's eight 16-byte pieces
+//                    are independent slicing-by-4 chains (tables replicated
+//                    32x in shared memory: replica `lane` lives in bank
+//                    `lane`, so the data-dependent lookups never conflict);
+//                    the lane folds them and its running value with
+//                    table-driven shifts (A = shift(A, 4 KB) ^ XOR_q
+//                    shift(p_q, (7-q) rows)), the warp folds
+//                    its lanes with shift((31-j)*16), shifts the range CRC into
+//                    place with the binary decomposition of its distance to the
+//                    end, and atomicXor folds the warps (XOR commutes: the
+//                    result is deterministic).
+//   crc_finish       one thread runs the (<16 byte) tail and the final xor.
+// HBM-bound by design: every byte is read once, in 8 KB coalesced runs.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -27,99 +35,138 @@
 namespace b200moe {
 
 constexpr uint32_t kPoly = 0x82F63B78u;   // reflected Castagnoli polynomial
-constexpr int kCrcThreads = 256;
-constexpr int kSegBytes = 64;
-constexpr int kTileBytes = kCrcThreads * kSegBytes;   // 16 KB
-constexpr int kSegWords = kSegBytes / 4;
-constexpr int kSegStride = kSegWords + 1;             // 17 words: conflict-free
-constexpr int kMaxCrcBlocks = kNumSMs * 8;
-constexpr int kLevels = 8;                            // log2(kCrcThreads)
+constexpr int kCrcThreads = 512;
+constexpr int kCrcWarps = kCrcThreads / 32;
+constexpr int kReps = 32;                 // table replicas (one per bank)
+constexpr int kPiece = 16;                // bytes per lane per row (one coalesced 16-byte load)
+constexpr int kRow = 32 * kPiece;         // 512 bytes per warp row
+constexpr int kChains = 8;                // rows per step: independent chains (ILP)
+constexpr int kStep = kChains * kRow;     // 2 KB per warp step
+// T[4][256][kReps] | S[kChains][4][256] (shift by kStep, then kChains-1 .. 1 rows) | L[32][33] | P[40][32]
+constexpr size_t kCrcSmem = (size_t)((4 * 256 * kReps + kChains * 4 * 256 + 32 * 33 + 40 * 32 + 3) / 4 * 4) * 4;
 
-// Shift matrices: lvl[l] = shift by kSegBytes << l bytes, tile = shift by
-// kTileBytes, block = shift by one block's bytes.  Column j = image of bit j.
-struct CrcMats {
-    uint32_t lvl[kLevels][32];
-    uint32_t tile[32];
-    uint32_t block[32];
-};
-
-__host__ __device__ inline uint32_t mat_apply(const uint32_t* m, uint32_t c) {
+__host__ __device__ inline uint32_t mat_apply(const uint32_t* m, uint32_t c, int stride = 1) {
     uint32_t r = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) r ^= m[j] & (0u - ((c >> j) & 1u));
+    for (int j = 0; j < 32; ++j) r ^= m[j * stride] & (0u - ((c >> j) & 1u));
     return r;
 }
 
-__device__ __forceinline__ void build_tables(uint32_t (*T)[256]) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+__device__ __forceinline__ uint32_t crc_word(const uint32_t* __restrict__ T, uint32_t c, uint32_t w, int lane) {
+    c ^= w;
+    return T[(3 * 256 + (c & 0xFF)) * kReps + lane] ^ T[(2 * 256 + ((c >> 8) & 0xFF)) * kReps + lane] ^
+           T[(1 * 256 + ((c >> 16) & 0xFF)) * kReps + lane] ^ T[(0 * 256 + (c >> 24)) * kReps + lane];
+}
+
+// Fixed tables, built once into the caller's workspace by crc_init_kernel:
+// slicing tables replicated per bank, the step / row shift tables and the
+// lane-fold matrices (row stride 33: conflict-free), laid out exactly as the
+// kernel's shared memory so each block copies them with 16-byte loads.
+constexpr int kPowBits = 40;           // P[b] = shift by kStep << b bytes
+constexpr int kTabWords = 4 * 256 * kReps + kChains * 4 * 256 + 32 * 33 + kPowBits * 32;
+constexpr int kTabWordsPadded = (kTabWords + 3) / 4 * 4;
+constexpr long long kWsTables = 256;   // byte offset of the tables in the workspace (after the accumulator)
+
+struct FixedMats {
+    uint32_t step[kChains][32];      // shift by kStep, then by kChains-1 .. 1 rows
+    uint32_t lane[32 * 32];          // lane[j] = shift by (31 - j) * kPiece bytes
+    uint32_t pow[kPowBits][32];      // pow[b] = shift by kStep << b bytes
+};
+
+__global__ void crc_init_kernel(const __grid_constant__ FixedMats mats, uint32_t* __restrict__ tab) {
+    uint32_t* T = tab;
+    uint32_t* S = T + 4 * 256 * kReps;
+    uint32_t* L = S + kChains * 4 * 256;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 256; i += gridDim.x * blockDim.x) {
+        uint32_t t[4];
         uint32_t c = i;
         for (int k = 0; k < 8; ++k) c = (c & 1) ? (c >> 1) ^ kPoly : c >> 1;
-        T[0][i] = c;
-    }
-    __syncthreads();
-    for (int t = 1; t < 4; ++t) {
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) T[t][i] = T[0][T[t - 1][i] & 0xFF] ^ (T[t - 1][i] >> 8);
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kCrcThreads) crc_blocks_kernel(const uint8_t* __restrict__ data, long long body,
-                                                                 long long pad, int tiles_per_block,
-                                                                 const CrcMats mats, uint32_t* __restrict__ out) {
-    __shared__ uint32_t T[4][256];
-    __shared__ uint32_t seg[kCrcThreads * kSegStride];
-    __shared__ uint32_t part[kCrcThreads];
-    __shared__ uint32_t M[kLevels][32];
-    build_tables(T);
-    for (int i = threadIdx.x; i < kLevels * 32; i += blockDim.x) M[i / 32][i % 32] = mats.lvl[i / 32][i % 32];
-    uint32_t acc = 0;
-    const long long blk0 = (long long)blockIdx.x * tiles_per_block * kTileBytes;   // logical (padded) offset
-    for (int tile = 0; tile < tiles_per_block; ++tile) {
-        const long long t0 = blk0 + (long long)tile * kTileBytes;
-        // coalesced load of the tile; logical bytes before `pad` are zeros
-        __syncthreads();
-#pragma unroll
+        t[0] = c;
+        for (int k = 1; k < 4; ++k) {
+            uint32_t q = t[k - 1] & 0xFF;
+            for (int b = 0; b < 8; ++b) q = (q & 1) ? (q >> 1) ^ kPoly : q >> 1;
+            t[k] = q ^ (t[k - 1] >> 8);
+        }
         for (int k = 0; k < 4; ++k) {
-            const int q = threadIdx.x + k * kCrcThreads;   // uint4 index inside the tile
-            const long long lo = t0 + 16LL * q;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (lo >= pad) {
-                v = *reinterpret_cast<const uint4*>(data + (lo - pad));
-                if (lo == pad) v.x ^= 0xFFFFFFFFu;         // init 0xFFFFFFFF == invert the first 4 bytes
-            }
-            const int s = q >> 2, w = (q & 3) * 4;
-            uint32_t* dst = seg + s * kSegStride + w;
-            dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
+            for (int r = 0; r < kReps; ++r) T[(k * 256 + i) * kReps + r] = t[k];
+            for (int sh = 0; sh < kChains; ++sh)
+                S[(sh * 4 + k) * 256 + i] = mat_apply(mats.step[sh], (uint32_t)i << (8 * k));
         }
-        __syncthreads();
-        // raw CRC of this thread's 64-byte segment
-        uint32_t c = 0;
-        const uint32_t* src = seg + threadIdx.x * kSegStride;
-#pragma unroll
-        for (int j = 0; j < kSegWords; ++j) {
-            c ^= src[j];
-            c = T[3][c & 0xFF] ^ T[2][(c >> 8) & 0xFF] ^ T[1][(c >> 16) & 0xFF] ^ T[0][c >> 24];
-        }
-        // tree fold: left partner is shifted past the right one's bytes
-        part[threadIdx.x] = c;
-#pragma unroll
-        for (int l = 0; l < kLevels; ++l) {
-            __syncthreads();
-            const int stride = 1 << l;
-            uint32_t nv = 0;
-            const bool active = (threadIdx.x & ((stride << 1) - 1)) == 0;
-            if (active) nv = mat_apply(M[l], part[threadIdx.x]) ^ part[threadIdx.x + stride];
-            __syncthreads();
-            if (active) part[threadIdx.x] = nv;
-        }
-        if (threadIdx.x == 0) acc = mat_apply(mats.tile, acc) ^ part[0];
     }
-    if (threadIdx.x == 0) out[blockIdx.x] = acc;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 32 * 32; i += gridDim.x * blockDim.x)
+        L[(i / 32) * 33 + i % 32] = mats.lane[i];
+    uint32_t* P = L + 32 * 33;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kPowBits * 32; i += gridDim.x * blockDim.x)
+        P[i] = mats.pow[i / 32][i % 32];
 }
 
-__global__ void crc_finish_kernel(const uint32_t* __restrict__ blk, int nblocks, const CrcMats mats,
-                                  const uint8_t* __restrict__ tail, int tail_len, int have_body,
-                                  uint32_t* __restrict__ out) {
+__global__ void __launch_bounds__(kCrcThreads) crc_warp_kernel(const uint8_t* __restrict__ data, long long pad,
+                                                               long long range_bytes, long long nranges,
+                                                               const uint4* __restrict__ tab,
+                                                               uint32_t* __restrict__ acc) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    uint32_t* T = sm;                               // slicing tables, replicated
+    uint32_t* S = T + 4 * 256 * kReps;              // shift tables: S[s][k][b] = step[s](b << 8k)
+    uint32_t* L = S + kChains * 4 * 256;            // lane fold matrices, row stride 33 (conflict-free)
+    uint32_t* P = L + 32 * 33;                      // P[b] = shift by kStep << b
+    for (int i = threadIdx.x; i < kTabWordsPadded / 4; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = tab[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long gw = (long long)blockIdx.x * kCrcWarps + (threadIdx.x >> 5);
+    const long long nw = (long long)gridDim.x * kCrcWarps;
+    for (long long r = gw; r < nranges; r += nw) {
+        uint32_t A = 0;
+        const long long base = r * range_bytes + (long long)lane * kPiece;   // logical offset of row 0, step 0
+        auto ld = [&](long long lo) -> uint4 {
+            if (lo < pad) return make_uint4(0, 0, 0, 0);
+            uint4 v = __ldg(reinterpret_cast<const uint4*>(data + (lo - pad)));
+            if (lo == pad) v.x ^= 0xFFFFFFFFu;
+            return v;
+        };
+        uint4 v[kChains];          // chain q = this lane's 16 bytes of row q of the step
+#pragma unroll
+        for (int q = 0; q < kChains; ++q) v[q] = ld(base + (long long)q * kRow);
+        for (long long st = 0; st < range_bytes; st += kStep) {
+            uint4 nx[kChains];     // next step, in flight while this one is hashed
+            const bool more = st + kStep < range_bytes;
+#pragma unroll
+            for (int q = 0; q < kChains; ++q)
+                nx[q] = more ? ld(base + st + kStep + (long long)q * kRow) : make_uint4(0, 0, 0, 0);
+            uint32_t c[kChains];
+#pragma unroll
+            for (int q = 0; q < kChains; ++q) c[q] = crc_word(T, 0u, v[q].x, lane);
+#pragma unroll
+            for (int q = 0; q < kChains; ++q) c[q] = crc_word(T, c[q], v[q].y, lane);
+#pragma unroll
+            for (int q = 0; q < kChains; ++q) c[q] = crc_word(T, c[q], v[q].z, lane);
+#pragma unroll
+            for (int q = 0; q < kChains; ++q) c[q] = crc_word(T, c[q], v[q].w, lane);
+            // step = XOR_q shift(c_q, kChains-1-q rows);  A = shift(A, kStep) ^ step
+            uint32_t x = c[kChains - 1];
+#pragma unroll
+            for (int q = 0; q < kChains - 1; ++q) {
+                const uint32_t* Sq = S + (q + 1) * 1024;
+                x ^= Sq[c[q] & 0xFF] ^ Sq[256 + ((c[q] >> 8) & 0xFF)] ^ Sq[512 + ((c[q] >> 16) & 0xFF)] ^
+                     Sq[768 + (c[q] >> 24)];
+            }
+            A = S[A & 0xFF] ^ S[256 + ((A >> 8) & 0xFF)] ^ S[512 + ((A >> 16) & 0xFF)] ^ S[768 + (A >> 24)] ^ x;
+#pragma unroll
+            for (int q = 0; q < kChains; ++q) v[q] = nx[q];
+        }
+        uint32_t w = mat_apply(L + lane * 33, A);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w ^= __shfl_xor_sync(0xffffffffu, w, o);
+        if (lane == 0) {
+            // distance to the end in kStep units, applied bit by bit
+            const unsigned long long d = (unsigned long long)(nranges - 1 - r) * (unsigned long long)(range_bytes / kStep);
+            for (int b = 0; b < kPowBits && (d >> b); ++b)
+                if ((d >> b) & 1ull) w = mat_apply(P + b * 32, w);
+            if (w != 0) atomicXor(acc, w);
+        }
+    }
+}
+
+__global__ void crc_finish_kernel(uint32_t* __restrict__ acc, const uint8_t* __restrict__ tail, int tail_len,
+                                  int have_body, uint32_t* __restrict__ out) {
     __shared__ uint32_t T0[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         uint32_t c = i;
@@ -128,11 +175,8 @@ __global__ void crc_finish_kernel(const uint32_t* __restrict__ blk, int nblocks,
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    uint32_t c = 0xFFFFFFFFu;
-    if (have_body) {
-        c = 0;
-        for (int b = 0; b < nblocks; ++b) c = mat_apply(mats.block, c) ^ blk[b];
-    }
+    uint32_t c = have_body ? acc[0] : 0xFFFFFFFFu;
+    acc[0] = 0;   // ready for the next (stream-ordered) call on this workspace
     for (int i = 0; i < tail_len; ++i) c = T0[(c ^ tail[i]) & 0xFF] ^ (c >> 8);
     out[0] = c ^ 0xFFFFFFFFu;
 }
@@ -146,14 +190,13 @@ static void mat_mul(const uint32_t* a, const uint32_t* b, uint32_t* r) {   // r 
 
 // m = shift by `bytes` zero bytes
 static void mat_shift(long long bytes, uint32_t* m) {
-    uint32_t base[32], id[32];
+    uint32_t base[32];
     for (int j = 0; j < 32; ++j) {   // one zero byte
         uint32_t c = 1u << j;
         for (int k = 0; k < 8; ++k) c = (c & 1) ? (c >> 1) ^ kPoly : c >> 1;
         base[j] = c;
-        id[j] = 1u << j;
+        m[j] = 1u << j;
     }
-    memcpy(m, id, sizeof(id));
     while (bytes > 0) {
         if (bytes & 1) mat_mul(base, m, m);
         mat_mul(base, base, base);
@@ -167,30 +210,49 @@ using namespace b200moe;
 
 extern "C" {
 
-long long b200moe_crc32c_workspace_bytes(void) { return (long long)kMaxCrcBlocks * 4; }
+// workspace: [0, 4) the XOR accumulator, [256, ...) the fixed tables
+long long b200moe_crc32c_workspace_bytes(void) { return kWsTables + (long long)kTabWordsPadded * 4; }
+
+int b200moe_crc32c_init(void* workspace, cudaStream_t stream) {
+    FixedMats f;
+    uint32_t piece[32];
+    mat_shift(kStep, f.step[0]);
+    for (int q = 0; q < kChains - 1; ++q) mat_shift((long long)kRow * (kChains - 1 - q), f.step[q + 1]);
+    mat_shift(kPiece, piece);
+    mat_shift(0, f.lane + 31 * 32);
+    for (int j = 30; j >= 0; --j) mat_mul(piece, f.lane + (j + 1) * 32, f.lane + j * 32);
+    memcpy(f.pow[0], f.step[0], sizeof(f.pow[0]));
+    for (int b = 1; b < kPowBits; ++b) mat_mul(f.pow[b - 1], f.pow[b - 1], f.pow[b]);
+    cudaMemsetAsync(workspace, 0, 4, stream);
+    crc_init_kernel<<<8, 256, 0, stream>>>(f, (uint32_t*)((char*)workspace + kWsTables));
+    B200_CHECK_LAUNCH("crc32c_init");
+    return B200MOE_OK;
+}
 
 int b200moe_crc32c(const void* data, long long nbytes, unsigned int* out, void* workspace, cudaStream_t stream) {
     B200_CHECK_ARG(nbytes >= 0, B200MOE_ERR_SHAPE, "crc32c: negative length");
     B200_CHECK_ARG(nbytes == 0 || ((uintptr_t)data & 15) == 0, B200MOE_ERR_CONFIG,
                    "crc32c: buffer must be 16-byte aligned");
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(crc_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem);
+        attr = true;
+    }
     const long long body = nbytes & ~15LL;
     const int tail_len = (int)(nbytes - body);
-    const long long tiles = (body + kTileBytes - 1) / kTileBytes;
-    int tpb = 1, nblocks = 0;
-    if (tiles > 0) {
-        tpb = (int)((tiles + kMaxCrcBlocks - 1) / kMaxCrcBlocks);
-        nblocks = (int)((tiles + tpb - 1) / tpb);
+    uint32_t* acc = (uint32_t*)workspace;
+    if (body > 0) {
+        // one range per warp of a full-chip grid, whole kStep steps
+        const long long warps = (long long)kNumSMs * kCrcWarps;
+        const long long steps = (body + kStep - 1) / kStep;
+        const long long range = (steps + warps - 1) / warps * kStep;
+        const long long nranges = (body + range - 1) / range;
+        const long long blocks = (nranges + kCrcWarps - 1) / kCrcWarps;
+        crc_warp_kernel<<<(int)(blocks < kNumSMs ? blocks : kNumSMs), kCrcThreads, kCrcSmem, stream>>>(
+            (const uint8_t*)data, nranges * range - body, range, nranges,
+            (const uint4*)((const char*)workspace + kWsTables), acc);
     }
-    const long long padded = (long long)nblocks * tpb * kTileBytes;
-    CrcMats mats;   // a few microseconds of host GF(2) algebra per call
-    for (int l = 0; l < kLevels; ++l) mat_shift((long long)kSegBytes << l, mats.lvl[l]);
-    mat_shift(kTileBytes, mats.tile);
-    mat_shift((long long)tpb * kTileBytes, mats.block);
-    if (nblocks > 0)
-        crc_blocks_kernel<<<nblocks, kCrcThreads, 0, stream>>>((const uint8_t*)data, body, padded - body, tpb, mats,
-                                                               (uint32_t*)workspace);
-    crc_finish_kernel<<<1, 256, 0, stream>>>((const uint32_t*)workspace, nblocks, mats,
-                                             (const uint8_t*)data + body, tail_len, body > 0 ? 1 : 0, out);
+    crc_finish_kernel<<<1, 256, 0, stream>>>(acc, (const uint8_t*)data + body, tail_len, body > 0 ? 1 : 0, out);
     B200_CHECK_LAUNCH("crc32c");
     return B200MOE_OK;
 }

@@ -20,6 +20,7 @@ buf = torch.randint(0, 255, (n,), dtype=torch.uint8, device="cuda")
 out = torch.zeros(1, dtype=torch.int64, device="cuda")
 ws = torch.empty(_lib.load().b200moe_crc32c_workspace_bytes(), dtype=torch.uint8, device="cuda")
 s = _lib.stream_ptr()
+_lib.call("b200moe_crc32c_init", ws.data_ptr(), s)
 ts = []
 for i in range(a.reps + 2):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
