@@ -44,7 +44,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--tokens", type=int, default=8192)
-    p.add_argument("--cf", type=float, default=1.0)
+    p.add_argument("--cf", type=lambda v: None if v.lower() in ("none", "dropless") else float(v), default=1.0,
+                   help="capacity factor, or 'none' for dropless (moe.py:193-194)")
     p.add_argument("--router", default="mixtral")
     p.add_argument("--policy", default="position")
     p.add_argument("--cpu-tokens", type=int, default=512, help="bounded CPU sample (tokens per oracle step)")
