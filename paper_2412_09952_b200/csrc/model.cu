@@ -339,33 +339,43 @@ __device__ __forceinline__ float sgd_elem(float& p, float& buf, float g, const O
     return p;
 }
 
-template <int kKind>
-__device__ __forceinline__ void opt_vec4(const b200moe_opt_tensor& d, long long i, const OptScalars& s) {
+// 4 consecutive elements per thread: 16-byte loads, the update, 16-byte stores
+// (a 2-group unroll measured slower: 25-27 ms vs 22.4 ms for 3.95 B params).
+struct OptVec {
     float g[4];
+    float4 p, m, v;
+};
+
+template <int kKind>
+__device__ __forceinline__ void opt_load4(const b200moe_opt_tensor& d, long long i, OptVec& o) {
     if (d.grad_bf16) {
         const float4 t = ld_bf16x4(reinterpret_cast<const bf16*>(d.grad) + i);
-        g[0] = t.x; g[1] = t.y; g[2] = t.z; g[3] = t.w;
+        o.g[0] = t.x; o.g[1] = t.y; o.g[2] = t.z; o.g[3] = t.w;
     } else {
         const float4 t = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(d.grad) + i);
-        g[0] = t.x; g[1] = t.y; g[2] = t.z; g[3] = t.w;
+        o.g[0] = t.x; o.g[1] = t.y; o.g[2] = t.z; o.g[3] = t.w;
     }
-    float4 p = *reinterpret_cast<const float4*>(d.param + i);
-    float4 m = *reinterpret_cast<const float4*>(d.m + i);
-    float* pp = &p.x;
-    float* mp = &m.x;
+    o.p = *reinterpret_cast<const float4*>(d.param + i);
+    o.m = *reinterpret_cast<const float4*>(d.m + i);
+    if constexpr (kKind == B200MOE_OPT_ADAM) o.v = *reinterpret_cast<const float4*>(d.v + i);
+}
+
+template <int kKind>
+__device__ __forceinline__ void opt_store4(const b200moe_opt_tensor& d, long long i, OptVec& o, const OptScalars& s) {
+    float* pp = &o.p.x;
+    float* mp = &o.m.x;
     if constexpr (kKind == B200MOE_OPT_ADAM) {
-        float4 v = *reinterpret_cast<const float4*>(d.v + i);
-        float* vp = &v.x;
+        float* vp = &o.v.x;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) adam_elem(pp[j], mp[j], vp[j], g[j], s);
-        *reinterpret_cast<float4*>(d.v + i) = v;
+        for (int j = 0; j < 4; ++j) adam_elem(pp[j], mp[j], vp[j], o.g[j], s);
+        *reinterpret_cast<float4*>(d.v + i) = o.v;
     } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sgd_elem(pp[j], mp[j], g[j], s);
+        for (int j = 0; j < 4; ++j) sgd_elem(pp[j], mp[j], o.g[j], s);
     }
-    *reinterpret_cast<float4*>(d.m + i) = m;
-    *reinterpret_cast<float4*>(d.param + i) = p;
-    if (d.shadow != nullptr) st_bf16x4(reinterpret_cast<bf16*>(d.shadow) + i, p);
+    *reinterpret_cast<float4*>(d.m + i) = o.m;
+    *reinterpret_cast<float4*>(d.param + i) = o.p;
+    if (d.shadow != nullptr) st_bf16x4(reinterpret_cast<bf16*>(d.shadow) + i, o.p);
 }
 
 template <int kKind>
@@ -380,7 +390,11 @@ __global__ void __launch_bounds__(256) optimizer_kernel(const b200moe_opt_tensor
         // Vector body: 4 elements per thread (all buffers are 16-byte aligned
         // torch allocations and chunks start at multiples of kOptChunk).
         const long long iv = i0 + ((i1 - i0) & ~3LL);
-        for (long long i = i0 + 4 * threadIdx.x; i < iv; i += 4 * blockDim.x) opt_vec4<kKind>(d, i, s);
+        for (long long i = i0 + 4 * threadIdx.x; i < iv; i += 4 * blockDim.x) {
+            OptVec a;
+            opt_load4<kKind>(d, i, a);
+            opt_store4<kKind>(d, i, a, s);
+        }
         for (long long i = iv + threadIdx.x; i < i1; i += blockDim.x) {
             const float g = d.grad_bf16 ? load_g<bf16>(d.grad, i) : load_g<float>(d.grad, i);
             float p = d.param[i];

@@ -259,32 +259,39 @@ router_wgrad_partial(const __nv_bfloat16* __restrict__ x, const float* __restric
             if (e < E) p[(size_t)(h0 + j) * E + e] = acc[j][e];
 }
 
-// E <= 8 variant with much more memory-level parallelism: a CTA owns a
-// 256-wide h slice and a 128-token chunk; each of its 8 warps sweeps 16 tokens
-// with all 16-byte loads issued up front (lane = 8 consecutive h), then the 8
-// warp partials are summed in fixed warp order through shared memory.
-constexpr int kWg2Warps = 8;
-constexpr int kWg2Tok = 16;  // tokens per warp
+// E <= 8, long token runs: a block owns 256 hidden units x kW3Tok tokens; each
+// warp walks its 64 tokens in groups of 8 rows (512 contiguous bytes per row),
+// the next group's loads in flight while the current one is accumulated in
+// registers; one cross-warp reduction per block, so the partial buffer is
+// ceil(T/512) x H x E floats (2 MiB at the bench shape).
+constexpr int kW3Tok = 512;
+constexpr int kW3Grp = 8;
+constexpr int kW3PerWarp = kW3Tok / 8;
 
 template <int EP>
 __global__ void __launch_bounds__(256)
-router_wgrad_partial2(const __nv_bfloat16* __restrict__ x, const float* __restrict__ d, int T, int H, int E,
+router_wgrad_partial3(const __nv_bfloat16* __restrict__ x, const float* __restrict__ d, int T, int H, int E,
                       float* __restrict__ part) {
     extern __shared__ float sm[];
-    float* ds = sm;                                  // [128][EP]
-    float* red = sm + kWgTok * EP;                   // [8 warps][256 h][EP]
+    float* ds = sm;                                  // [kW3Tok][EP]
+    float* red = sm + kW3Tok * EP;                   // [8 warps][256 h][EP]
     const int chunk = blockIdx.y;
-    const int t0 = chunk * kWgTok;
+    const int t0 = chunk * kW3Tok;
     const int h0 = blockIdx.x * 256;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int hl = lane * 8;  // local h of this lane
-    uint4 u[kWg2Tok];         // x loads first: their latency overlaps the dh staging below
+    const int hl = lane * 8;
+    const int tw = t0 + warp * kW3PerWarp;
+    const bool hok = h0 + hl < H;
+    auto load = [&](uint4* u, int g) {
 #pragma unroll
-    for (int i = 0; i < kWg2Tok; ++i) {
-        const int t = t0 + warp * kWg2Tok + i;
-        u[i] = (t < T && h0 + hl < H) ? ld_nc_v4(x + (size_t)t * H + h0 + hl) : make_uint4(0, 0, 0, 0);
-    }
-    for (int i = threadIdx.x; i < kWgTok * EP; i += blockDim.x) {
+        for (int i = 0; i < kW3Grp; ++i) {
+            const int t = tw + g * kW3Grp + i;
+            u[i] = (t < T && hok) ? ld_nc_v4(x + (size_t)t * H + h0 + hl) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    uint4 u[kW3Grp];
+    load(u, 0);
+    for (int i = threadIdx.x; i < kW3Tok * EP; i += blockDim.x) {
         const int tt = i / EP, e = i % EP;
         const int t = t0 + tt;
         ds[i] = (t < T && e < E) ? d[(size_t)t * E + e] : 0.f;
@@ -295,17 +302,23 @@ router_wgrad_partial2(const __nv_bfloat16* __restrict__ x, const float* __restri
     for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int e = 0; e < EP; ++e) acc[j][e] = 0.f;
+    for (int g = 0; g < kW3PerWarp / kW3Grp; ++g) {
+        uint4 un[kW3Grp];
+        if (g + 1 < kW3PerWarp / kW3Grp) load(un, g + 1);
 #pragma unroll
-    for (int i = 0; i < kWg2Tok; ++i) {
-        float xv[8];
-        unpack8(u[i], xv);
-        const float* dr = ds + (warp * kWg2Tok + i) * EP;
+        for (int i = 0; i < kW3Grp; ++i) {
+            float xv[8];
+            unpack8(u[i], xv);
+            const float* dr = ds + (warp * kW3PerWarp + g * kW3Grp + i) * EP;
 #pragma unroll
-        for (int e = 0; e < EP; ++e) {
-            const float dv = dr[e];
+            for (int e = 0; e < EP; ++e) {
+                const float dv = dr[e];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j][e] = fmaf(xv[j], dv, acc[j][e]);
+                for (int j = 0; j < 8; ++j) acc[j][e] = fmaf(xv[j], dv, acc[j][e]);
+            }
         }
+#pragma unroll
+        for (int i = 0; i < kW3Grp; ++i) u[i] = un[i];
     }
     float* rw = red + (size_t)warp * 256 * EP;  // [(j * EP + e) * 32 + lane]: conflict-free
 #pragma unroll
@@ -320,7 +333,7 @@ router_wgrad_partial2(const __nv_bfloat16* __restrict__ x, const float* __restri
         const int hh = l * 8 + j;
         float s = 0.f;
 #pragma unroll
-        for (int w = 0; w < kWg2Warps; ++w) s += red[(size_t)w * 256 * EP + i];
+        for (int w = 0; w < 8; ++w) s += red[(size_t)w * 256 * EP + i];
         if (e < E && h0 + hh < H) p[(size_t)(h0 + hh) * E + e] = s;
     }
 }
@@ -477,11 +490,11 @@ int router_bwd_k(int k, const void* dxp, const uint64_t* dxp_bufs, int e_per_ran
 
 template <int EP>
 int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, float* part, cudaStream_t stream) {
-    const int nch = ceil_div(T, kWgTok);
+    int nch = ceil_div(T, kWgTok);
     if constexpr (EP <= 8) {
-        static_assert(kWg2Warps * kWg2Tok == kWgTok, "token tiling");
-        const size_t sh = (size_t)(kWgTok * EP + kWg2Warps * 256 * EP) * sizeof(float);
-        auto kern = router_wgrad_partial2<EP>;
+        nch = ceil_div(T, kW3Tok);
+        const size_t sh = (size_t)(kW3Tok * EP + 8 * 256 * EP) * sizeof(float);
+        auto kern = router_wgrad_partial3<EP>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
         dim3 grid(ceil_div(H, 256), nch);
         kern<<<grid, 256, sh, stream>>>((const __nv_bfloat16*)x, d, T, H, E, part);

@@ -76,6 +76,16 @@ class RouterParams:
         if not bool(torch.isfinite(self.w_g).all() & torch.isfinite(self.w_noise).all()):
             raise ConfigError("router weights must be finite")
 
+    @classmethod
+    def trusted(cls, w_g: torch.Tensor, w_noise: torch.Tensor) -> "RouterParams":
+        """View over a checkpoint's router tensors without the finiteness scan
+        (a host sync); the model forward builds one per MoE layer per step."""
+        if tuple(w_g.shape) != tuple(w_noise.shape):
+            raise ShapeError(f"router matrices differ in shape: {tuple(w_g.shape)} vs {tuple(w_noise.shape)}")
+        obj = cls.__new__(cls)
+        obj.w_g, obj.w_noise = w_g, w_noise
+        return obj
+
 
 @dataclass
 class ExpertFFN:

@@ -23,7 +23,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2412_09952_b200 as P  # noqa: E402
-from paper_2412_09952_b200.train import Optimizer, prepare_for_training  # noqa: E402
+from paper_2412_09952_b200.train import TrainState  # noqa: E402
 
 
 def model_flops(cfg, gate, tokens: int, kept_slots: int) -> float:
@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--small", action="store_true", help="tiny shape for a smoke run")
+    ap.add_argument("--no-shadows", action="store_true", help="cast fp32 GEMM weights per step instead")
     a = ap.parse_args()
     dev = torch.device("cuda")
     if a.small:
@@ -69,7 +70,8 @@ def main():
     dense = random_dense(cfg, dev)
     moe = P.upcycle_full(dense, 8, 2, router_seed=1, capacity_factor=a.cf)
     del dense
-    opt = Optimizer("adam", prepare_for_training(moe))
+    state = TrainState(moe, shadows=not a.no_shadows)
+    opt = state.optimizer("adam")
     rng = np.random.default_rng(0)
     tokens = rng.integers(0, cfg.vocab, (a.batch, a.seq + 1))
     inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
@@ -79,7 +81,7 @@ def main():
     def step(ev=None):
         if ev is not None:
             ev[0].record()
-        fwd = P.forward_with_stats(moe, inputs, training=True)
+        fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute)
         loss = P.cross_entropy(fwd.logits, targets)
         for g in fwd.gates:
             loss = loss + (aux / len(fwd.gates)) * P.importance_penalty(g)
