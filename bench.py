@@ -345,6 +345,16 @@ def run_single(args, dev):
                          f"fp32 on {cores} threads, {cpu_model()}"}
 
     clocks = clk.summary()
+    # Roofline denominator (B200_PROFILING.md): the burst cuBLAS figure for a
+    # kernel timed alone, the sustained (power-capped, seconds-long loop) one for
+    # a kernel timed inside a long step.  The GEMMs here run back to back for
+    # the whole timed region; when that region is long and the sampled clocks
+    # show the power cap, the sustained figure is the one that applies.
+    timed_ms = ms * args.steps
+    capped = "sw_power_cap" in (clocks or {}).get("reasons", [])
+    peak_s = MEASURED.get("bf16_tflops_sustained", peak)
+    use_sustained = capped and timed_ms >= 100.0
+    roof_peak = peak_s if use_sustained else peak
     line = {
         "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 1), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
@@ -356,8 +366,13 @@ def run_single(args, dev):
         "mfu": {"measured_peak": round(mfu_measured, 4), "spec_2250": round(mfu_spec, 4),
                 "flops_per_step": flops},
         "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM, all 5 launches/step)", "bound": "tensor",
-                     "achieved": round(achieved_tf, 1), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved_tf / peak, 4), "traffic": gemm_traffic(),
+                     "achieved": round(achieved_tf, 1), "peak": roof_peak, "unit": "TFLOP/s",
+                     "frac": round(achieved_tf / roof_peak, 4),
+                     "peak_kind": (f"measured sustained bf16 (MEASURED_PEAKS.json): GEMMs timed inside a "
+                                   f"{timed_ms:.0f} ms back-to-back region, clocks show sw_power_cap")
+                                  if use_sustained else "measured burst bf16 (MEASURED_PEAKS.json)",
+                     "frac_of_burst": round(achieved_tf / peak, 4), "burst_peak": peak, "sustained_peak": peak_s,
+                     "traffic": gemm_traffic(),
                      "traffic_unit": "DRAM bytes per step (5 launches), ncu --set full capture, profiles/",
                      "algorithmic_dram_bytes_per_step": gemm_min_bytes(S),
                      "gemm_ms_per_step": round(gemm_ms, 4), "gemm_share_of_step": round(gemm_ms / ms, 4)},

@@ -14,7 +14,8 @@ import threading
 from .errors import ConfigError, GateError, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libb200moe.so")
+# B200MOE_LIB overrides the library path (A/B experiments with variant builds).
+LIB_PATH = os.environ.get("B200MOE_LIB") or os.path.join(_HERE, "lib", "libb200moe.so")
 
 OK, ERR_SHAPE, ERR_CONFIG, ERR_GATE, ERR_CUDA = 0, -1, -2, -3, -4
 ROUTER = {"mixtral": 0, "st": 1}

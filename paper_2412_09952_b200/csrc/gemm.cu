@@ -80,7 +80,10 @@ struct Cfg {
 // 2 x (a, b) 2 KB chunks and trades two operand stages for it).
 template <int kMode, int kCG>
 struct Geo {
-    static constexpr bool kTmaEpiLoads = (kMode == kBwd2) && (kCG == 2);
+#ifndef B200_BWD2_TMA_EPI
+#define B200_BWD2_TMA_EPI 1
+#endif
+    static constexpr bool kTmaEpiLoads = B200_BWD2_TMA_EPI && (kMode == kBwd2) && (kCG == 2);
     // Store-ring depth per epilogue warp (4 buffers + 5 stages measured no
     // better than 2 + 6 for WGRAD on B200).
     static constexpr int kRing = 2;
@@ -443,8 +446,10 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
             // SwiGLU backward with the stored pre-activations (a, b) streamed by
             // TMA one 32-column chunk ahead; chunk 0 is requested before the
             // accumulator wait.
+            // experiment switches: debug & 32 skips the a/b loads, & 64 the stores
+            const bool no_ld = a.debug & 32, no_st = a.debug & 64;
             const int col0 = ti.n_tile * kBN + half * 128;
-            if (live) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0, row0, lane);
+            if (live && !no_ld) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0, row0, lane);
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
             if (!live) return;
@@ -452,9 +457,14 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
             for (int cc = 0; cc < 4; ++cc) {
                 const int c = cc * 32;
                 const int cur = ld.idx ^ 1;  // buffer holding chunk cc
-                if (cc + 1 < 4) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0 + c + 32, row0, lane);
+                if (cc + 1 < 4 && !no_ld) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0 + c + 32, row0, lane);
                 ptx::tmem_ld_32x32b_x32(lane_addr + half * 128 + c, r0);
-                epi_load_take(ld, cur, lane, v0, v1);
+                if (!no_ld) {
+                    epi_load_take(ld, cur, lane, v0, v1);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) { v0[i] = 0.5f; v1[i] = 0.25f; }
+                }
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
@@ -464,6 +474,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
                     v1[i] = dm * (av * sg);
                 }
+                if (no_st) continue;
                 emit32<kRing>(ring, &tm.st[0], a.out0, a.F, v0, lane, col0 + c, row0, a.debug);
                 emit32<kRing>(ring, &tm.st[1], a.out1, a.F, v1, lane, col0 + c, row0, a.debug);
             }
