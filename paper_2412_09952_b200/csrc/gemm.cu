@@ -287,7 +287,7 @@ __device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m,
 // 16-byte chunk lane%4) so every st.global instruction writes eight complete
 // 64-byte row segments.  Keeps the TMA engine free for operand loads.
 __device__ __forceinline__ void stage_store_lsu(uint8_t* buf, __nv_bfloat16* gdst, size_t ld, const float* v,
-                                                int lane) {
+                                                int lane, bool stream) {
     uint4* rowp = reinterpret_cast<uint4*>(buf + lane * 64);
     const int sw = (lane >> 1) & 3;
     __syncwarp();  // previous chunk's readers are done with buf
@@ -299,7 +299,8 @@ __device__ __forceinline__ void stage_store_lsu(uint8_t* buf, __nv_bfloat16* gds
     for (int i = 0; i < 4; ++i) {
         const int r = i * 8 + (lane >> 2);
         const uint4 val = *reinterpret_cast<const uint4*>(buf + r * 64 + ((cj ^ ((r >> 1) & 3)) << 4));
-        *reinterpret_cast<uint4*>(gdst + (size_t)r * ld + cj * 8) = val;
+        if (stream) ptx::st_cs_v4(gdst + (size_t)r * ld + cj * 8, val);
+        else *reinterpret_cast<uint4*>(gdst + (size_t)r * ld + cj * 8) = val;
     }
 }
 
@@ -312,7 +313,7 @@ template <int kRing, bool kLsuDefault = false>
 __device__ __forceinline__ void emit32(EpiRing& ring, const CUtensorMap* m, __nv_bfloat16* gbase, size_t ld,
                                        const float* v, int lane, int col, int row0, int debug) {
     const bool lsu = (debug & 4) ? false : ((debug & 8) ? true : kLsuDefault);
-    if (lsu) stage_store_lsu(ring.base, gbase + (size_t)row0 * ld + col, ld, v, lane);
+    if (lsu) stage_store_lsu(ring.base, gbase + (size_t)row0 * ld + col, ld, v, lane, debug & 128);
     else stage_store<kRing>(ring, m, v, lane, col, row0);
 }
 

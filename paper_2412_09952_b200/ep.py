@@ -216,17 +216,20 @@ class _EPFunction(torch.autograd.Function):
 
 
 class _PeerBuffers:
-    """One symmetric-memory allocation per (receive rows, hidden, group) holding
-    this rank's receive-side buffers -- xr (tokens in), O (expert outputs), dO,
-    dxp, each [R*E_local*cap_pad, H] bf16 -- plus the int32 receive-count table.
-    Peers address them through device arrays of per-rank base pointers."""
+    """One symmetric-memory allocation per (buffer slot, receive rows, hidden,
+    group) holding this rank's receive-side buffers -- xr (tokens in), O (expert
+    outputs), dO, dxp, each [R*E_local*cap_pad, H] bf16 -- plus the int32
+    receive-count table.  Peers address them through device arrays of per-rank
+    base pointers.  xr and O are saved for the backward, so every layer that is
+    alive in one autograd graph needs its own slot (the model forward uses the
+    layer index)."""
 
     _cache: dict = {}
 
     @classmethod
-    def get(cls, rows: int, H: int, n_counts: int, group, device):
+    def get(cls, rows: int, H: int, n_counts: int, group, device, slot: int = 0):
         grp = group if group is not None else dist.group.WORLD
-        key = (rows, H, n_counts, grp.group_name, device.index)
+        key = (slot, rows, H, n_counts, grp.group_name, device.index)
         b = cls._cache.get(key)
         if b is None:
             b = cls(rows, H, n_counts, grp, device)
@@ -284,7 +287,7 @@ class _EPPeerFunction(torch.autograd.Function):
         bf = dict(dtype=torch.bfloat16, device=dev)
         rt = _lib.ROUTER[cfg.router_type]
         Rs = plan.send_rows
-        pb = _PeerBuffers.get(Rs, H, plan.world * El, group, dev)
+        pb = _PeerBuffers.get(Rs, H, plan.world * El, group, dev, st.get("buffer_slot", 0))
 
         logits = torch.empty(T, E, **f32)
         gates = torch.empty(T, E, **f32)
@@ -402,10 +405,14 @@ class ExpertParallelMoE:
 
     TRANSPORTS = ("p2p", "nccl")
 
-    def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None, transport: str = "p2p"):
+    def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None, transport: str = "p2p",
+                 buffer_slot: int = 0):
         """transport: "p2p" (default) fuses the dispatch/combine exchange into the
         permute/combine kernels over NVLink symmetric memory; "nccl" uses
-        all_to_all_single between separate kernels (the comparison baseline)."""
+        all_to_all_single between separate kernels (the comparison baseline).
+        buffer_slot: which symmetric receive buffers the p2p transport uses;
+        layers whose forwards are alive in the same autograd graph need
+        distinct slots (a slot's xr / O are saved for its backward)."""
         if transport not in self.TRANSPORTS:
             raise ConfigError(f"transport must be one of {self.TRANSPORTS}, got {transport!r}")
         self.transport = transport
@@ -419,6 +426,7 @@ class ExpertParallelMoE:
         if cfg.n_experts > 32:
             raise ConfigError("the B200 router supports up to 32 experts")
         self.w_g, self.w_noise, self.W1, self.W2, self.W3, self.cfg = w_g, w_noise, W1, W2, W3, cfg
+        self.buffer_slot = buffer_slot
 
     def forward(self, x: torch.Tensor, rng=None, training: bool = False, noise=None, reduce_router: bool = True):
         T, H = x.shape
@@ -426,7 +434,7 @@ class ExpertParallelMoE:
             raise ShapeError("the EP path needs hidden and ffn multiples of 256")
         plan = EPPlan.make(self.world, self.rank, self.cfg.n_experts, T, self.cfg.capacity_factor)
         z = _noise(T, self.cfg.n_experts, x.device, self.cfg.noise_enabled and training, rng, noise)
-        st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router)
+        st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router, buffer_slot=self.buffer_slot)
         fn = _EPPeerFunction if self.transport == "p2p" else _EPFunction
         y, gates = fn.apply(x.to(torch.bfloat16).contiguous(), self.w_g.to(torch.float32).contiguous(),
                             self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)

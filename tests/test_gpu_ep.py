@@ -24,3 +24,16 @@ def test_ep_matches_single_gpu_per_rank():
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
     assert r.stdout.count("PASS") == 8 * n   # 4 cases x {p2p, nccl} per rank
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_model_step_ep_dp_matches_single_gpu():
+    """Model step with EP MoE layers + overlapped DP gradient all-reduce vs the
+    single-GPU model on every rank's batch (tools/model_ep_check.py)."""
+    n = 4 if torch.cuda.device_count() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29562", os.path.join(ROOT, "tools", "model_ep_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+    assert r.stdout.count("PASS") == 2   # rank 0 checks both transports

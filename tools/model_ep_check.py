@@ -1,0 +1,116 @@
+"""Multi-GPU parity of the model step (SURVEY 8(e) + 8(f) row 1), run under
+torchrun on N GPUs: expert-parallel MoE layers (each rank owns E/N experts from
+upcycle_shard) + data-parallel reduction of the replicated gradients, against
+the single-GPU model (upcycle_full, all experts) run on every rank's batch with
+the gradients summed -- the same global-batch-mean gradient.
+
+Prints one PASS/FAIL line per rank; exit code 0 iff every rank passes."""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2412_09952_b200 as P  # noqa: E402
+from paper_2412_09952_b200.train import DataParallelGrads, TrainState  # noqa: E402
+
+CFG = dict(vocab=512, hidden=256, layers=2, heads=4, kv_heads=2, ffn_hidden=512, seq_len=64)
+E, K, CF, AUX = 4, 2, 1.0, 0.01
+MOE_LAYERS = (0, 1)
+
+
+def rel(a, b):
+    if a is None and b is None:
+        return 0.0
+    if a is None or b is None:
+        return float("inf")
+    a = a.detach().double().cpu()
+    b = b.detach().double().cpu()
+    return float((a - b).norm() / max(float(b.norm()), 1e-30))
+
+
+def batch(rank: int, cfg):
+    r = np.random.default_rng(100 + rank)
+    t = r.integers(0, cfg.vocab, (4, cfg.seq_len + 1))
+    return t[:, :-1], t[:, 1:].reshape(-1)
+
+
+def loss_of(fwd, targets, world):
+    loss = P.cross_entropy(fwd.logits, targets)
+    for g in fwd.gates:
+        loss = loss + (AUX / len(fwd.gates)) * P.importance_penalty(g)
+    return loss / world
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    cfg = P.ModelConfig(**CFG)
+    ok = True
+    for transport in ("p2p", "nccl"):
+        dense = P.init_dense(cfg, seed=11)
+        shard = P.shard_dense(dense, 1, world)[rank]
+        ms = P.upcycle_shard(shard, E, K, moe_layers=MOE_LAYERS, router_seed=3, capacity_factor=CF)
+        state = TrainState(ms)
+        dp = DataParallelGrads(state.leaves)
+        inputs, targets = batch(rank, cfg)
+        fwd = P.forward_with_stats(ms, inputs, training=True, compute=state.compute, ep_group=dist.group.WORLD,
+                                   transport=transport)
+        loss = loss_of(fwd, targets, world)
+        loss.backward()
+        dp.wait()
+        dp.remove()
+        total = loss.detach().clone()
+        dist.all_reduce(total)
+        # gather every rank's expert gradients (owned experts, stacked layout)
+        gathered = {}
+        for name, t in state.leaves.items():
+            if ".moe.experts." in name:
+                parts = [torch.empty_like(t.grad) for _ in range(world)]
+                dist.all_gather(parts, t.grad.contiguous())
+                gathered[name] = torch.cat(parts, 0)
+        if rank == 0:
+            full = P.upcycle_full(dense, E, K, moe_layers=MOE_LAYERS, router_seed=3, capacity_factor=CF)
+            ref_state = TrainState(full)
+            ref_loss = 0.0
+            for r in range(world):
+                ri, rt = batch(r, cfg)
+                rf = P.forward_with_stats(full, ri, training=True, compute=ref_state.compute)
+                lr = loss_of(rf, rt, world)
+                lr.backward()
+                ref_loss += float(lr.detach())
+            errs = {"loss": abs(float(total) - ref_loss) / abs(ref_loss)}
+            worst = ("", 0.0)
+            for name, t in ref_state.leaves.items():
+                got = gathered[name] if name in gathered else state.leaves[name].grad
+                e = rel(got, t.grad)
+                if e > worst[1]:
+                    worst = (name, e)
+                tol = 3e-2 if (".moe." in name) else 2e-2
+                if os.environ.get("VERBOSE"):
+                    print(f"[{transport}] {name}: rel {e:.3e}", flush=True)
+                if e > tol:
+                    ok = False
+                    print(f"[{transport}] grad mismatch {name}: rel {e:.3e} > {tol}", flush=True)
+            if errs["loss"] > 1e-3:
+                ok = False
+            print(f"[{transport}] world={world} loss={float(total):.6f} ref={ref_loss:.6f} "
+                  f"loss_rel={errs['loss']:.2e} worst_grad={worst[0]} {worst[1]:.2e} "
+                  f"{'PASS' if ok else 'FAIL'}", flush=True)
+        dist.barrier()
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    dist.destroy_process_group()
+    sys.exit(int(flag.item() != 0))
+
+
+if __name__ == "__main__":
+    main()
