@@ -214,6 +214,11 @@ int b200moe_embedding_fwd(const float* table, const int64_t* ids, int T, int H, 
  * Replaces the np.add.at of moefold/tensor.py:333-336. */
 int b200moe_embedding_bwd(const float* g, const int* order, const int* seg_start, const int* seg_id, int n_seg, int H,
                           float* grad, cudaStream_t stream);
+/* Same sums from a device-side stable sort: sorted_ids[i] = ids[order[i]]
+ * (n entries); rows of grad for absent ids untouched.  Used for the
+ * data-parallel embedding gradient over all ranks' gathered tokens. */
+int b200moe_embedding_bwd_sorted(const float* g, const int64_t* order, const int64_t* sorted_ids, int n, int H,
+                                 float* grad, cudaStream_t stream);
 /* nll[t] = logsumexp(logits[t]) - logits[t, targets[t]], lse[t], loss[0] =
  * mean(nll); logits bf16 [T, V].  Replaces moefold/tensor.py:340-359. */
 int b200moe_cross_entropy_fwd(const void* logits, const int64_t* targets, int T, int V, float* nll, float* lse,

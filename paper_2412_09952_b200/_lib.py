@@ -60,6 +60,7 @@ SIGNATURES = {
     "b200moe_rmsnorm_bwd": [_P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P],
     "b200moe_embedding_fwd": [_P, _P, _I, _I, _I, _P, _P, _P],
     "b200moe_embedding_bwd": [_P, _P, _P, _P, _I, _I, _P, _P],
+    "b200moe_embedding_bwd_sorted": [_P, _P, _P, _I, _I, _P, _P],
     "b200moe_cross_entropy_fwd": [_P, _P, _I, _I, _P, _P, _P, _P, _P],
     "b200moe_cross_entropy_bwd": [_P, _P, _P, _P, _I, _I, _P, _P],
     "b200moe_optimizer_chunk": [],
@@ -111,6 +112,7 @@ KERNELS_PER_CALL = {
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_upcycle_copy": 3,
     "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 3,
     "b200moe_rmsnorm_fwd": 1, "b200moe_rmsnorm_bwd": 2, "b200moe_embedding_fwd": 1, "b200moe_embedding_bwd": 1,
+    "b200moe_embedding_bwd_sorted": 1,
     "b200moe_cross_entropy_fwd": 2, "b200moe_cross_entropy_bwd": 1, "b200moe_optimizer_step": 1,
     "b200moe_crc32c": 2, "b200moe_crc32c_init": 1,
 }

@@ -209,6 +209,30 @@ __global__ void __launch_bounds__(kRowThreads) embedding_bwd_kernel(const float*
     }
 }
 
+// Same scatter-add from a device-sorted token order, no host round trip:
+// position i starts a segment iff sid[i] != sid[i-1]; that block sums the
+// segment's rows in order.  Used by the data-parallel embedding backward over
+// the all-gathered tokens of every rank.
+__global__ void __launch_bounds__(kRowThreads) embedding_bwd_sorted_kernel(const float* __restrict__ g,
+                                                                           const int64_t* __restrict__ order,
+                                                                           const int64_t* __restrict__ sid, int n,
+                                                                           int H, float* __restrict__ grad) {
+    const int i0 = blockIdx.x;
+    const int64_t id = sid[i0];
+    if (i0 > 0 && sid[i0 - 1] == id) return;
+    int i1 = i0 + 1;
+    while (i1 < n && sid[i1] == id) ++i1;
+    float* dst = grad + (size_t)id * H;
+    for (int c = threadIdx.x * 4; c < H; c += kRowThreads * 4) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = i0; i < i1; ++i) {
+            const float4 v = *reinterpret_cast<const float4*>(g + (size_t)order[i] * H + c);
+            a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        }
+        *reinterpret_cast<float4*>(dst + c) = a;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Cross entropy (tensor.py:340-364): per row m = max, z = sum exp(x - m),
 // lse = log z + m, nll = lse - x[target]; loss = mean nll.  Backward writes
@@ -460,6 +484,15 @@ int b200moe_embedding_bwd(const float* g, const int* order, const int* seg_start
     if (n_seg == 0) return B200MOE_OK;
     embedding_bwd_kernel<<<n_seg, kRowThreads, 0, stream>>>(g, order, seg_start, seg_id, H, grad);
     B200_CHECK_LAUNCH("embedding_bwd");
+    return B200MOE_OK;
+}
+
+int b200moe_embedding_bwd_sorted(const float* g, const int64_t* order, const int64_t* sorted_ids, int n, int H,
+                                 float* grad, cudaStream_t stream) {
+    B200_CHECK_ARG(H >= 4 && H % 4 == 0, B200MOE_ERR_SHAPE, "embedding_bwd: hidden %d must be a multiple of 4", H);
+    if (n == 0) return B200MOE_OK;
+    embedding_bwd_sorted_kernel<<<n, kRowThreads, 0, stream>>>(g, order, sorted_ids, n, H, grad);
+    B200_CHECK_LAUNCH("embedding_bwd_sorted");
     return B200MOE_OK;
 }
 

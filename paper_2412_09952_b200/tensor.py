@@ -143,9 +143,50 @@ class _Embedding(torch.autograd.Function):
         return grad, None, None, None, None
 
 
-def embedding(table: torch.Tensor, ids) -> torch.Tensor:
+class _EmbeddingDP(torch.autograd.Function):
+    """Embedding whose backward produces the gradient of the whole data-parallel
+    batch on every rank: all-gather each rank's output gradient [T, H] and ids,
+    stable-sort the ids on the device, ordered scatter-add.  Moves world x T x H
+    floats instead of all-reducing the [V, H] table gradient, and equals the
+    single-GPU np.add.at over the concatenated batch bit for bit."""
+
+    @staticmethod
+    def forward(ctx, table, ids_dev, group):
+        V, H = table.shape
+        T = ids_dev.shape[0]
+        out = torch.empty(T, H, dtype=torch.float32, device=table.device)
+        err = torch.zeros(1, dtype=torch.int32, device=table.device)
+        _lib.call("b200moe_embedding_fwd", table.data_ptr(), ids_dev.data_ptr(), T, H, V, out.data_ptr(),
+                  err.data_ptr(), _lib.stream_ptr())
+        ctx.save_for_backward(ids_dev)
+        ctx.shape = (V, H)
+        ctx.group = group
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        import torch.distributed as dist
+        (ids,) = ctx.saved_tensors
+        V, H = ctx.shape
+        world = dist.get_world_size(ctx.group)
+        g = g.to(torch.float32).contiguous()
+        T = ids.shape[0]
+        g_all = torch.empty(world * T, H, dtype=torch.float32, device=g.device)
+        ids_all = torch.empty(world * T, dtype=torch.int64, device=g.device)
+        dist.all_gather_into_tensor(g_all, g, group=ctx.group)
+        dist.all_gather_into_tensor(ids_all, ids, group=ctx.group)
+        sid, order = torch.sort(ids_all, stable=True)
+        grad = torch.zeros(V, H, dtype=torch.float32, device=g.device)
+        _lib.call("b200moe_embedding_bwd_sorted", g_all.data_ptr(), order.data_ptr(), sid.data_ptr(), world * T, H,
+                  grad.data_ptr(), _lib.stream_ptr())
+        return grad, None, None
+
+
+def embedding(table: torch.Tensor, ids, dp_group=None) -> torch.Tensor:
     """Row gather from an fp32 embedding table; the backward is the ordered
-    per-id scatter-add of np.add.at (tensor.py:324-337).  ids: host ints."""
+    per-id scatter-add of np.add.at (tensor.py:324-337).  ids: host ints.
+    With `dp_group`, the backward returns the gradient of every rank's batch
+    (equal on all ranks; no all-reduce of the table gradient needed)."""
     _require_cuda(table, "table")
     ids = np.asarray(ids.cpu() if isinstance(ids, torch.Tensor) else ids, dtype=np.int64).reshape(-1)
     V = table.shape[0]
@@ -153,6 +194,9 @@ def embedding(table: torch.Tensor, ids) -> torch.Tensor:
         raise InputError(f"token id out of range [0, {V}): min={ids.min()}, max={ids.max()}")
     if table.shape[1] % 4:
         raise ShapeError(f"embedding width {table.shape[1]} must be a multiple of 4")
+    if dp_group is not None:
+        ids_dev = torch.from_numpy(ids).pin_memory().to(table.device, non_blocking=True)
+        return _EmbeddingDP.apply(table.to(torch.float32).contiguous(), ids_dev, dp_group)
     order = np.argsort(ids, kind="stable")
     sid = ids[order]
     starts = np.flatnonzero(np.r_[True, sid[1:] != sid[:-1]]) if ids.size else np.zeros(0, dtype=np.int64)

@@ -23,7 +23,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2412_09952_b200 as P  # noqa: E402
-from paper_2412_09952_b200.train import TrainState  # noqa: E402
+from paper_2412_09952_b200.train import DataParallelGrads, TrainState  # noqa: E402
 
 
 def model_flops(cfg, gate, tokens: int, kept_slots: int) -> float:
@@ -59,8 +59,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--small", action="store_true", help="tiny shape for a smoke run")
     ap.add_argument("--no-shadows", action="store_true", help="cast fp32 GEMM weights per step instead")
+    ap.add_argument("--transport", default="p2p", choices=("p2p", "nccl"))
     a = ap.parse_args()
-    dev = torch.device("cuda")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = 0
+    group = None
+    if world > 1:   # torchrun: EP over all ranks for the MoE layers, DP for the rest
+        import torch.distributed as dist
+        local = int(os.environ["LOCAL_RANK"])
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        rank, group = dist.get_rank(), dist.group.WORLD
+    dev = torch.device("cuda", torch.cuda.current_device())
     if a.small:
         cfg = P.ModelConfig(vocab=1024, hidden=512, layers=a.layers, heads=8, kv_heads=2, ffn_hidden=1024,
                             seq_len=a.seq)
@@ -68,11 +78,15 @@ def main():
         cfg = P.ModelConfig(vocab=128256, hidden=4096, layers=a.layers, heads=32, kv_heads=8, ffn_hidden=14336,
                             seq_len=a.seq)
     dense = random_dense(cfg, dev)
-    moe = P.upcycle_full(dense, 8, 2, router_seed=1, capacity_factor=a.cf)
+    if world > 1:   # online upcycling of this rank's experts only (upcycle.py:187-227)
+        moe = P.upcycle_shard(P.shard_dense(dense, 1, world)[rank], 8, 2, router_seed=1, capacity_factor=a.cf)
+    else:
+        moe = P.upcycle_full(dense, 8, 2, router_seed=1, capacity_factor=a.cf)
     del dense
     state = TrainState(moe, shadows=not a.no_shadows)
     opt = state.optimizer("adam")
-    rng = np.random.default_rng(0)
+    dp = DataParallelGrads(state.leaves, group) if world > 1 else None
+    rng = np.random.default_rng(rank)
     tokens = rng.integers(0, cfg.vocab, (a.batch, a.seq + 1))
     inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
     T = a.batch * a.seq
@@ -81,15 +95,19 @@ def main():
     def step(ev=None):
         if ev is not None:
             ev[0].record()
-        fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute)
+        fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute, ep_group=group,
+                                   transport=a.transport)
         loss = P.cross_entropy(fwd.logits, targets)
         for g in fwd.gates:
             loss = loss + (aux / len(fwd.gates)) * P.importance_penalty(g)
+        loss = loss / world
         if ev is not None:
             ev[1].record()
         for p in opt.params.values():
             p.grad = None
         loss.backward()
+        if dp is not None:
+            dp.wait()
         if ev is not None:
             ev[2].record()
         opt.step(1e-4)
@@ -100,7 +118,9 @@ def main():
     for _ in range(a.warmup):
         loss, stats = step()
     torch.cuda.synchronize()
-    kept = sum(int(s.assigned.sum()) for s in stats) // cfg.layers
+    kept = sum(int(s.assigned.sum()) for s in stats) // cfg.layers   # this rank's tokens' kept slots
+    if world > 1:
+        dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
     t0 = time.perf_counter()
     for i in range(a.steps):
@@ -108,20 +128,29 @@ def main():
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / a.steps
     ms = float(np.median([e[0].elapsed_time(e[3]) for e in evs]))
+    if world > 1:   # the step takes as long as the slowest rank
+        t = torch.tensor([ms, float(kept)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ms, kept = float(t[0]), int(t[1]) // world
     split = {k: round(float(np.median([e[i].elapsed_time(e[i + 1]) for e in evs])), 3)
              for i, k in enumerate(("forward", "backward", "optimizer"))}
-    flops = model_flops(cfg, moe.gate, T, kept)
+    flops = world * model_flops(cfg, moe.gate, T, kept)
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                         "MEASURED_PEAKS.json")))
     n_params = sum(t.numel() for t in opt.params.values())
+    if rank != 0:
+        dist.destroy_process_group()
+        return
     out = {
         "metric": f"Llama-3-8B-shape E8T2 {cfg.layers}-layer training step tokens/s",
-        "value": round(T / (ms * 1e-3), 1), "unit": "tokens/s", "ms_per_step": round(ms, 3),
+        "value": round(world * T / (ms * 1e-3), 1), "unit": "tokens/s", "ms_per_step": round(ms, 3),
+        "n_gpus": world, "parallelism": f"ep{world} (MoE) + dp{world} (rest)" if world > 1 else "single GPU",
         "wall_ms_per_step": round(wall * 1e3, 3), "phases_ms": split,
-        "mfu": {"measured_peak": round(flops / (ms * 1e-3) / (peaks["bf16_tflops"] * 1e12), 4),
-                "spec_2250": round(flops / (ms * 1e-3) / 2250e12, 4), "flops_per_step": flops,
+        "mfu": {"measured_peak": round(flops / (ms * 1e-3) / (world * peaks["bf16_tflops"] * 1e12), 4),
+                "spec_2250": round(flops / (ms * 1e-3) / (world * 2250e12), 4), "flops_per_step": flops,
                 "convention": "6P (plan.py:forward_flops) with kept slots for the expert FFNs"},
-        "loss": float(loss.detach()), "kept_slots_per_layer": kept, "params": n_params,
+        "loss": float(loss.detach()) * world, "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
         "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
                    "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": 8,
@@ -129,6 +158,8 @@ def main():
         "data": "synthetic (random token ids, random-init weights)",
     }
     print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
