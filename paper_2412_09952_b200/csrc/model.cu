@@ -403,7 +403,10 @@ __device__ __forceinline__ void opt_store4(const b200moe_opt_tensor& d, long lon
 }
 
 template <int kKind>
-__global__ void __launch_bounds__(256) optimizer_kernel(const b200moe_opt_tensor* __restrict__ list,
+// 6 resident blocks per SM (40 registers): the loads are latency-bound, so
+// occupancy is in-flight bytes -- 0.89 of HBM vs 0.74 at the default 58
+// registers (tools/opt_bench.py, 2 B parameters); 8 blocks spill.
+__global__ void __launch_bounds__(256, 6) optimizer_kernel(const b200moe_opt_tensor* __restrict__ list,
                                                         const int* __restrict__ chunk_tensor,
                                                         const long long* __restrict__ chunk_off, int n_chunks,
                                                         OptScalars s) {
