@@ -235,9 +235,10 @@ __global__ void __launch_bounds__(kRowThreads) embedding_bwd_sorted_kernel(const
 
 // ---------------------------------------------------------------------------
 // Cross entropy (tensor.py:340-364): per row m = max, z = sum exp(x - m),
-// lse = log z + m, nll = lse - x[target]; loss = mean nll.  Backward writes
-// (softmax - onehot) * dloss / T in bf16.  One block per row; two passes over
-// the row (the second hits L2).
+// lse = log z + m, nll = lse - x[target]; loss = mean nll, evaluated as
+// (m - x_t) + log1p(z - 1) so near-zero losses are not rounded to 0.
+// Backward writes (softmax - onehot) * dloss / T in bf16.  One block per row;
+// two passes over the row (the second hits L2).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void load8(const bf16* p, float* f) { unpack8(*reinterpret_cast<const uint4*>(p), f); }
 
@@ -261,27 +262,41 @@ __global__ void __launch_bounds__(kRowThreads) ce_fwd_kernel(const bf16* __restr
         for (int c = threadIdx.x; c < V; c += kRowThreads) m = fmaxf(m, bf2f(xr[c]));
     }
     m = block_max(m, red);
-    float z = 0.f;
+    // z - 1 = sum over every element but one occurrence of the maximum, kept
+    // apart from the max's exact 1.0 so confident rows keep their tiny loss:
+    // nll = (m - x_t) + log1p(z - 1).  Each thread leaves out its own first
+    // maximum; the surplus exclusions (ties across threads) are added back.
+    float z1 = 0.f;
+    bool seen = false;
     if (vec) {
         for (int c = threadIdx.x * 8; c < V; c += kRowThreads * 8) {
             float f[8];
             load8(xr + c, f);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) z += expf(f[i] - m);
+            for (int i = 0; i < 8; ++i) {
+                if (!seen && f[i] == m) seen = true;
+                else z1 += expf(f[i] - m);
+            }
         }
     } else {
-        for (int c = threadIdx.x; c < V; c += kRowThreads) z += expf(bf2f(xr[c]) - m);
+        for (int c = threadIdx.x; c < V; c += kRowThreads) {
+            const float f = bf2f(xr[c]);
+            if (!seen && f == m) seen = true;
+            else z1 += expf(f - m);
+        }
     }
-    z = block_sum(z, red);
+    z1 = block_sum(z1, red);
+    const float holders = block_sum(seen ? 1.f : 0.f, red);
+    z1 += holders - 1.f;
     if (threadIdx.x == 0) {
         const int64_t t = targets[row];
-        const float l = logf(z) + m;
-        lse[row] = l;
+        const float lp = log1pf(z1);
+        lse[row] = m + lp;
         if (t < 0 || t >= V) {
             atomicExch(err, 1);
             nll[row] = 0.f;
         } else {
-            nll[row] = l - bf2f(xr[t]);
+            nll[row] = (m - bf2f(xr[t])) + lp;
         }
     }
 }
