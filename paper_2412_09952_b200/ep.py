@@ -1,25 +1,27 @@
 """Expert parallelism for the E8T2 layer: one process per GPU, E/R experts per
-rank, NCCL all-to-all dispatch / combine (reference ownership
-rule moefold/upcycle.py:207-208, byte model moefold/plan.py:246-247).
+rank (reference ownership rule moefold/upcycle.py:207-208, byte
+model moefold/plan.py:246-247).  Two transports:
 
-Per rank r (T_local tokens, rank-local capacity, so routing equals the
-single-GPU oracle on that rank's batch):
+* "p2p" (default, `_EPPeerFunction`): the dispatch / combine exchange is fused
+  into the permute / combine kernels, which write and read the expert owners'
+  receive buffers directly over NVLink (torch symmetric memory, device
+  barriers).  Counts never leave the device; no host synchronisation.
+* "nccl" (`_EPFunction`, the comparison baseline): separate kernels around
+  NCCL all_to_all_single with exact splits (one host round trip for the
+  counts), per rank r (T_local tokens, rank-local capacity, so routing equals
+  the single-GPU oracle on that rank's batch):
 
-  forward   K1 router -> K1b dispatch (fixed layout: expert e's segment at
-            e * cap_pad) -> K2 permute into the send buffer [E, cap_pad, H]
-            -> all_to_all(counts[E]) and all_to_all(send) with equal splits
-            -> grouped GEMMs over R * E_local received segments
+  forward   K1 router -> K1b dispatch (compact layout) -> K2 permute into the
+            send buffer -> all_to_all(counts) -> all_to_all(rows, exact
+            splits) -> grouped GEMMs over R * E_local received segments
             -> all_to_all back -> K5 combine
   backward  K6 combine' -> all_to_all(dO) -> BWD2 / WGRAD / BWD1 over the
             received segments -> all_to_all(dxp) back -> router' ->
             all_reduce(dW_g, dW_noise)  (the router is replicated)
 
-Counts never leave the device: the GEMM kernels read the received counts
-directly, so no host synchronisation happens inside the layer.
-
-The data-movement plan (`EPPlan`) is plain torch and is exercised on CPU with
-the gloo backend in tests/test_ep_gloo.py; the compute runs only in the CUDA
-library.
+The fixed-capacity data-movement plan (`EPPlan`, used by the p2p receive
+buffers) is plain torch and is exercised on CPU with the gloo backend in
+tests/test_ep_gloo.py; the compute runs only in the CUDA library.
 """
 
 from __future__ import annotations
@@ -93,6 +95,44 @@ class EPPlan:
         return out
 
 
+class _Splits:
+    """Exact all-to-all splits of the NCCL transport.  Send side: the compact
+    dispatch layout (segments padded to 128 rows, experts in order), so the
+    rows for destination d are the padded segments of d's experts, contiguous.
+    Receive side: source-major, local-expert-minor padded segments.  Only kept
+    rows (+ <128 pad rows per segment) cross the wire, also when dropless."""
+
+    def __init__(self, counts, rcounts, plan: "EPPlan", device):
+        El = plan.e_local
+        ch = torch.stack([counts, rcounts]) if counts.numel() == rcounts.numel() else None
+        if ch is not None:
+            c_h, r_h = ch.cpu().tolist()
+        else:
+            c_h, r_h = counts.cpu().tolist(), rcounts.cpu().tolist()
+        pad = lambda c: (c + SEG_PAD - 1) // SEG_PAD * SEG_PAD  # noqa: E731
+        self.send = [sum(pad(c_h[d * El + el]) for el in range(El)) for d in range(plan.world)]
+        self.recv = [sum(pad(r_h[src * El + el]) for el in range(El)) for src in range(plan.world)]
+        self.rows_send, self.rows_recv = sum(self.send), sum(self.recv)
+        base, acc = [], 0
+        for c in r_h:
+            base.append(acc)
+            acc += pad(c)
+        self.rbase = torch.tensor(base, dtype=torch.int32, device=device)
+        self.rexp = torch.arange(plan.world * El, dtype=torch.int32, device=device) % El
+
+    def to_owners(self, rows_send: torch.Tensor, H: int, group) -> torch.Tensor:
+        out = torch.empty(max(self.rows_recv, 1), H, dtype=rows_send.dtype, device=rows_send.device)
+        dist.all_to_all_single(out[:self.rows_recv], rows_send[:self.rows_send], output_split_sizes=self.recv,
+                               input_split_sizes=self.send, group=group)
+        return out
+
+    def to_sources(self, rows_recv: torch.Tensor, H: int, group) -> torch.Tensor:
+        out = torch.empty(max(self.rows_send, 1), H, dtype=rows_recv.dtype, device=rows_recv.device)
+        dist.all_to_all_single(out[:self.rows_send], rows_recv[:self.rows_recv], output_split_sizes=self.send,
+                               input_split_sizes=self.recv, group=group)
+        return out
+
+
 class _EPFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w_g, w_noise, W1, W2, W3, z, st):
@@ -123,16 +163,19 @@ class _EPFunction(torch.autograd.Function):
         imp = torch.empty(E, **f32)
         stats = torch.empty(2, dtype=torch.int64, device=dev)
         _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if plan.capacity is None else plan.capacity,
-                  _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_FIXED, plan.cap_pad, slot_rank.data_ptr(),
+                  _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_COMPACT, 0, slot_rank.data_ptr(),
                   counts.data_ptr(), seg_base.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),
                   _dispatch_ws(dev).data_ptr(), s)
-        Rs = plan.send_rows
-        xs = torch.empty(Rs, H, **bf)
+        # exact splits: the compact layout keeps each destination's experts
+        # contiguous; one host round trip fetches both count vectors
+        rcounts = plan.exchange_counts(counts, group)
+        sp = _Splits(counts, rcounts, plan, dev)
+        xs = torch.empty(max(sp.rows_send, 1), H, **bf)
         _lib.call("b200moe_permute", x.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), counts.data_ptr(), T,
                   H, E, xs.data_ptr(), s)
-        rcounts = plan.exchange_counts(counts, group)
-        xr = plan.exchange_rows(torch.empty_like(xs), xs, group)
-        rbase, rexp = plan.recv_segments(dev)
+        xr = sp.to_owners(xs, H, group)
+        Rs = max(sp.rows_recv, 1)
+        rbase, rexp = sp.rbase, sp.rexp
         nseg = plan.world * El
         A = torch.empty(Rs, F, **bf)
         B = torch.empty(Rs, F, **bf)
@@ -142,13 +185,14 @@ class _EPFunction(torch.autograd.Function):
         Or = torch.empty(Rs, H, **bf)
         _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
                   rexp.data_ptr(), nseg, Rs, H, F, El, Or.data_ptr(), s)
-        Os = plan.exchange_rows(torch.empty_like(Or), Or, group)
+        Os = sp.to_sources(Or, H, group)
         y = torch.empty(T, H, **bf)
         _lib.call("b200moe_combine", Os.data_ptr(), gates.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), T,
                   H, E, y.data_ptr(), s)
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_base,
                              gate_mass=gate_mass, importance=imp, stats=stats, err=err, recv_counts=rcounts)
         ctx.st = st
+        ctx.splits = sp
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_base,
                               rcounts, xr, A, B, Hh, Os)
         return y, gates
@@ -163,20 +207,21 @@ class _EPFunction(torch.autograd.Function):
         E = w_g.shape[1]
         El = plan.e_local
         F = W1.shape[1]
-        Rs = plan.send_rows
+        sp = ctx.splits
+        Rs = max(sp.rows_recv, 1)
         dev = x.device
         s = _lib.stream_ptr()
         f32 = dict(dtype=torch.float32, device=dev)
         bf = dict(dtype=torch.bfloat16, device=dev)
         nseg = plan.world * El
-        rbase, rexp = plan.recv_segments(dev)
+        rbase, rexp = sp.rbase, sp.rexp
 
         dy = (torch.zeros(T, H, **bf) if dy is None else dy).to(torch.bfloat16).contiguous()
-        dOs = torch.empty(Rs, H, **bf)
+        dOs = torch.empty(max(sp.rows_send, 1), H, **bf)
         dg = torch.empty(T, E, **f32)
         _lib.call("b200moe_combine_bwd", dy.data_ptr(), Os.data_ptr(), gates.data_ptr(), slot_rank.data_ptr(),
                   seg_base.data_ptr(), counts.data_ptr(), T, H, E, dOs.data_ptr(), dg.data_ptr(), s)
-        dOr = plan.exchange_rows(torch.empty_like(dOs), dOs, group)
+        dOr = sp.to_owners(dOs, H, group)
         dA = torch.empty(Rs, F, **bf)
         dB = torch.empty(Rs, F, **bf)
         _lib.call("b200moe_expert_bwd2", dOr.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(), rbase.data_ptr(),
@@ -190,7 +235,7 @@ class _EPFunction(torch.autograd.Function):
         dxr = torch.empty(Rs, H, **bf)
         _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
                   rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dxr.data_ptr(), s)
-        dxs = plan.exchange_rows(torch.empty_like(dxr), dxr, group)
+        dxs = sp.to_sources(dxr, H, group)
         dx = torch.empty(T, H, **bf)
         dh = torch.empty(T, E, **f32)
         dn = torch.empty(T, E, **f32) if z is not None else None
@@ -549,7 +594,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                        "kept_slots_total": int(S_tot), "parallelism": f"ep{world}",
                        "comm": ("dispatch/combine fused into permute/combine kernels over NVLink symmetric memory "
                                 "(device barriers) + NCCL all_reduce(dW_g)" if args.transport == "p2p" else
-                                "NCCL all_to_all_single (equal splits, fixed capacity segments) + all_reduce(dW_g)"),
+                                "NCCL all_to_all_single (exact splits) + all_reduce(dW_g)"),
                        "transport": args.transport,
                        "l2": "working set > L2 (expert weights + activations)"},
             "mfu": {"measured_peak": round(flops / (ms_max * 1e-3) / (world * peak * 1e12), 4),
