@@ -47,7 +47,8 @@ def make_params(T, H, F, E, identical, seed=10, wscale=(0.5, 0.1, 0.3)):
     return wg, wn, w1, w2, w3, x, dy, z
 
 
-def run_and_compare(T, H, F, E, rt, pol, cf, noise, identical=False, lam=0.37, seed=10, wscale=(0.5, 0.1, 0.3)):
+def run_and_compare(T, H, F, E, rt, pol, cf, noise, identical=False, lam=0.37, seed=10, wscale=(0.5, 0.1, 0.3),
+                    k=2):
     wg, wn, w1, w2, w3, x, dy, z = make_params(T, H, F, E, identical, seed, wscale)
     dev = torch.device("cuda")
     W1 = torch.stack([torch.from_numpy(w.T.copy()) for w in w1]).to(dev, torch.bfloat16).requires_grad_()
@@ -58,7 +59,7 @@ def run_and_compare(T, H, F, E, rt, pol, cf, noise, identical=False, lam=0.37, s
     layer = B.MoELayer.from_stacked(B.RouterParams(wg_t, wn_t), W1, W2, W3)
     x_t = torch.from_numpy(x).to(dev, torch.bfloat16).requires_grad_()
     dy_t = torch.from_numpy(dy).to(dev)
-    cfg = B.GateConfig(n_experts=E, top_k=2, router_type=rt, noise_enabled=noise, capacity_factor=cf,
+    cfg = B.GateConfig(n_experts=E, top_k=k, router_type=rt, noise_enabled=noise, capacity_factor=cf,
                        drop_policy=pol)
     out = B.moe_forward(x_t, layer, cfg, training=True, noise=torch.from_numpy(z).to(dev) if noise else None)
     loss = (out.output.float() * dy_t).sum() + lam * B.importance_penalty(out.gates)
@@ -71,7 +72,7 @@ def run_and_compare(T, H, F, E, rt, pol, cf, noise, identical=False, lam=0.37, s
     w1r = [bf16_round(w) for w in w1]
     w2r = [bf16_round(w) for w in w2]
     w3r = [bf16_round(w) for w in w3]
-    ocfg = O.LayerCfg(n_experts=E, top_k=2, router_type=rt, noise=noise, capacity_factor=cf, drop_policy=pol)
+    ocfg = O.LayerCfg(n_experts=E, top_k=k, router_type=rt, noise=noise, capacity_factor=cf, drop_policy=pol)
     y_o, g_o, cache = O.moe_forward(xr, wg, wn, w1r, w2r, w3r, ocfg, z=z if noise else None, logits=logits)
     _, dimp = O.importance_penalty(g_o)
     gr = O.moe_backward(cache, bf16_round(dy), dgates=lam * dimp)
@@ -121,6 +122,14 @@ def test_cfg1_upcycled_layer(rt, cf):
     # exactly (sum of p*(dg - dg) = 0), so dW_g is carried by the aux term.
     run_and_compare(2048, 256, 512, 8, rt, "position", cf, False, identical=True, lam=1.0,
                     wscale=(0.02, 0.0, 0.02))
+
+
+@pytest.mark.parametrize("E,k", [(2, 1), (4, 2), (4, 4), (6, 3), (16, 2), (16, 5), (32, 2), (32, 8)])
+@pytest.mark.parametrize("rt,pol,cf", [("mixtral", "position", 1.0), ("st", "score", 2.0), ("mixtral", "score", None)])
+def test_expert_count_and_fanout_sweep(E, k, rt, pol, cf):
+    """Other E / top-k than E8T2 (every router / dispatch / backward template
+    bucket: E in 4, 8, 16, 32 buckets, kept-per-token 1..8), with noise."""
+    run_and_compare(160, 32, 48, E, rt, pol, cf, True, k=k, seed=30 + E + k)
 
 
 @pytest.mark.parametrize("pol", ["position", "score"])
