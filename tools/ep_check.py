@@ -21,8 +21,7 @@ def rel(a, b):
     return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
 
 
-def case(rank, world, dev, T, H, F, router, policy, cf, noise, transport):
-    E = 8
+def case(rank, world, dev, T, H, F, router, policy, cf, noise, transport, E=8, k=2):
     El = E // world
     g = torch.Generator(device=dev).manual_seed(5)
     W1 = (torch.randn(E, F, H, generator=g, device=dev) * 0.05).to(torch.bfloat16)
@@ -34,7 +33,7 @@ def case(rank, world, dev, T, H, F, router, policy, cf, noise, transport):
     x = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
     dy = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
     z = torch.randn(T, E, generator=gx, device=dev) if noise else None
-    cfg = P.GateConfig(n_experts=E, top_k=2, router_type=router, noise_enabled=noise, capacity_factor=cf,
+    cfg = P.GateConfig(n_experts=E, top_k=k, router_type=router, noise_enabled=noise, capacity_factor=cf,
                        drop_policy=policy)
     own = slice(rank * El, (rank + 1) * El)
 
@@ -78,7 +77,7 @@ def case(rank, world, dev, T, H, F, router, policy, cf, noise, transport):
         refn = rw[1].grad.clone()
         dist.all_reduce(refn)
         check("dW_noise", rel(lw[1].grad, refn) < 2e-2)
-    tag = f"[{transport}] T={T} H={H} F={F} {router} {policy} cf={cf} noise={noise}"
+    tag = f"[{transport}] T={T} H={H} F={F} E={E} k={k} {router} {policy} cf={cf} noise={noise}"
     print(f"rank {rank}: {'PASS' if ok else 'FAIL ' + ','.join(msgs)} {tag}", flush=True)
     return ok
 
@@ -96,6 +95,8 @@ def main():
                      (512, 256, 512, "mixtral", "position", None, False),
                      (2048, 1024, 1024, "mixtral", "position", 0.5, False)]:
             ok &= case(rank, world, dev, *args, transport)
+        # more experts than E8T2 and a wider fan-out (E/N experts per rank, k=4)
+        ok &= case(rank, world, dev, 768, 512, 512, "st", "score", None, True, transport, E=16, k=4)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     dist.destroy_process_group()
