@@ -15,29 +15,41 @@
 namespace b200moe {
 
 constexpr int kTile = 64;
+constexpr int kTPad = 8;   // row stride 72 bf16 = 144 B: 16-byte aligned rows, 4-way conflicts on the transposed fill
 
-// src [R, C] (fp32 or bf16) -> dst[e] [C, R] bf16 for e < E_local.
+// src [R, C] (fp32 or bf16) -> dst[e] [C, R] bf16 for e < E_local.  The tile
+// is transposed on its way into shared memory, so each output row segment is
+// 8 contiguous bf16 there and goes out as one 16-byte store per expert copy
+// (the E_local-fold write stream is what bounds this kernel).
 template <typename T>
 __global__ void __launch_bounds__(256) transpose_replicate(const T* __restrict__ src, int R, int C, int E_local,
                                                            __nv_bfloat16* __restrict__ dst) {
-    __shared__ __nv_bfloat16 tile[kTile][kTile + 2];
+    __shared__ __align__(16) __nv_bfloat16 tile[kTile][kTile + kTPad];   // tile[c][r]
     const int r0 = blockIdx.y * kTile, c0 = blockIdx.x * kTile;
     for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
-        const int r = i / kTile, c = i % kTile;
+        const int r = i / kTile, c = i % kTile;   // coalesced along c in the source
         __nv_bfloat16 v = __float2bfloat16_rn(0.f);
         if (r0 + r < R && c0 + c < C) {
             if constexpr (sizeof(T) == 4) v = __float2bfloat16_rn(src[(size_t)(r0 + r) * C + c0 + c]);
             else v = src[(size_t)(r0 + r) * C + c0 + c];
         }
-        tile[r][c] = v;
+        tile[c][r] = v;
     }
     __syncthreads();
     const size_t plane = (size_t)R * C;
-    for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
-        const int c = i / kTile, r = i % kTile;  // dst row = c, dst col = r
-        if (r0 + r < R && c0 + c < C) {
-            const __nv_bfloat16 v = tile[r][c];
-            for (int e = 0; e < E_local; ++e) dst[e * plane + (size_t)(c0 + c) * R + r0 + r] = v;
+    const bool vec = (R % 8) == 0;
+    for (int i = threadIdx.x; i < kTile * (kTile / 8); i += blockDim.x) {
+        const int c = i / (kTile / 8), r = (i % (kTile / 8)) * 8;   // 8 consecutive destination columns
+        if (c0 + c >= C || r0 + r >= R) continue;
+        __nv_bfloat16* out = dst + (size_t)(c0 + c) * R + r0 + r;
+        if (vec && r0 + r + 8 <= R) {
+            const uint4 v = *reinterpret_cast<const uint4*>(&tile[c][r]);
+            for (int e = 0; e < E_local; ++e) *reinterpret_cast<uint4*>(out + e * plane) = v;
+        } else {
+            for (int j = 0; j < 8 && r0 + r + j < R; ++j) {
+                const __nv_bfloat16 v = tile[c][r + j];
+                for (int e = 0; e < E_local; ++e) out[e * plane + j] = v;
+            }
         }
     }
 }
