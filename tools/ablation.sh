@@ -9,3 +9,6 @@ for cf in 1.0 2.0 4.0; do
   done
   timeout 300 python bench.py --steps 15 --warmup 4 --cf $cf --router mixtral --policy score --no-cpu-baseline --no-e2e 2>/dev/null | grep "^{"
 done
+for r in mixtral st; do   # dropless (CF=None)
+  timeout 300 python bench.py --steps 15 --warmup 4 --cf none --router $r --no-cpu-baseline --no-e2e 2>/dev/null | grep "^{"
+done
