@@ -201,3 +201,22 @@ def test_tiny_model_training_run_tracks_reference(tiny, tmp_path):
     ref = str(tiny["routing_csv"]).splitlines()
     assert got[0] == ref[0] and len(got) == len(ref)
     assert (tmp_path / "m.csv").read_text().splitlines()[0] == str(tiny["metrics_csv"]).splitlines()[0]
+
+
+def test_tiny_model_training_with_router_noise(tiny):
+    """Training with noise_enabled: z ~ Rng(noise_seed, step) drawn layer by
+    layer on the host (train.py:283-285), losses track the reference's."""
+    import paper_2412_09952_b200 as P
+    cfg = json.loads(str(tiny["config"]))
+    t = cfg["train"]
+    m = P.ModelConfig(**cfg["model"])
+    g = cfg["gate"]
+    moe = P.upcycle_full(P.init_dense(m, seed=3), g["n_experts"], g["top_k"], moe_layers=tuple(g["moe_layers"]),
+                         router_seed=g["router_seed"], capacity_factor=g["capacity_factor"], noise_enabled=True)
+    spec = P.BlendSpec(tuple(tuple(s) for s in t["blend"][0]), t["blend"][1])
+    lo, hi, wu, tot = t["lr"]
+    tc = P.TrainConfig(steps=3, schedule=P.Schedule(lo, hi, wu, tot), blend=spec, batch_size=t["batch_size"],
+                       seq_len=t["seq_len"], aux_loss_coeff=t["aux"], noise_seed=9)
+    run = P.train(moe, tc, run_id="tiny_noise")
+    np.testing.assert_allclose(run.loss, tiny["noise_train_loss"], rtol=3e-3)
+    np.testing.assert_allclose(run.load_entropy, tiny["noise_train_entropy"], atol=5e-2)
