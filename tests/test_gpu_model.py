@@ -220,3 +220,39 @@ def test_tiny_model_training_with_router_noise(tiny):
     run = P.train(moe, tc, run_id="tiny_noise")
     np.testing.assert_allclose(run.loss, tiny["noise_train_loss"], rtol=3e-3)
     np.testing.assert_allclose(run.load_entropy, tiny["noise_train_entropy"], atol=5e-2)
+
+
+def test_overlapped_optimizer_equals_serial_step(tiny):
+    """OverlappedStep (per-tensor updates on a side stream, launched from
+    post-accumulate hooks during the backward) gives the same weights as
+    Optimizer.step after the backward, bit for bit, over 3 steps."""
+    import paper_2412_09952_b200 as P
+    from paper_2412_09952_b200.train import OverlappedStep, TrainState
+    cfg = json.loads(str(tiny["config"]))
+    tokens = tiny["tokens"]
+    inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
+    runs = []
+    for overlapped in (False, True):
+        moe = _tiny_moe(cfg)
+        state = TrainState(moe)
+        opt = state.optimizer("adam")
+        ov = OverlappedStep(opt) if overlapped else None
+        for step in range(3):
+            lr = 1e-3 * (step + 1)
+            fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute)
+            loss = P.cross_entropy(fwd.logits, targets)
+            for g in fwd.gates:
+                loss = loss + 0.01 * P.importance_penalty(g)
+            for p in opt.params.values():
+                p.grad = None
+            if ov is not None:
+                ov.begin(lr)
+                loss.backward()
+                ov.finish()
+            else:
+                loss.backward()
+                opt.step(lr)
+        torch.cuda.synchronize()
+        runs.append({n: m.detach().clone() for n, m in opt.master.items()})
+    for name in runs[0]:
+        assert torch.equal(runs[0][name], runs[1][name]), name

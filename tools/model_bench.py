@@ -23,7 +23,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2412_09952_b200 as P  # noqa: E402
-from paper_2412_09952_b200.train import DataParallelGrads, TrainState  # noqa: E402
+from paper_2412_09952_b200.train import DataParallelGrads, OverlappedStep, TrainState  # noqa: E402
 
 
 def model_flops(cfg, gate, tokens: int, kept_slots: int) -> float:
@@ -60,6 +60,8 @@ def main():
     ap.add_argument("--small", action="store_true", help="tiny shape for a smoke run")
     ap.add_argument("--no-shadows", action="store_true", help="cast fp32 GEMM weights per step instead")
     ap.add_argument("--transport", default="p2p", choices=("p2p", "nccl"))
+    ap.add_argument("--serial-opt", action="store_true",
+                    help="optimizer after the backward in one launch (default: overlapped with the backward)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = 0
@@ -85,7 +87,8 @@ def main():
     del dense
     state = TrainState(moe, shadows=not a.no_shadows)
     opt = state.optimizer("adam")
-    dp = DataParallelGrads(state.leaves, group) if world > 1 else None
+    ov = None if a.serial_opt else OverlappedStep(opt, group)
+    dp = DataParallelGrads(state.leaves, group) if (world > 1 and ov is None) else None
     rng = np.random.default_rng(rank)
     tokens = rng.integers(0, cfg.vocab, (a.batch, a.seq + 1))
     inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
@@ -105,12 +108,17 @@ def main():
             ev[1].record()
         for p in opt.params.values():
             p.grad = None
+        if ov is not None:
+            ov.begin(1e-4)
         loss.backward()
         if dp is not None:
             dp.wait()
         if ev is not None:
             ev[2].record()
-        opt.step(1e-4)
+        if ov is not None:
+            ov.finish()          # updates ran on the side stream during the backward
+        else:
+            opt.step(1e-4)
         if ev is not None:
             ev[3].record()
         return loss, fwd.stats
@@ -154,7 +162,9 @@ def main():
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
         "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
                    "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": 8,
-                   "top_k": 2, "capacity_factor": a.cf, "optimizer": "adam (fp32 masters)"},
+                   "top_k": 2, "capacity_factor": a.cf,
+                   "optimizer": "adam (fp32 masters), " + ("after the backward" if a.serial_opt else
+                                                           "per tensor on a side stream during the backward")},
         "data": "synthetic (random token ids, random-init weights)",
     }
     print(json.dumps(out))
