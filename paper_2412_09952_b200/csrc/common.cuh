@@ -1,6 +1,7 @@
 // Shared helpers for the b200moe CUDA library (sm_100a only).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -15,6 +16,12 @@ namespace b200moe {
 
 // Thread-local error message behind b200moe_last_error().
 void set_error(const char* fmt, ...);
+
+// 2-D bf16 TMA map over a row-major [outer, inner] tensor (row pitch ld
+// elements), box {box_inner, box_outer}, no swizzle (rows land contiguous in
+// shared memory), out-of-bounds rows zero-filled.  Returns a B200MOE_* code.
+int make_tmap_bf16_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                      uint32_t box_inner, uint32_t box_outer);
 
 #define B200_CHECK_ARG(cond, code, ...)          \
     do {                                         \

@@ -89,7 +89,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 #define B200MOE_WATCHDOG_SPINS (1u << 28)
 #endif
 
-__device__ __noinline__ void watchdog_trap(uint32_t parity) {
+static __device__ __noinline__ void watchdog_trap(uint32_t parity) {
     printf("b200moe: mbarrier wait timed out (block %d thread %d parity %u)\n", blockIdx.x, threadIdx.x, parity);
     __trap();
 }
@@ -115,6 +115,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 }
 
 // ---------------------------------------------------------------- TMA
+// 1-D bulk async copy global -> shared (bytes: multiple of 16, both 16-byte
+// aligned), completing on `bar` with transaction-count bytes.
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }

@@ -14,6 +14,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "ptx.cuh"
 #include "npexp.cuh"
 
 namespace b200moe {
@@ -167,8 +168,17 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict_
                                                  : make_uint4(0, 0, 0, 0);
     const float4* W = wsw;
     if constexpr (kSmemW) {
-        for (int i = threadIdx.x; i < nvec; i += blockDim.x) smem_w[i] = wsw[i];
+        // the swizzled W table (H*EP floats) arrives with one bulk async copy
+        // (a float4 load loop here cost ~16 dependent L2 round trips per block)
+        __shared__ uint64_t wbar;
+        if (threadIdx.x == 0) {
+            ptx::mbar_init(&wbar, 1);
+            ptx::fence_mbar_init();
+            ptx::mbar_arrive_expect_tx(&wbar, (uint32_t)(nvec * 16));
+            ptx::bulk_load_1d(smem_w, wsw, (uint32_t)(nvec * 16), &wbar);
+        }
         __syncthreads();
+        ptx::mbar_wait(&wbar, 0);
         W = smem_w;
     }
 

@@ -20,6 +20,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace b200moe {
 
@@ -109,7 +110,9 @@ router_dh_kernel(const int32_t* __restrict__ slot_rank, const int32_t* __restric
 // ---- pass 2: warp per TT tokens, lane owns 8 hidden units per 256-wide chunk
 constexpr int kDxThreads = 256;
 // 32/EP tokens per warp (4 at E=8).  Two tokens per warp cut registers from 128
-// to 80 but measured slower in the bench (0.062 -> 0.088 ms: W traffic doubles).
+// to 80 but measured slower in the bench (0.062 -> 0.088 ms: W traffic doubles);
+// W_g in shared memory (bulk copy) with 2 tokens per warp, 16 warps per block
+// and a one-chunk prefetch of the dxp rows measured 45.4 vs 42.9 us (ncu).
 __host__ __device__ constexpr int dx_tokens_per_warp(int ep) { return 32 / ep; }
 
 template <int EP, int KM, bool kNoise>
@@ -259,82 +262,131 @@ router_wgrad_partial(const __nv_bfloat16* __restrict__ x, const float* __restric
             if (e < E) p[(size_t)(h0 + j) * E + e] = acc[j][e];
 }
 
-// E <= 8, long token runs: a block owns 256 hidden units x kW3Tok tokens; each
-// warp walks its 64 tokens in groups of 8 rows (512 contiguous bytes per row),
-// the next group's loads in flight while the current one is accumulated in
-// registers; one cross-warp reduction per block, so the partial buffer is
-// ceil(T/512) x H x E floats (2 MiB at the bench shape).
-constexpr int kW3Tok = 512;
-constexpr int kW3Grp = 8;
-constexpr int kW3PerWarp = kW3Tok / 8;
+// E <= 8, TMA ring: a block owns 256 hidden units x kRgTok tokens.  A producer
+// thread streams the block's x tile into a kRgStages-deep shared-memory ring,
+// one 2-D TMA box (256 hidden x 32 tokens, 16 KB) per stage (32 separate 1-D
+// row copies per stage were request-rate bound: 41 us vs 38 us with the
+// prologue fixed), so ~64 KB per block are in flight without registers;
+// 8 consumer warps take 4 rows of each 32-row stage, accumulate 8 hidden x EP
+// experts per lane in registers, and hand the slot back.  One cross-warp
+// reduction per block (through the drained ring), fixed order: deterministic.
+constexpr int kRgTok = 512;
+constexpr int kRgStageRows = 32;
+constexpr int kRgStages = 4;
+constexpr int kRgStageBytes = kRgStageRows * 256 * 2;   // 16 KB
+constexpr int kRgConsumers = 8;
 
 template <int EP>
-__global__ void __launch_bounds__(256)
-router_wgrad_partial3(const __nv_bfloat16* __restrict__ x, const float* __restrict__ d, int T, int H, int E,
-                      float* __restrict__ part) {
-    extern __shared__ float sm[];
-    float* ds = sm;                                  // [kW3Tok][EP]
-    float* red = sm + kW3Tok * EP;                   // [8 warps][256 h][EP]
+__global__ void __launch_bounds__((kRgConsumers + 1) * 32, 2)
+router_wgrad_ring(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ d, int T, int H, int E,
+                  float* __restrict__ part) {
+    extern __shared__ __align__(128) uint8_t sm_raw[];
+    __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(sm_raw);
+    float* ds = reinterpret_cast<float*>(sm_raw + kRgStages * kRgStageBytes);       // [kRgTok][EP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ds + kRgTok * EP);
+    uint64_t* empty = full + kRgStages;
+    uint64_t* dsbar = empty + kRgStages;
     const int chunk = blockIdx.y;
-    const int t0 = chunk * kW3Tok;
+    const int t0 = chunk * kRgTok;
     const int h0 = blockIdx.x * 256;
+    const int hw = min(256, H - h0);                       // hidden units of this block (multiple of 8)
+    const int ntok = min(kRgTok, T - t0);
+    const int nst = ceil_div(ntok, kRgStageRows);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int hl = lane * 8;
-    const int tw = t0 + warp * kW3PerWarp;
-    const bool hok = h0 + hl < H;
-    auto load = [&](uint4* u, int g) {
-#pragma unroll
-        for (int i = 0; i < kW3Grp; ++i) {
-            const int t = tw + g * kW3Grp + i;
-            u[i] = (t < T && hok) ? ld_nc_v4(x + (size_t)t * H + h0 + hl) : make_uint4(0, 0, 0, 0);
+    // the block's dh rows: one bulk copy when they are contiguous in the [T, EP]
+    // layout (E == EP), else an unrolled gather (a dependent load loop here
+    // was the kernel's main stall)
+    const bool dh_bulk = (E == EP) && ((ntok * E * 4) % 16 == 0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kRgStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], kRgConsumers);
         }
-    };
-    uint4 u[kW3Grp];
-    load(u, 0);
-    for (int i = threadIdx.x; i < kW3Tok * EP; i += blockDim.x) {
-        const int tt = i / EP, e = i % EP;
-        const int t = t0 + tt;
-        ds[i] = (t < T && e < E) ? d[(size_t)t * E + e] : 0.f;
+        ptx::mbar_init(dsbar, 1);
+        ptx::fence_mbar_init();
     }
     __syncthreads();
-    float acc[8][EP];
+    if (dh_bulk) {
+        if (threadIdx.x == 0) {
+            ptx::mbar_arrive_expect_tx(dsbar, (uint32_t)(ntok * E * 4));
+            ptx::bulk_load_1d(ds, d + (size_t)t0 * E, (uint32_t)(ntok * E * 4), dsbar);
+        }
+    } else {
+        constexpr int kPer = (kRgTok * EP + (kRgConsumers + 1) * 32 - 1) / ((kRgConsumers + 1) * 32);
+        float v[kPer];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+        for (int u = 0; u < kPer; ++u) {
+            const int i = threadIdx.x + u * blockDim.x;
+            const int tt = i / EP, e = i % EP, t = t0 + tt;
+            v[u] = (i < kRgTok * EP && t < T && e < E) ? d[(size_t)t * E + e] : 0.f;
+        }
 #pragma unroll
-        for (int e = 0; e < EP; ++e) acc[j][e] = 0.f;
-    for (int g = 0; g < kW3PerWarp / kW3Grp; ++g) {
-        uint4 un[kW3Grp];
-        if (g + 1 < kW3PerWarp / kW3Grp) load(un, g + 1);
-#pragma unroll
-        for (int i = 0; i < kW3Grp; ++i) {
-            float xv[8];
-            unpack8(u[i], xv);
-            const float* dr = ds + (warp * kW3PerWarp + g * kW3Grp + i) * EP;
-#pragma unroll
-            for (int e = 0; e < EP; ++e) {
-                const float dv = dr[e];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j][e] = fmaf(xv[j], dv, acc[j][e]);
+        for (int u = 0; u < kPer; ++u) {
+            const int i = threadIdx.x + u * blockDim.x;
+            if (i < kRgTok * EP) ds[i] = v[u];
+        }
+        __syncthreads();
+    }
+    if (warp == kRgConsumers) {            // producer: one 2-D TMA box (256 hidden x 32 tokens) per stage
+        if (lane == 0) {
+            for (int st = 0; st < nst; ++st) {
+                const int slot = st % kRgStages;
+                if (st >= kRgStages) ptx::mbar_wait(&empty[slot], ((st / kRgStages) - 1) & 1);
+                ptx::mbar_arrive_expect_tx(&full[slot], (uint32_t)kRgStageBytes);   // OOB rows arrive as zeros
+                ptx::tma_load_2d(&xmap, &full[slot], ring + (size_t)slot * kRgStageRows * 256, h0,
+                                 t0 + st * kRgStageRows);
             }
         }
+    } else {                               // consumers
+        float acc[8][EP];
 #pragma unroll
-        for (int i = 0; i < kW3Grp; ++i) u[i] = un[i];
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int e = 0; e < EP; ++e) acc[j][e] = 0.f;
+        const bool hok = lane * 8 < hw;
+        if (dh_bulk) ptx::mbar_wait(dsbar, 0);
+        for (int st = 0; st < nst; ++st) {
+            const int slot = st % kRgStages;
+            ptx::mbar_wait(&full[slot], (st / kRgStages) & 1);
+            const int rows = min(kRgStageRows, ntok - st * kRgStageRows);
+            const __nv_bfloat16* base = ring + (size_t)slot * kRgStageRows * 256;
+#pragma unroll
+            for (int i = 0; i < kRgStageRows / kRgConsumers; ++i) {
+                const int r = warp * (kRgStageRows / kRgConsumers) + i;
+                if (r < rows && hok) {
+                    float xv[8];
+                    unpack8(*reinterpret_cast<const uint4*>(base + r * 256 + lane * 8), xv);
+                    const float* dr = ds + (st * kRgStageRows + r) * EP;
+#pragma unroll
+                    for (int e = 0; e < EP; ++e) {
+                        const float dv = dr[e];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) acc[j][e] = fmaf(xv[j], dv, acc[j][e]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+        }
+        __syncthreads();                    // (A) every consumer is done with the ring
+        float* rw = reinterpret_cast<float*>(sm_raw) + (size_t)warp * 256 * EP;   // [(j*EP+e)*32 + lane]
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int e = 0; e < EP; ++e) rw[(j * EP + e) * 32 + lane] = acc[j][e];
     }
-    float* rw = red + (size_t)warp * 256 * EP;  // [(j * EP + e) * 32 + lane]: conflict-free
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-#pragma unroll
-        for (int e = 0; e < EP; ++e) rw[(j * EP + e) * 32 + lane] = acc[j][e];
+    if (warp == kRgConsumers) __syncthreads();   // matches (A)
     __syncthreads();
+    const float* red = reinterpret_cast<const float*>(sm_raw);
     float* p = part + (size_t)chunk * H * E;
     for (int i = threadIdx.x; i < 256 * EP; i += blockDim.x) {
         const int l = i % 32, je = i / 32;
         const int j = je / EP, e = je % EP;
         const int hh = l * 8 + j;
-        float s = 0.f;
+        float sum = 0.f;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) s += red[(size_t)w * 256 * EP + i];
-        if (e < E && h0 + hh < H) p[(size_t)(h0 + hh) * E + e] = s;
+        for (int w = 0; w < kRgConsumers; ++w) sum += red[(size_t)w * 256 * EP + i];
+        if (e < E && hh < hw) p[(size_t)(h0 + hh) * E + e] = sum;
     }
 }
 
@@ -492,12 +544,18 @@ template <int EP>
 int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, float* part, cudaStream_t stream) {
     int nch = ceil_div(T, kWgTok);
     if constexpr (EP <= 8) {
-        nch = ceil_div(T, kW3Tok);
-        const size_t sh = (size_t)(kW3Tok * EP + 8 * 256 * EP) * sizeof(float);
-        auto kern = router_wgrad_partial3<EP>;
+        nch = ceil_div(T, kRgTok);
+        const size_t sh = (size_t)kRgStages * kRgStageBytes + (size_t)kRgTok * EP * sizeof(float) +
+                          (2 * kRgStages + 1) * sizeof(uint64_t);
+        static_assert((size_t)kRgConsumers * 256 * 8 * sizeof(float) <= (size_t)kRgStages * kRgStageBytes,
+                      "the drained ring holds the cross-warp reduction");
+        CUtensorMap xmap;
+        const int rc = make_tmap_bf16_2d(&xmap, x, (uint64_t)H, (uint64_t)T, (uint64_t)H, 256, kRgStageRows);
+        if (rc) return rc;
+        auto kern = router_wgrad_ring<EP>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
         dim3 grid(ceil_div(H, 256), nch);
-        kern<<<grid, 256, sh, stream>>>((const __nv_bfloat16*)x, d, T, H, E, part);
+        kern<<<grid, (kRgConsumers + 1) * 32, sh, stream>>>(xmap, d, T, H, E, part);
     } else {
         dim3 grid(ceil_div(H, 1024), nch);
         router_wgrad_partial<EP><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, d, T, H, E, part);
