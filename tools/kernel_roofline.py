@@ -28,7 +28,7 @@ ALG = {  # algorithmic bytes per launch (bf16 activations, fp32 [T, E] routing t
     "combine_kernel": S * H * BF + T * H * BF + T * E * 4,
     "combine_bwd_kernel": T * H * BF + 2 * S * H * BF + T * E * 4,
     "router_dx_kernel": S * H * BF + T * H * BF,
-    "router_wgrad_partial3": T * H * BF + T * E * 4,
+    "router_wgrad_ring": T * H * BF + T * E * 4,
     "router_dh_kernel": 4 * T * E * 4,
 }
 
