@@ -577,6 +577,24 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     kt = kp.times_ms()
     gemm_ms = sum(v[0] for k_, v in kt.items() if k_.startswith("b200moe_expert_")) / n_prof
     achieved = 18.0 * H * F * S / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    # NVLink side of the fused exchange (p2p): bytes each peer kernel moves to or
+    # from other ranks' buffers per step -- (R-1)/R of this rank's kept rows
+    # (S_send of them, H bf16 each) one way -- against the measured 770 GB/s per
+    # direction (B200_PROFILING.md).  Event times include the kernels' local work.
+    exchange = None
+    if args.transport == "p2p" and world > 1:
+        s_send = int(out.routing["counts"].sum().item())
+        remote = s_send * H * 2 * (world - 1) / world
+        per = {"b200moe_permute_peer": remote, "b200moe_combine_peer": remote,
+               "b200moe_combine_bwd_peer": 2 * remote, "b200moe_router_bwd_peer": remote}
+        exchange = {}
+        for name, nbytes in per.items():
+            if name in kt:
+                t_ms = kt[name][0] / n_prof
+                exchange[name.replace("b200moe_", "")] = {
+                    "ms": round(t_ms, 4), "nvlink_bytes": int(nbytes),
+                    "GBps": round(nbytes / (t_ms * 1e-3) / 1e9, 1),
+                    "frac_of_770": round(nbytes / (t_ms * 1e-3) / 1e9 / 770.0, 3)}
     if rank == 0:
         tps = world * T / (ms_max * 1e-3)
         flops = 18.0 * H * F * S_tot + 6.0 * world * T * H * E
@@ -608,5 +626,6 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                     "h2d_bytes_per_step": world * e2e_rank["h2d_bytes_per_step"], "d2h_bytes_per_step": 4 * world,
                     "h2d": e2e_rank["h2d"]},
             "cpu_baseline": None, "clocks": clocks, "gpu_launches": prof.launches,
+            "exchange": exchange,
         }
         print(json.dumps(line), flush=True)
