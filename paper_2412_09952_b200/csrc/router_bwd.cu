@@ -112,7 +112,9 @@ constexpr int kDxThreads = 256;
 // 32/EP tokens per warp (4 at E=8).  Two tokens per warp cut registers from 128
 // to 80 but measured slower in the bench (0.062 -> 0.088 ms: W traffic doubles);
 // W_g in shared memory (bulk copy) with 2 tokens per warp, 16 warps per block
-// and a one-chunk prefetch of the dxp rows measured 45.4 vs 42.9 us (ncu).
+// and a one-chunk prefetch of the dxp rows measured 45.4 vs 42.9 us (ncu); the
+// dxp rows through a 3-stage cp.async ring (96 KB per block) 56.0 us -- the
+// ring evicts the 128 KB W_g table from L1.
 __host__ __device__ constexpr int dx_tokens_per_warp(int ep) { return 32 / ep; }
 
 template <int EP, int KM, bool kNoise>
