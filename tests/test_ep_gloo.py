@@ -80,9 +80,10 @@ def _worker(rank, world, port, cf, policy, router, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("cf,policy,router", [(1.0, "position", "mixtral"), (0.5, "score", "st"),
-                                              (None, "position", "mixtral")])
+@pytest.mark.parametrize("world,cf,policy,router",
+                         [(w, *c) for w in (2, 4) for c in ((1.0, "position", "mixtral"), (0.5, "score", "st"),
+                                                           (None, "position", "mixtral"))]
+                         + [(8, 1.0, "position", "mixtral")])   # one expert per rank, as on an 8-GPU box
 def test_ep_plan_matches_rank_local_oracle(world, cf, policy, router):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
