@@ -566,35 +566,11 @@ def moe_forward(x: torch.Tensor, layer: MoELayer, cfg: GateConfig, rng: Rng | No
 
 
 def ffn_forward(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
-    """SwiGLU feed-forward down(silu(gate(x)) * up(x)) (moe.py:131-133) as a
-    one-segment grouped GEMM; reference [in, out] weight shapes.  Forward only."""
-    _require_cuda(x, "x")
-    T, H = x.shape
-    F = w1.shape[1]
-    Hp, Fp = _pad_to(H, GEMM_ALIGN), _pad_to(F, GEMM_ALIGN)
-    dev = x.device
-    R = _pad_to(T, SEG_PAD)
-    bf = dict(dtype=torch.bfloat16, device=dev)
-    xp = torch.zeros(R, Hp, **bf)
-    xp[:T, :H] = x.detach()
-    W1 = torch.zeros(1, Fp, Hp, **bf)
-    W3 = torch.zeros(1, Fp, Hp, **bf)
-    W2 = torch.zeros(1, Hp, Fp, **bf)
-    W1[0, :F, :H] = w1.detach().t()
-    W3[0, :F, :H] = w3.detach().t()
-    W2[0, :H, :F] = w2.detach().t()
-    base = torch.zeros(1, dtype=torch.int32, device=dev)
-    cnt = torch.full((1,), T, dtype=torch.int32, device=dev)
-    s = _lib.stream_ptr()
-    A = torch.empty(R, Fp, **bf)
-    B = torch.empty(R, Fp, **bf)
-    Hh = torch.empty(R, Fp, **bf)
-    _lib.call("b200moe_expert_fwd1", xp.data_ptr(), W1.data_ptr(), W3.data_ptr(), base.data_ptr(), cnt.data_ptr(),
-              base.data_ptr(), 1, R, Hp, Fp, 1, A.data_ptr(), B.data_ptr(), Hh.data_ptr(), s)
-    O = torch.empty(R, Hp, **bf)
-    _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), base.data_ptr(), cnt.data_ptr(), base.data_ptr(),
-              1, R, Hp, Fp, 1, O.data_ptr(), s)
-    return O[:T, :H]
+    """SwiGLU feed-forward down(silu(gate(x)) * up(x)) (moe.py:131-133) with the
+    reference [in, out] weight shapes, as a one-segment grouped GEMM;
+    differentiable (tensor.ffn).  Returns bf16 [T, H]."""
+    from .tensor import ffn
+    return ffn(x, w1, w2, w3)
 
 
 # --------------------------------------------------------------------------
