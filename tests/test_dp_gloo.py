@@ -43,7 +43,8 @@ def _worker(rank, world, port, q):
         loss.backward()
         dp.wait()
         dp.remove()
-        q.put((rank, {k: (None if v.grad is None else v.grad.clone()) for k, v in leaves.items()}))
+        # numpy, not tensors: a tensor is shared by fd and the sender may exit first
+        q.put((rank, {k: (None if v.grad is None else v.grad.numpy().copy()) for k, v in leaves.items()}))
     finally:
         dist.destroy_process_group()
 
@@ -71,7 +72,7 @@ def test_data_parallel_grads_sum_replicated_only(world):
         for k in want:
             want[k] += ls[k].grad
     for r in range(world):
-        g = res[r]
+        g = {k: (None if v is None else torch.from_numpy(v)) for k, v in res[r].items()}
         for k in want:
             torch.testing.assert_close(g[k], want[k], rtol=1e-5, atol=1e-5)
         assert g["layers.0.moe.router.wnoise"] is None
