@@ -53,6 +53,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                    help="EP exchange: fused NVLink peer-memory kernels (default) or NCCL all-to-all")
+    p.add_argument("--gemm-debug", type=int, default=0, help=argparse.SUPPRESS)  # A/B experiment switches
     return p.parse_args()
 
 
@@ -271,6 +272,7 @@ def run_single(args, dev):
     from paper_2412_09952_b200.upcycle import upcycle_experts, router_weights
 
     T = args.tokens
+    _lib.call("b200moe_gemm_set_debug", args.gemm_debug)
     torch.manual_seed(0)
     # upcycled layer: one random-init dense SwiGLU FFN copied into 8 experts (K12)
     w1 = (torch.randn(H, F, device=dev) * 0.02).to(torch.bfloat16)

@@ -35,7 +35,19 @@
 
 namespace b200moe {
 
-enum GemmMode : int { kFwd1 = 0, kFwd2 = 1, kBwd2 = 2, kBwd1 = 3, kWgrad = 4 };
+enum GemmMode : int { kFwd1 = 0, kFwd2 = 1, kBwd2 = 2, kBwd1 = 3, kWgrad = 4, kWgradW = 5 };
+
+// kWgradW ("wide" WGRAD, CTA pairs only, opt-in -- see b200moe_expert_wgrad
+// for the measurement): each tile is two 256 x 256
+// accumulators that share one operand, so a k-block loads three 16 KB operand
+// pieces per CTA instead of four:
+//   sub 0: dW1 and dW3 tiles at the same (f, h) share the xp columns,
+//   sub 2: two adjacent dW2 tiles (f and f + 256) share the do columns.
+// With K = the expert's rows (1024 at the bench shape) WGRAD is bound by L2 ->
+// SM operand bandwidth, not by the tensor pipe, and this cuts its operand
+// traffic by 25%.  Both accumulators fill all 512 TMEM columns; instead of a
+// double buffer, the MMA issuer starts the next tile on slot 0 as soon as the
+// epilogue has drained it and catches slot 1 up a few k-blocks later.
 
 constexpr int kBK = 64;            // K per pipeline stage (128 B of bf16 = one swizzle row)
 constexpr int kBN = 256;           // accumulator columns per tile
@@ -94,9 +106,11 @@ struct Geo {
     // and FWD2 within noise -- so disabled; kept for the next tile-shape study.
     static constexpr bool kWide = kWideStores && (kCG == 2) && (kMode == kFwd2 || kMode == kBwd1 || kMode == kWgrad);
     static constexpr int kStoreBytes = kWide ? 4096 : 2048;
-    static constexpr int kStages = kTmaEpiLoads ? 4 : (kWide ? 5 : Cfg<kCG>::kStages);
+    static constexpr bool kPairAcc = (kMode == kWgradW);   // two accumulators sharing one operand
+    static constexpr int kStageBytes = kPairAcc ? 3 * 16384 : Cfg<kCG>::kStageBytes;
+    static constexpr int kStages = kPairAcc ? 4 : (kTmaEpiLoads ? 4 : (kWide ? 5 : Cfg<kCG>::kStages));
     static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? 4 * 2048 : 0) + kRing * kStoreBytes;
-    static constexpr int kSmemBytes = kStages * Cfg<kCG>::kStageBytes + kNumEpiWarps * kEpiWarpBytes +
+    static constexpr int kSmemBytes = kStages * kStageBytes + kNumEpiWarps * kEpiWarpBytes +
                                       1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2);
 };
 
@@ -120,7 +134,19 @@ struct Sched {
         while (prefix[s + 1] <= t) ++s;
         int r = t - prefix[s];
         ti.seg = s;
-        if constexpr (kMode == kWgrad) {
+        if constexpr (kMode == kWgradW) {
+            const int tiles_w13 = (a.F / 256) * (a.H / 256);   // (dW1, dW3) pairs
+            if (r < tiles_w13) {
+                ti.sub = 0;
+                ti.m_tile = r / (a.H / 256);
+                ti.n_tile = r % (a.H / 256);
+            } else {                                            // dW2 column pairs
+                ti.sub = 2;
+                r -= tiles_w13;
+                ti.m_tile = r / (a.F / 512);
+                ti.n_tile = r % (a.F / 512);
+            }
+        } else if constexpr (kMode == kWgrad) {
             const int tiles_w13 = (a.F / Cfg<kCG>::kTileM) * (a.H / kBN);
             if (r < 2 * tiles_w13) {
                 ti.sub = r / tiles_w13;
@@ -199,6 +225,26 @@ template <> struct Majors<kFwd2>  { static constexpr bool a = false, b = false; 
 template <> struct Majors<kBwd2>  { static constexpr bool a = false, b = true; };
 template <> struct Majors<kBwd1>  { static constexpr bool a = false, b = true; };
 template <> struct Majors<kWgrad> { static constexpr bool a = true, b = true; };
+template <> struct Majors<kWgradW> { static constexpr bool a = true, b = true; };
+
+// kWgradW k-block (absolute row kb) into the three 16 KB pieces of a stage:
+//   sub 0: s0 = da[:, f], s1 = db[:, f], s2 = xp[:, h]   (MMA0: s0 x s2, MMA1: s1 x s2)
+//   sub 2: s0 = do[:, h], s1 = h[:, f],  s2 = h[:, f+256] (MMA0: s0 x s1, MMA1: s0 x s2)
+__device__ __forceinline__ void produce_wide(const TmaSet& tm, const TileInfo& ti, int kb, uint32_t rank,
+                                             uint64_t* bar, uint8_t* st) {
+    const int m0 = ti.m_tile * 256 + rank * kRowsPerCta;
+    if (ti.sub == 0) {
+        const int n0 = ti.n_tile * 256 + rank * 128;
+        load_operand<true>(&tm.m[2], bar, st, m0, kb, 128, true);
+        load_operand<true>(&tm.m[4], bar, st + 16384, m0, kb, 128, true);
+        load_operand<true>(&tm.m[3], bar, st + 32768, n0, kb, 128, true);
+    } else {
+        const int f0 = ti.n_tile * 512 + rank * 128;
+        load_operand<true>(&tm.m[0], bar, st, m0, kb, 128, true);
+        load_operand<true>(&tm.m[1], bar, st + 16384, f0, kb, 128, true);
+        load_operand<true>(&tm.m[1], bar, st + 32768, f0 + 256, kb, 128, true);
+    }
+}
 
 // Issue the TMA loads of k-block `kb` of tile `ti` into stage buffers.
 template <int kMode, int kCG>
@@ -578,6 +624,148 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
     (void)r1;
 }
 
+// kWgradW epilogue.  Per slot: read the warp's 32 rows x 128 columns from
+// TMEM into registers (as packed bf16), release the slot, then write them out;
+// the MMA issuer, which starts the next tile on slot 0 as soon as it is
+// released, only waits for the TMEM reads, not for the global stores.  Each
+// warp owns TMEM lane quarter q and a 128-column half of each 256-column slot.
+// An expert without rows (k_empty) writes zeros.
+__device__ __forceinline__ void tmem_take64(uint32_t taddr, uint32_t* pk) {
+    uint32_t r0[32], r1[32];
+    ptx::tmem_ld_32x32b_x32(taddr, r0);
+    ptx::tmem_ld_32x32b_x32(taddr + 32, r1);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        pk[i] = pack2(__uint_as_float(r0[2 * i]), __uint_as_float(r0[2 * i + 1]));
+        pk[16 + i] = pack2(__uint_as_float(r1[2 * i]), __uint_as_float(r1[2 * i + 1]));
+    }
+}
+
+// 32 x 32 chunk of packed bf16 (16 words per lane = its row) through the
+// swizzled staging buffer to global memory (same pattern as stage_store_lsu).
+__device__ __forceinline__ void store_packed_lsu(uint8_t* buf, __nv_bfloat16* gdst, size_t ld, const uint32_t* p,
+                                                 int lane, bool stream) {
+    uint4* rowp = reinterpret_cast<uint4*>(buf + lane * 64);
+    const int sw = (lane >> 1) & 3;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) rowp[j ^ sw] = make_uint4(p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+    __syncwarp();
+    const int cj = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = i * 8 + (lane >> 2);
+        const uint4 val = *reinterpret_cast<const uint4*>(buf + r * 64 + ((cj ^ ((r >> 1) & 3)) << 4));
+        if (stream) ptx::st_cs_v4(gdst + (size_t)r * ld + cj * 8, val);
+        else *reinterpret_cast<uint4*>(gdst + (size_t)r * ld + cj * 8) = val;
+    }
+}
+
+__device__ __forceinline__ void epilogue_wide(const GemmArgs& a, const TileInfo& ti, uint32_t tmem_base, int q,
+                                              int half, int lane, uint32_t rank, bool k_empty, uint64_t* tfull,
+                                              uint64_t* tempty, uint32_t tphase, uint8_t* buf) {
+    uint32_t pk[64];
+    const int e = ti.seg;
+    const int orow = ti.m_tile * 256 + rank * kRowsPerCta + q * 32;
+    const uint32_t lane_addr = tmem_base + ((uint32_t)(q * 32) << 16) + half * 128;
+#pragma unroll 1
+    for (int slot = 0; slot < 2; ++slot) {
+        __nv_bfloat16* dst;
+        size_t ld;
+        if (ti.sub == 0) {   // slot 0: dW1, slot 1: dW3 (same rows and columns)
+            dst = (slot == 0 ? a.out0 : a.out2) + (size_t)(e * a.F + orow) * a.H + ti.n_tile * 256 + half * 128;
+            ld = a.H;
+        } else {             // dW2 columns f and f + 256
+            dst = a.out1 + (size_t)(e * a.H + orow) * a.F + ti.n_tile * 512 + slot * 256 + half * 128;
+            ld = a.F;
+        }
+        ptx::mbar_wait(&tfull[slot], tphase);
+        ptx::tc_fence_after();
+        if (!k_empty) {
+            tmem_take64(lane_addr + slot * 256, pk);
+            tmem_take64(lane_addr + slot * 256 + 64, pk + 32);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) pk[i] = 0u;
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(&tempty[slot], 0);
+        if (!(a.debug & 1)) {
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) store_packed_lsu(buf, dst + cc * 32, ld, pk + 16 * cc, lane, a.debug & 128);
+        }
+    }
+}
+
+// kWgradW MMA issuer (one thread of the leader CTA).  Per k-block it issues
+// the slot-0 MMAs, then the slot-1 MMAs.  At the start of a tile slot 1 may
+// still be draining the previous tile, so up to kStages - 1 k-blocks of slot-0
+// MMAs run ahead (their stages stay held) and slot 1 catches up once the
+// epilogue releases it.  tfull[0] is committed after the last slot-0 MMA so the
+// epilogue starts on slot 0 while the last slot-1 MMAs still run.
+template <int kStages, class S>
+__device__ __forceinline__ void mma_wide(const GemmArgs& a, const S& sched, uint8_t* stages, uint64_t* full,
+                                         uint64_t* empty, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
+                                         int cid, int ncl) {
+    constexpr int kSB = 3 * 16384;
+    constexpr int kLag = kStages - 1;
+    constexpr uint32_t idesc = ptx::make_idesc_bf16(256, kBN, true, true);
+    auto issue = [&](uint32_t dtm, uint32_t aaddr, uint32_t baddr, int kb) {
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)
+            ptx::mma_bf16<2>(dtm, ptx::make_sdesc(aaddr + k * 2048, 8192, 1024),
+                             ptx::make_sdesc(baddr + k * 2048, 8192, 1024), idesc, (kb | k) != 0);
+    };
+    int stage = 0;
+    uint32_t phase = 0, tph = 0;
+    for (int t = cid; t < sched.total; t += ncl) {
+        const TileInfo ti = sched.decode(t, a);
+        const int nkb = wgrad_k_blocks(a, ti.seg);
+        const uint32_t a0 = 0, b0 = ti.sub == 0 ? 32768 : 16384;   // MMA0 operands within a stage
+        const uint32_t a1 = ti.sub == 0 ? 16384 : 0, b1 = 32768;   // MMA1 operands
+        ptx::mbar_wait_cluster(&tempty[0], tph ^ 1);
+        ptx::tc_fence_after();
+        bool s1 = false;
+        int pend0 = 0, pkb0 = 0, npend = 0;   // k-blocks whose slot-1 MMAs are still to issue
+        for (int kb = 0; kb < nkb; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t sb = ptx::smem_u32(stages + stage * kSB);
+            issue(tmem_base, sb + a0, sb + b0, kb);
+            if (kb == nkb - 1) ptx::mma_commit<2>(&tfull[0], 0x3);
+            if (npend == 0) { pend0 = stage; pkb0 = kb; }
+            ++npend;
+            if (!s1) {
+                if (npend >= kLag || kb == nkb - 1) {
+                    ptx::mbar_wait_cluster(&tempty[1], tph ^ 1);
+                    s1 = true;
+                } else {
+                    s1 = ptx::mbar_try_wait_cluster(&tempty[1], tph ^ 1);
+                }
+                if (s1) ptx::tc_fence_after();
+            }
+            if (s1) {
+                for (int i = 0; i < npend; ++i) {
+                    const int st = (pend0 + i) % kStages;
+                    const uint32_t pb = ptx::smem_u32(stages + st * kSB);
+                    issue(tmem_base + kBN, pb + a1, pb + b1, pkb0 + i);
+                    ptx::mma_commit<2>(&empty[st], 0x3);
+                }
+                npend = 0;
+            }
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        if (nkb == 0) {   // expert without rows: the epilogue writes zeros
+            ptx::mbar_wait_cluster(&tempty[1], tph ^ 1);
+            ptx::mma_commit<2>(&tfull[0], 0x3);
+        }
+        ptx::mma_commit<2>(&tfull[1], 0x3);
+        tph ^= 1;
+    }
+}
+
 // ------------------------------------------------------------------ kernel
 template <int kMode, int kCG>
 __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_constant__ TmaSet tm, GemmArgs a) {
@@ -586,7 +774,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stages = smem;
-    uint8_t* staging = smem + G::kStages * C::kStageBytes;  // per-epilogue-warp rings
+    uint8_t* staging = smem + G::kStages * G::kStageBytes;  // per-epilogue-warp rings
     uint64_t* full = reinterpret_cast<uint64_t*>(staging + kNumEpiWarps * G::kEpiWarpBytes);
     uint64_t* empty = full + G::kStages;
     uint64_t* tfull = empty + G::kStages;
@@ -605,7 +793,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
     if (threadIdx.x == 0) {
         int acc = 0;
         prefix[0] = 0;
-        if constexpr (kMode == kWgrad) {
+        if constexpr (kMode == kWgradW) {
+            const int per_e = (a.F / 256) * (a.H / 256) + (a.H / 256) * (a.F / 512);
+            for (int e = 0; e < a.E_local; ++e) {
+                acc += per_e;
+                prefix[e + 1] = acc;
+            }
+        } else if constexpr (kMode == kWgrad) {
             const int per_e = 2 * (a.F / C::kTileM) * (a.H / kBN) + (a.H / C::kTileM) * (a.F / kBN);
             for (int e = 0; e < a.E_local; ++e) {
                 acc += per_e;
@@ -643,7 +837,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
     Sched<kMode, kCG> sched;
     sched.prefix = prefix;
     sched.n_tiles = mode_n_tiles<kMode>(a);
-    sched.total = prefix[(kMode == kWgrad) ? a.E_local : a.nseg];
+    constexpr bool kW = (kMode == kWgrad || kMode == kWgradW);
+    sched.total = prefix[kW ? a.E_local : a.nseg];
 
     if (warp == 0) {
         // ================= TMA producer
@@ -652,16 +847,19 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
             uint32_t phase = 0;
             for (int t = cid; t < sched.total; t += ncl) {
                 const TileInfo ti = sched.decode(t, a);
-                if constexpr (kMode == kWgrad) {
+                if constexpr (kW) {
                     for (int s = 0; s < a.nseg; ++s) {
                         if (a.seg_expert[s] != ti.seg) continue;
                         const int nkb = ceil_div(a.seg_count[s], kBK);
                         for (int kb = 0; kb < nkb; ++kb) {
                             ptx::mbar_wait(&empty[stage], phase ^ 1);
-                            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes * kCG);
-                            uint8_t* sA = stages + stage * C::kStageBytes;
-                            produce_kblock<kMode, kCG>(tm, a, ti, a.seg_base[s] + kb * kBK, 0, rank, &full[stage],
-                                                       sA, sA + C::kABytes);
+                            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], G::kStageBytes * kCG);
+                            uint8_t* sA = stages + stage * G::kStageBytes;
+                            if constexpr (kMode == kWgradW)
+                                produce_wide(tm, ti, a.seg_base[s] + kb * kBK, rank, &full[stage], sA);
+                            else
+                                produce_kblock<kMode, kCG>(tm, a, ti, a.seg_base[s] + kb * kBK, 0, rank,
+                                                           &full[stage], sA, sA + C::kABytes);
                             if (++stage == G::kStages) { stage = 0; phase ^= 1; }
                         }
                     }
@@ -669,8 +867,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
                     const int nkb = mode_k_blocks<kMode>(a);
                     for (int kb = 0; kb < nkb; ++kb) {
                         ptx::mbar_wait(&empty[stage], phase ^ 1);
-                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes * kCG);
-                        uint8_t* sA = stages + stage * C::kStageBytes;
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], G::kStageBytes * kCG);
+                        uint8_t* sA = stages + stage * G::kStageBytes;
                         produce_kblock<kMode, kCG>(tm, a, ti, kb, 0, rank, &full[stage], sA, sA + C::kABytes);
                         if (++stage == G::kStages) { stage = 0; phase ^= 1; }
                     }
@@ -679,7 +877,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
         }
     } else if (warp == 1) {
         // ================= MMA issuer (leader CTA of the pair)
-        if (rank == 0) {
+        if constexpr (kMode == kWgradW) {
+            if (rank == 0 && lane == 0)
+                mma_wide<G::kStages>(a, sched, stages, full, empty, tfull, tempty, tmem_base, cid, ncl);
+        } else if (rank == 0) {
             constexpr uint32_t idesc = ptx::make_idesc_bf16(kRowsPerCta * kCG, kBN, Majors<kMode>::a, Majors<kMode>::b);
             int stage = 0;
             uint32_t phase = 0;
@@ -695,7 +896,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint32_t aaddr = ptx::smem_u32(stages + stage * C::kStageBytes);
+                        const uint32_t aaddr = ptx::smem_u32(stages + stage * G::kStageBytes);
                         const uint32_t baddr = aaddr + C::kABytes;
 #pragma unroll
                         for (int k = 0; k < kBK / 16; ++k) {
@@ -724,6 +925,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
         EpiRing ring{staging + (warp - 2) * G::kEpiWarpBytes, 0};
         EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + G::kRing * G::kStoreBytes, ldbar + 2 * (warp - 2), 0,
                     0};
+        if constexpr (kMode == kWgradW) {
+            uint32_t tphase = 0;
+            for (int t = cid; t < sched.total; t += ncl) {
+                const TileInfo ti = sched.decode(t, a);
+                const bool k_empty = wgrad_k_blocks(a, ti.seg) == 0;
+                epilogue_wide(a, ti, tmem_base, q, half, lane, rank, k_empty, tfull, tempty, tphase, ring.base);
+                tphase ^= 1;
+            }
+        } else
         for (int t = cid; t < sched.total; t += ncl) {
             const TileInfo ti = sched.decode(t, a);
             const bool k_empty = (kMode == kWgrad) ? (wgrad_k_blocks(a, ti.seg) == 0) : false;
@@ -959,6 +1169,12 @@ int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const 
     B200_TRY(make_map(&tm.st[2], dw3, H, (uint64_t)E_local * F, H, false, true, wide));
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dw1, (__nv_bfloat16*)dw2, (__nv_bfloat16*)dw3, nullptr, nullptr};
+    // Wide tiles (shared-operand accumulator pairs) are opt-in (GemmArgs.debug
+    // bit 8 = 256, CTA pairs, F % 512 == 0): bit-identical and 25% less operand
+    // traffic, but measured inside the layer step WGRAD takes 2.36-2.41 ms vs
+    // 2.27-2.32 ms with the double-buffered one-accumulator tiles (standalone:
+    // 2.10 ms both; 1.77 vs 1.82 ms without the weight-gradient stores).
+    if (g_cta_group == 2 && F % 512 == 0 && (g_debug & 256)) return launch<kWgradW, 2>(tm, a, stream);
     return dispatch_launch<kWgrad>(tm, a, stream);
 }
 

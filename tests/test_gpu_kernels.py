@@ -125,6 +125,54 @@ def test_grouped_gemm_all_modes(cg, H, F, counts):
     _lib.call("b200moe_gemm_set_cta_group", 2)
 
 
+@pytest.mark.parametrize("H,F,counts,owners", [
+    (256, 1024, [1, 0, 513], [0, 1, 2]),
+    (512, 512, [300, 129, 700, 64], [0, 1, 0, 1]),      # EP layout: two source segments per expert
+    (256, 512, [1024, 1024], [0, 1]),
+])
+def test_wgrad_wide_tiles_match_one_accumulator_tiles(H, F, counts, owners):
+    """The opt-in wide WGRAD tiles (debug bit 256: dW1/dW3 sharing xp, dW2 column pairs sharing do)
+    issue the same MMA sequence into each accumulator as the one-accumulator
+    tiles, so the weight gradients must be bit-identical; both are also checked
+    against an fp32 reference."""
+    dev = torch.device("cuda")
+    _lib.call("b200moe_gemm_set_cta_group", 2)
+    E = max(owners) + 1
+    base, cnt, _, R = _segments(counts, dev)
+    sege = torch.tensor(owners, dtype=torch.int32, device=dev)
+    nseg = len(counts)
+    xp = _fill_rows(R, H, base, cnt, dev, seed=1)
+    Hh = _fill_rows(R, F, base, cnt, dev, seed=2)
+    dO = _fill_rows(R, H, base, cnt, dev, seed=3)
+    dA = _fill_rows(R, F, base, cnt, dev, seed=4)
+    dB = _fill_rows(R, F, base, cnt, dev, seed=5)
+    bf = dict(dtype=torch.bfloat16, device=dev)
+    s = _lib.stream_ptr()
+    outs = []
+    for debug in (0, 256):
+        _lib.call("b200moe_gemm_set_debug", debug)
+        dW1, dW3 = (torch.full((E, F, H), float("nan"), **bf) for _ in range(2))
+        dW2 = torch.full((E, H, F), float("nan"), **bf)
+        _lib.call("b200moe_expert_wgrad", xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(),
+                  dB.data_ptr(), base.data_ptr(), cnt.data_ptr(), sege.data_ptr(), nseg, R, H, F, E,
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
+        torch.cuda.synchronize()
+        outs.append((dW1, dW2, dW3))
+    _lib.call("b200moe_gemm_set_debug", 0)
+    for w, n in zip(range(3), ("dW1", "dW2", "dW3")):
+        assert torch.equal(outs[0][w], outs[1][w]), n
+    dW1, dW2, dW3 = outs[0]
+    for e in range(E):
+        r = torch.cat([_rows(base, cnt, s_) for s_ in range(nseg) if owners[s_] == e])
+        if len(r) == 0:
+            assert bool((dW1[e] == 0).all() and (dW2[e] == 0).all() and (dW3[e] == 0).all()), e
+            continue
+        x = xp[r].float()
+        assert rel(dW1[e].float(), dA[r].float().t() @ x) < 1e-2, ("dW1", e)
+        assert rel(dW3[e].float(), dB[r].float().t() @ x) < 1e-2, ("dW3", e)
+        assert rel(dW2[e].float(), dO[r].float().t() @ Hh[r].float()) < 1e-2, ("dW2", e)
+
+
 # --------------------------------------------------------------------------
 # router: gate arithmetic bit-exact vs the reference goldens
 # --------------------------------------------------------------------------
