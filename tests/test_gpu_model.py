@@ -256,3 +256,58 @@ def test_overlapped_optimizer_equals_serial_step(tiny):
         runs.append({n: m.detach().clone() for n, m in opt.master.items()})
     for name in runs[0]:
         assert torch.equal(runs[0][name], runs[1][name]), name
+
+
+def test_micro_batch_accumulation_with_overlapped_optimizer(tiny):
+    """Gradient accumulation as tools/model_bench.py --micro-batches runs it:
+    the overlapped optimizer is armed only for the last micro-batch's backward,
+    so its updates see the summed gradients -- equal, bit for bit, to two
+    backwards followed by Optimizer.step -- and the summed gradient matches
+    the gradient of the two batches' mean loss computed in one pass."""
+    import paper_2412_09952_b200 as P
+    from paper_2412_09952_b200.train import OverlappedStep, TrainState
+    cfg = json.loads(str(tiny["config"]))
+    tokens = tiny["tokens"]
+    inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
+    half = inputs.shape[0] // 2
+    assert half >= 1
+    mbs = [(inputs[:half], tokens[:half, 1:].reshape(-1)), (inputs[half:], tokens[half:, 1:].reshape(-1))]
+
+    def losses(moe, state, batch):
+        fwd = P.forward_with_stats(moe, batch[0], training=True, compute=state.compute)
+        return P.cross_entropy(fwd.logits, batch[1])
+
+    runs, grads = [], []
+    for overlapped in (False, True):
+        moe = _tiny_moe(cfg)
+        state = TrainState(moe)
+        opt = state.optimizer("adam")
+        ov = OverlappedStep(opt) if overlapped else None
+        for p in opt.params.values():
+            p.grad = None
+        for i, mb in enumerate(mbs):
+            loss = losses(moe, state, mb) / len(mbs)
+            if ov is not None and i == len(mbs) - 1:
+                ov.begin(1e-3)
+            loss.backward()
+        if not overlapped:
+            grads.append({n: p.grad.detach().float().clone() for n, p in opt.params.items() if p.grad is not None})
+            opt.step(1e-3)
+        else:
+            ov.finish()
+        torch.cuda.synchronize()
+        runs.append({n: m.detach().clone() for n, m in opt.master.items()})
+    for name in runs[0]:
+        assert torch.equal(runs[0][name], runs[1][name]), name
+    # the accumulated gradient vs one pass over the whole batch (same mean loss when halves are equal-sized)
+    if inputs.shape[0] == 2 * half:
+        moe = _tiny_moe(cfg)
+        state = TrainState(moe)
+        opt = state.optimizer("adam")
+        for p in opt.params.values():
+            p.grad = None
+        losses(moe, state, (inputs, targets)).backward()
+        for n, p in opt.params.items():
+            if n in grads[0]:
+                g1, g0 = p.grad.detach().float(), grads[0][n]
+                assert float((g1 - g0).norm()) <= 2e-2 * float(g0.norm()) + 1e-6, n

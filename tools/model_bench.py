@@ -2,7 +2,11 @@
 a Llama-3-8B-shape E8T2 model with `--layers` transformer blocks (all MoE),
 one full step = forward + cross-entropy + aux loss + backward + Adam over every
 parameter, on one GPU.  Weights are random-init on the device (synthetic), the
-batch is one sequence of `--seq` random token ids.
+batch is one sequence of `--seq` random token ids.  `--micro-batches M` runs M
+forward+backward passes per optimizer step (gradient accumulation, as the
+paper's global batch does over its micro-batches): gradients accumulate in the
+leaves' dtype, the data-parallel reduction and the overlapped optimizer act in
+the last backward only.
 
 Prints one JSON line: tokens/s, ms/step, model MFU with the reference's
 forward_flops(..., "6P") convention (plan.py:195-215) with the expert term
@@ -60,6 +64,7 @@ def main():
     ap.add_argument("--small", action="store_true", help="tiny shape for a smoke run")
     ap.add_argument("--no-shadows", action="store_true", help="cast fp32 GEMM weights per step instead")
     ap.add_argument("--transport", default="p2p", choices=("p2p", "nccl"))
+    ap.add_argument("--micro-batches", type=int, default=1, help="forward+backward passes per optimizer step")
     ap.add_argument("--serial-opt", action="store_true",
                     help="optimizer after the backward in one launch (default: overlapped with the backward)")
     a = ap.parse_args()
@@ -90,27 +95,37 @@ def main():
     ov = None if a.serial_opt else OverlappedStep(opt, group)
     dp = DataParallelGrads(state.leaves, group) if (world > 1 and ov is None) else None
     rng = np.random.default_rng(rank)
-    tokens = rng.integers(0, cfg.vocab, (a.batch, a.seq + 1))
-    inputs, targets = tokens[:, :-1], tokens[:, 1:].reshape(-1)
-    T = a.batch * a.seq
+    M = a.micro_batches
+    batches = []
+    for _ in range(M):
+        tokens = rng.integers(0, cfg.vocab, (a.batch, a.seq + 1))
+        batches.append((tokens[:, :-1], tokens[:, 1:].reshape(-1)))
+    T = a.batch * a.seq * M   # tokens per optimizer step (this rank)
     aux = 0.01
 
     def step(ev=None):
         if ev is not None:
             ev[0].record()
-        fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute, ep_group=group,
-                                   transport=a.transport)
-        loss = P.cross_entropy(fwd.logits, targets)
-        for g in fwd.gates:
-            loss = loss + (aux / len(fwd.gates)) * P.importance_penalty(g)
-        loss = loss / world
-        if ev is not None:
-            ev[1].record()
         for p in opt.params.values():
             p.grad = None
-        if ov is not None:
-            ov.begin(1e-4)
-        loss.backward()
+        stats = []
+        for mb, (inputs, targets) in enumerate(batches):
+            last = mb == M - 1
+            fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute, ep_group=group,
+                                       transport=a.transport)
+            loss = P.cross_entropy(fwd.logits, targets)
+            for g in fwd.gates:
+                loss = loss + (aux / len(fwd.gates)) * P.importance_penalty(g)
+            loss = loss / (world * M)
+            if ev is not None and mb == 0:
+                ev[1].record()
+            if ov is not None and last:
+                ov.begin(1e-4)
+            if dp is not None:
+                dp.enabled = last
+            loss.backward()
+            stats += fwd.stats
+            del fwd
         if dp is not None:
             dp.wait()
         if ev is not None:
@@ -121,7 +136,7 @@ def main():
             opt.step(1e-4)
         if ev is not None:
             ev[3].record()
-        return loss, fwd.stats
+        return loss, stats
 
     for _ in range(a.warmup):
         loss, stats = step()
@@ -142,7 +157,7 @@ def main():
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
         ms, kept = float(t[0]), int(t[1]) // world
     split = {k: round(float(np.median([e[i].elapsed_time(e[i + 1]) for e in evs])), 3)
-             for i, k in enumerate(("forward", "backward", "optimizer"))}
+             for i, k in enumerate(("forward_mb0", "fwd_bwd_rest", "optimizer"))}
     flops = world * model_flops(cfg, moe.gate, T, kept)
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                         "MEASURED_PEAKS.json")))
@@ -158,7 +173,7 @@ def main():
         "mfu": {"measured_peak": round(flops / (ms * 1e-3) / (world * peaks["bf16_tflops"] * 1e12), 4),
                 "spec_2250": round(flops / (ms * 1e-3) / (world * 2250e12), 4), "flops_per_step": flops,
                 "convention": "6P (plan.py:forward_flops) with kept slots for the expert FFNs"},
-        "loss": float(loss.detach()) * world, "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
+        "loss": float(loss.detach()) * world * M, "micro_batches": M, "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
         "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
                    "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": 8,
