@@ -60,11 +60,14 @@ def parse():
 def cpu_sample(tokens: int, cf: float, router: str, policy: str, reps: int):
     """Oracle (numpy port of moefold) fwd+bwd at the Llama shape on `tokens` tokens."""
     import numpy as np  # noqa: F401
+    from threadpoolctl import threadpool_info, threadpool_limits
     from oracle import moe_oracle as O
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    times = [O.time_fwd_bwd(tokens, H, F, E, K_TOP, cf, router, policy, reps=1) for _ in range(reps)]
-    return times, cores
+    # every host core, also under torchrun (which exports OMP_NUM_THREADS=1)
+    with threadpool_limits(limits=cores, user_api="blas"):
+        used = max([p["num_threads"] for p in threadpool_info() if p["user_api"] == "blas"] or [1])
+        times = [O.time_fwd_bwd(tokens, H, F, E, K_TOP, cf, router, policy, reps=1) for _ in range(reps)]
+    return times, used
 
 
 def cpu_model() -> str:
