@@ -97,6 +97,9 @@ def main():
             ok &= case(rank, world, dev, *args, transport)
         # more experts than E8T2 and a wider fan-out (E/N experts per rank, k=4)
         ok &= case(rank, world, dev, 768, 512, 512, "st", "score", None, True, transport, E=16, k=4)
+        # one expert per rank, as EP8 runs E8T2 (E_local = 1: every segment of the local expert GEMMs
+        # comes from a different source rank)
+        ok &= case(rank, world, dev, 1024, 512, 512, "mixtral", "position", 1.0, False, transport, E=world, k=2)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     dist.destroy_process_group()
