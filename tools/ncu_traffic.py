@@ -41,7 +41,7 @@ def main(rep, out):
         rec = {"kernel": name[:80], "mode": mode}
         for col, key in WANT.items():
             for i, h in enumerate(hdr):
-                if h.endswith(col) and r[i] not in ("", "n/a"):
+                if h.endswith(col) and r[i] not in ("", "n/a", "no data"):
                     rec[key] = float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
                     break
         launches.append(rec)
