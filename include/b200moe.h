@@ -201,7 +201,7 @@ int b200moe_upcycle_copy(const void* w1, const void* w2, const void* w3, int src
 int b200moe_rmsnorm_fwd(const float* x, const void* delta, const float* gain, int T, int H, float eps, float* x_out,
                         void* y, float* rstd, cudaStream_t stream);
 /* dx = rmsnorm'(dy) + dres (dres optional), written as fp32 (dx) and/or bf16
- * (dx_bf16); dgain[H] = sum_t dy*x*rstd.  workspace >= ceil(T/32) * H floats.
+ * (dx_bf16); dgain[H] = sum_t dy*x*rstd.  workspace >= ceil(T/8) * H floats.
  * Replaces moefold/tensor.py:314-319. */
 int b200moe_rmsnorm_bwd(const void* dy, const float* x, const float* rstd, const float* gain, const float* dres, int T,
                         int H, float* dx, void* dx_bf16, float* dgain, float* workspace, cudaStream_t stream);

@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace b200moe {
 
@@ -103,14 +104,35 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_fwd_kernel(const float* _
 // dgain = sum_rows dy * x * r.  Each block owns kBwdRows rows and all columns
 // (NV float4 per thread), so the dgain partial sums stay in registers; a
 // second kernel reduces the per-block partials in fixed order.
-constexpr int kBwdRows = 32;
+constexpr int kBwdRows = 8;
 
+// Two block sums in one pass (same fixed order as block_sum for each).
+__device__ __forceinline__ float2 block_sum2(float a, float b, float* red) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { red[w] = a; red[16 + w] = b; }
+    __syncthreads();
+    float ta = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
+    float tb = (threadIdx.x < (blockDim.x >> 5)) ? red[16 + threadIdx.x] : 0.f;
+    if (w == 0) { ta = warp_sum(ta); tb = warp_sum(tb); }
+    if (threadIdx.x == 0) { red[32] = ta; red[33] = tb; }
+    __syncthreads();
+    return make_float2(red[32], red[33]);
+}
+
+// Rows are taken two at a time with every load of both rows (dy, x and the
+// residual gradient) issued before the row reductions: the kernel is bound by
+// load latency, not bandwidth, at one row per step (measured 0.4 ms vs ~60 us
+// of traffic at T=8192, H=4096 with 32 rows per block, one row at a time).
 template <int NV>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_bwd_kernel(
     const bf16* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ rstd,
     const float* __restrict__ gain, const float* __restrict__ dres, int T, int H, float* __restrict__ dx,
     bf16* __restrict__ dx_bf16, float* __restrict__ dgain_part) {
-    __shared__ float red[33];
+    static_assert(kRowThreads / 32 <= 16, "block_sum2 holds 16 warp partials per value");
+    __shared__ float red[34];
     float4 acc[NV], g[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -118,41 +140,63 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_bwd_kernel(
         const int c = (j * kRowThreads + threadIdx.x) * 4;
         g[j] = c < H ? *reinterpret_cast<const float4*>(gain + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     const int r0 = blockIdx.x * kBwdRows;
     const int r1 = min(T, r0 + kBwdRows);
-    for (int row = r0; row < r1; ++row) {
-        const size_t o = (size_t)row * H;
-        const float r = rstd[row];
-        float4 xv[NV], gg[NV];
-        float dot = 0.f;
+    constexpr int kQ = NV <= 4 ? 2 : 1;   // rows per step (register budget: no spills at NV 8/16)
+    for (int row = r0; row < r1; row += kQ) {
+        const bool two = kQ == 2 && row + 1 < r1;
+        float4 xv[kQ][NV], dv[kQ][NV], rv[kQ][NV];
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const int c = (j * kRowThreads + threadIdx.x) * 4;
-            if (c < H) {
-                const float4 d = ld_bf16x4(dy + o + c);
-                xv[j] = *reinterpret_cast<const float4*>(x + o + c);
-                gg[j] = make_float4(d.x * g[j].x, d.y * g[j].y, d.z * g[j].z, d.w * g[j].w);
-                dot += gg[j].x * xv[j].x + gg[j].y * xv[j].y + gg[j].z * xv[j].z + gg[j].w * xv[j].w;
-                acc[j].x += d.x * xv[j].x * r;
-                acc[j].y += d.y * xv[j].y * r;
-                acc[j].z += d.z * xv[j].z * r;
-                acc[j].w += d.w * xv[j].w * r;
+        for (int q = 0; q < kQ; ++q) {
+            const size_t o = (size_t)(row + q) * H;
+            const bool on = q == 0 || two;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const int c = (j * kRowThreads + threadIdx.x) * 4;
+                const bool in = on && c < H;
+                dv[q][j] = in ? ld_bf16x4(dy + o + c) : z4;
+                xv[q][j] = in ? *reinterpret_cast<const float4*>(x + o + c) : z4;
+                rv[q][j] = (in && dres != nullptr) ? *reinterpret_cast<const float4*>(dres + o + c) : z4;
             }
         }
-        dot = block_sum(dot, red);
-        const float k3 = r * r * r / (float)H * dot;
+        const float ra = rstd[row];
+        const float rb = two ? rstd[row + 1] : 0.f;
+        float dot[2] = {0.f, 0.f};
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const int c = (j * kRowThreads + threadIdx.x) * 4;
-            if (c < H) {
-                float4 v = make_float4(r * gg[j].x - k3 * xv[j].x, r * gg[j].y - k3 * xv[j].y,
-                                       r * gg[j].z - k3 * xv[j].z, r * gg[j].w - k3 * xv[j].w);
-                if (dres != nullptr) {
-                    const float4 d = *reinterpret_cast<const float4*>(dres + o + c);
-                    v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w;
+        for (int q = 0; q < kQ; ++q) {
+            const float r = q == 0 ? ra : rb;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const float4 d = dv[q][j];
+                const float4 xx = xv[q][j];
+                const float4 gg = make_float4(d.x * g[j].x, d.y * g[j].y, d.z * g[j].z, d.w * g[j].w);
+                dot[q] += gg.x * xx.x + gg.y * xx.y + gg.z * xx.z + gg.w * xx.w;
+                acc[j].x += d.x * xx.x * r;
+                acc[j].y += d.y * xx.y * r;
+                acc[j].z += d.z * xx.z * r;
+                acc[j].w += d.w * xx.w * r;
+                dv[q][j] = gg;
+            }
+        }
+        const float2 dots = kQ == 2 ? block_sum2(dot[0], dot[1], red) : make_float2(block_sum(dot[0], red), 0.f);
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            if (q == 1 && !two) break;
+            const float r = q == 0 ? ra : rb;
+            const float k3 = r * r * r / (float)H * (q == 0 ? dots.x : dots.y);
+            const size_t o = (size_t)(row + q) * H;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const int c = (j * kRowThreads + threadIdx.x) * 4;
+                if (c < H) {
+                    const float4 gg = dv[q][j], xx = xv[q][j], d = rv[q][j];
+                    float4 v = make_float4(r * gg.x - k3 * xx.x, r * gg.y - k3 * xx.y, r * gg.z - k3 * xx.z,
+                                           r * gg.w - k3 * xx.w);
+                    if (dres != nullptr) { v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w; }
+                    if (dx != nullptr) *reinterpret_cast<float4*>(dx + o + c) = v;
+                    if (dx_bf16 != nullptr) st_bf16x4(dx_bf16 + o + c, v);
                 }
-                if (dx != nullptr) *reinterpret_cast<float4*>(dx + o + c) = v;
-                if (dx_bf16 != nullptr) st_bf16x4(dx_bf16 + o + c, v);
             }
         }
     }
@@ -163,12 +207,121 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_bwd_kernel(
     }
 }
 
-__global__ void reduce_rows_kernel(const float* __restrict__ part, int nrows, int H, float* __restrict__ out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= H) return;
+// Pipelined variant for the model shapes (H % 8 == 0): one block per SM
+// walks a contiguous run of rows; each row's dy, x and residual gradient
+// arrive in shared memory by three 1-D bulk async copies, kRmsStages rows
+// ahead of the row being reduced, so the loads are not bounded by register
+// space (the register kernel above holds two rows per block in flight and
+// reaches ~1.9 TB/s at T=8192, H=4096).  Same arithmetic as rmsnorm_bwd_kernel
+// per row; dgain partials per block.
+constexpr int kRmsStages = 4;
+constexpr int kRmsSmemMax = 200 * 1024;
+
+template <int NV>
+__global__ void __launch_bounds__(kRowThreads, 1) rmsnorm_bwd_ring_kernel(
+    const bf16* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ rstd,
+    const float* __restrict__ gain, const float* __restrict__ dres, int T, int H, int rows_per_block, int stages,
+    float* __restrict__ dx, bf16* __restrict__ dx_bf16, float* __restrict__ dgain_part) {
+    extern __shared__ __align__(128) uint8_t rsm[];
+    __shared__ float red[34];
+    __shared__ __align__(8) uint64_t bar[kRmsStages];
+    const size_t stage_bytes = (size_t)H * (2 + 4 + (dres != nullptr ? 4 : 0));
+    const int r0 = blockIdx.x * rows_per_block;
+    const int r1 = min(T, r0 + rows_per_block);
+    auto issue = [&](int row, int st) {   // thread 0: the three row copies into stage st
+        uint8_t* b = rsm + st * stage_bytes;
+        const uint32_t bytes = (uint32_t)stage_bytes;
+        ptx::mbar_arrive_expect_tx(&bar[st], bytes);
+        ptx::bulk_load_1d(b, dy + (size_t)row * H, H * 2, &bar[st]);
+        ptx::bulk_load_1d(b + H * 2, x + (size_t)row * H, H * 4, &bar[st]);
+        if (dres != nullptr) ptx::bulk_load_1d(b + H * 6, dres + (size_t)row * H, H * 4, &bar[st]);
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < stages; ++i) ptx::mbar_init(&bar[i], 1);
+        ptx::fence_mbar_init();
+        for (int i = 0; i < stages && r0 + i < r1; ++i) issue(r0 + i, i);
+    }
+    float4 acc[NV], g[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int c = (j * kRowThreads + threadIdx.x) * 4;
+        g[j] = c < H ? *reinterpret_cast<const float4*>(gain + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    int st = 0;
+    uint32_t ph = 0;
+    float r_next = r0 < r1 ? rstd[r0] : 0.f;   // one row ahead: its load latency is not on the row's path
+    for (int row = r0; row < r1; ++row) {
+        const float r = r_next;
+        if (row + 1 < r1) r_next = rstd[row + 1];
+        ptx::mbar_wait(&bar[st], ph);
+        const uint8_t* b = rsm + st * stage_bytes;
+        const bf16* sdy = reinterpret_cast<const bf16*>(b);
+        const float* sx = reinterpret_cast<const float*>(b + H * 2);
+        const float* sr = reinterpret_cast<const float*>(b + H * 6);
+        float4 xv[NV], gv[NV], rv[NV];
+        float dot = 0.f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int c = (j * kRowThreads + threadIdx.x) * 4;
+            if (c < H) {
+                const float4 d = ld_bf16x4(sdy + c);
+                xv[j] = *reinterpret_cast<const float4*>(sx + c);
+                rv[j] = dres != nullptr ? *reinterpret_cast<const float4*>(sr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                gv[j] = make_float4(d.x * g[j].x, d.y * g[j].y, d.z * g[j].z, d.w * g[j].w);
+                dot += gv[j].x * xv[j].x + gv[j].y * xv[j].y + gv[j].z * xv[j].z + gv[j].w * xv[j].w;
+                acc[j].x += d.x * xv[j].x * r;
+                acc[j].y += d.y * xv[j].y * r;
+                acc[j].z += d.z * xv[j].z * r;
+                acc[j].w += d.w * xv[j].w * r;
+            }
+        }
+        dot = block_sum(dot, red);   // its barriers also mean every thread is done with stage st
+        if (threadIdx.x == 0 && row + stages < r1) issue(row + stages, st);
+        const float k3 = r * r * r / (float)H * dot;
+        const size_t o = (size_t)row * H;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int c = (j * kRowThreads + threadIdx.x) * 4;
+            if (c < H) {
+                float4 v = make_float4(r * gv[j].x - k3 * xv[j].x, r * gv[j].y - k3 * xv[j].y,
+                                       r * gv[j].z - k3 * xv[j].z, r * gv[j].w - k3 * xv[j].w);
+                v.x += rv[j].x; v.y += rv[j].y; v.z += rv[j].z; v.w += rv[j].w;
+                if (dx != nullptr) *reinterpret_cast<float4*>(dx + o + c) = v;
+                if (dx_bf16 != nullptr) st_bf16x4(dx_bf16 + o + c, v);
+            }
+        }
+        if (++st == stages) { st = 0; ph ^= 1; }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int c = (j * kRowThreads + threadIdx.x) * 4;
+        if (c < H) *reinterpret_cast<float4*>(dgain_part + (size_t)blockIdx.x * H + c) = acc[j];
+    }
+}
+
+// Column sums of part[nrows, H] in a fixed order: a block owns 32 columns;
+// its 8 row lanes sum rows y, y+8, ... (coalesced 128-byte rows), then lane 0
+// adds the 8 partials in order.
+constexpr int kRedCols = 32, kRedLanes = 8;
+
+__global__ void __launch_bounds__(kRedCols * kRedLanes) reduce_rows_kernel(const float* __restrict__ part, int nrows,
+                                                                           int H, float* __restrict__ out) {
+    __shared__ float sm[kRedLanes][kRedCols];
+    const int cx = threadIdx.x % kRedCols, y = threadIdx.x / kRedCols;
+    const int c = blockIdx.x * kRedCols + cx;
     float s = 0.f;
-    for (int i = 0; i < nrows; ++i) s += part[(size_t)i * H + c];
-    out[c] = s;
+    if (c < H)
+        for (int i = y; i < nrows; i += kRedLanes) s += part[(size_t)i * H + c];
+    sm[y][cx] = s;
+    __syncthreads();
+    if (y == 0 && c < H) {
+        float t = sm[0][cx];
+#pragma unroll
+        for (int k = 1; k < kRedLanes; ++k) t += sm[k][cx];
+        out[c] = t;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -471,8 +624,37 @@ int b200moe_rmsnorm_bwd(const void* dy, const float* x, const float* rstd, const
                         int H, float* dx, void* dx_bf16, float* dgain, float* workspace, cudaStream_t stream) {
     B200_CHECK_ARG(T >= 1 && H >= 4 && H % 4 == 0 && H <= 16 * 1024, B200MOE_ERR_SHAPE,
                    "rmsnorm_bwd: hidden %d must be a multiple of 4 and <= 16384", H);
-    const int nb = ceil_div(T, kBwdRows);
     const int nv = ceil_div(H, kRowThreads * 4);
+    const size_t stage_bytes = (size_t)H * (2 + 4 + (dres != nullptr ? 4 : 0));
+    const int stages = (int)(kRmsSmemMax / stage_bytes) < kRmsStages ? (int)(kRmsSmemMax / stage_bytes) : kRmsStages;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(x) |
+                           reinterpret_cast<uintptr_t>(dres)) & 15) == 0;   // bulk copies need 16-byte addresses
+    // the register kernel's vector accesses: 8-byte bf16 quads, 16-byte fp32 quads
+    B200_CHECK_ARG(((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx_bf16)) & 7) == 0 &&
+                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dres) |
+                         reinterpret_cast<uintptr_t>(dx)) & 15) == 0,
+                   B200MOE_ERR_SHAPE, "rmsnorm_bwd: misaligned buffer (bf16 rows need 8, fp32 rows 16 bytes)");
+    if (H % 8 == 0 && nv <= 4 && stages >= 2 && aligned) {
+        // one wave: rows split evenly over the SMs, at least kBwdRows per block (workspace contract)
+        const int rpb = max(kBwdRows, ceil_div(T, kNumSMs));
+        const int nbr = ceil_div(T, rpb);
+        const size_t smem = stages * stage_bytes;
+#define B200_RMS_RING(NV)                                                                                         \
+    do {                                                                                                          \
+        auto kern = rmsnorm_bwd_ring_kernel<NV>;                                                                  \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRmsSmemMax);                     \
+        kern<<<nbr, kRowThreads, smem, stream>>>((const bf16*)dy, x, rstd, gain, dres, T, H, rpb, stages, dx,     \
+                                                 (bf16*)dx_bf16, workspace);                                      \
+    } while (0)
+        if (nv <= 1) B200_RMS_RING(1);
+        else if (nv <= 2) B200_RMS_RING(2);
+        else B200_RMS_RING(4);
+#undef B200_RMS_RING
+        reduce_rows_kernel<<<ceil_div(H, kRedCols), kRedCols * kRedLanes, 0, stream>>>(workspace, nbr, H, dgain);
+        B200_CHECK_LAUNCH("rmsnorm_bwd");
+        return B200MOE_OK;
+    }
+    const int nb = ceil_div(T, kBwdRows);
 #define B200_RMS_BWD(NV)                                                                                         \
     rmsnorm_bwd_kernel<NV><<<nb, kRowThreads, 0, stream>>>((const bf16*)dy, x, rstd, gain, dres, T, H, dx,       \
                                                            (bf16*)dx_bf16, workspace)
@@ -482,7 +664,7 @@ int b200moe_rmsnorm_bwd(const void* dy, const float* x, const float* rstd, const
     else if (nv <= 8) B200_RMS_BWD(8);
     else B200_RMS_BWD(16);
 #undef B200_RMS_BWD
-    reduce_rows_kernel<<<ceil_div(H, 256), 256, 0, stream>>>(workspace, nb, H, dgain);
+    reduce_rows_kernel<<<ceil_div(H, kRedCols), kRedCols * kRedLanes, 0, stream>>>(workspace, nb, H, dgain);
     B200_CHECK_LAUNCH("rmsnorm_bwd");
     return B200MOE_OK;
 }

@@ -43,7 +43,7 @@ def _rms_bwd(ctx, dy, dres):
     dx = torch.empty(T, H, dtype=torch.float32, device=x.device)
     dx_bf = torch.empty(T, H, dtype=torch.bfloat16, device=x.device) if ctx.want_bf16 else None
     dgain = torch.empty(H, dtype=torch.float32, device=x.device)
-    ws = torch.empty((T + 31) // 32 * H, dtype=torch.float32, device=x.device)
+    ws = torch.empty((T + 7) // 8 * H, dtype=torch.float32, device=x.device)   # include/b200moe.h
     _lib.call("b200moe_rmsnorm_bwd", dy.data_ptr(), x.data_ptr(), rstd.data_ptr(), gain.data_ptr(), _lib.ptr(dres),
               T, H, dx.data_ptr(), _lib.ptr(dx_bf), dgain.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
     return dx, dx_bf, dgain

@@ -311,3 +311,39 @@ def test_micro_batch_accumulation_with_overlapped_optimizer(tiny):
             if n in grads[0]:
                 g1, g0 = p.grad.detach().float(), grads[0][n]
                 assert float((g1 - g0).norm()) <= 2e-2 * float(g0.norm()) + 1e-6, n
+
+
+@pytest.mark.parametrize("T,H,offset", [(2048, 4096, 0), (1000, 4096, 4), (37, 1028, 0), (513, 2048, 0)])
+def test_rmsnorm_bwd_ring_and_register_paths(T, H, offset):
+    """b200moe_rmsnorm_bwd at model-like shapes: the bulk-copy ring kernel
+    (H % 8 == 0, 16-byte aligned rows) and the register kernel (H % 8 != 0,
+    or a dy view only 8-byte aligned: offset 4) both match an fp64 reference of
+    tensor.py:314-319 plus the residual gradient."""
+    from paper_2412_09952_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(T + H)
+    x = torch.randn(T, H, device="cuda", generator=g)
+    gain = 1 + 0.1 * torch.randn(H, device="cuda", generator=g)
+    dres = torch.randn(T, H, device="cuda", generator=g)
+    big = torch.randn(T * H + offset, device="cuda", generator=g).to(torch.bfloat16)
+    dy = big[offset:].view(T, H)
+    rstd = torch.rsqrt((x.double() ** 2).mean(1) + 1e-5).float()
+    dx = torch.empty(T, H, device="cuda")
+    dxb = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+    dgain = torch.empty(H, device="cuda")
+    ws = torch.empty((T + 7) // 8 * H, device="cuda")
+    _lib.call("b200moe_rmsnorm_bwd", dy.data_ptr(), x.data_ptr(), rstd.data_ptr(), gain.data_ptr(), dres.data_ptr(),
+              T, H, dx.data_ptr(), dxb.data_ptr(), dgain.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    xd, r, gd, dyd = x.double(), rstd.double()[:, None], gain.double(), dy.double()
+    gg = dyd * gd
+    dot = (gg * xd).sum(1, keepdim=True)
+    want = r * gg - r ** 3 / H * xd * dot + dres.double()
+    assert float((dx.double() - want).norm() / want.norm()) < 1e-6
+    assert float((dxb.double() - want).norm() / want.norm()) < 4e-3
+    wg = (dyd * xd * r).sum(0)
+    assert float((dgain.double() - wg).norm() / wg.norm()) < 1e-5
+    if offset == 4:   # 2-byte aligned dy: refused, not faulted
+        with pytest.raises(Exception):
+            _lib.call("b200moe_rmsnorm_bwd", big[1:].data_ptr(), x.data_ptr(), rstd.data_ptr(), gain.data_ptr(),
+                      dres.data_ptr(), T, H, dx.data_ptr(), dxb.data_ptr(), dgain.data_ptr(), ws.data_ptr(),
+                      _lib.stream_ptr())
