@@ -393,6 +393,13 @@ __global__ void __launch_bounds__(kRowThreads) embedding_bwd_sorted_kernel(const
 // Backward writes (softmax - onehot) * dloss / T in bf16.  One block per row;
 // two passes over the row (the second hits L2).
 // ---------------------------------------------------------------------------
+// 2^x on the SFU (ex2.approx: ~2 ulp; -inf -> 0, +inf -> +inf; results below 2^-126 flush to 0)
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));   // .ftz: one MUFU.EX2, no denormal fix-up
+    return y;
+}
+
 __device__ __forceinline__ void load8(const bf16* p, float* f) { unpack8(*reinterpret_cast<const uint4*>(p), f); }
 
 __global__ void __launch_bounds__(kRowThreads) ce_fwd_kernel(const bf16* __restrict__ logits,
@@ -403,44 +410,76 @@ __global__ void __launch_bounds__(kRowThreads) ce_fwd_kernel(const bf16* __restr
     const size_t row = blockIdx.x;
     const bf16* xr = logits + row * V;
     const bool vec = (V & 7) == 0;
-    float m = -INFINITY;
-    if (vec) {
-        for (int c = threadIdx.x * 8; c < V; c += kRowThreads * 8) {
-            float f[8];
-            load8(xr + c, f);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) m = fmaxf(m, f[i]);
+    // One pass (the row is read once): each thread keeps a running maximum m
+    // and s = sum of exp(f - m) over its elements except one occurrence of m,
+    // rescaled when the maximum moves.  The block then forms
+    //   z - 1 = sum_t s_t * [m_t == M] + (s_t + 1) e^{m_t - M} * [m_t < M] + (holders - 1)
+    // (holders: threads whose maximum is the row maximum M), which keeps the
+    // max's exact 1.0 apart so confident rows keep their tiny loss:
+    // nll = (M - x_t) + log1p(z - 1).
+    float m = -INFINITY, sacc = 0.f;
+    auto upd = [&](float f) {
+        if (f > m) {
+            sacc = (sacc + 1.f) * expf(m - f);   // the old maximum now counts; first element: 0
+            m = f;
+        } else if (f > -INFINITY || f != f) {   // -inf contributes 0; NaN propagates
+            sacc += expf(f - m);
         }
-    } else {
-        for (int c = threadIdx.x; c < V; c += kRowThreads) m = fmaxf(m, bf2f(xr[c]));
-    }
-    m = block_max(m, red);
-    // z - 1 = sum over every element but one occurrence of the maximum, kept
-    // apart from the max's exact 1.0 so confident rows keep their tiny loss:
-    // nll = (m - x_t) + log1p(z - 1).  Each thread leaves out its own first
-    // maximum; the surplus exclusions (ties across threads) are added back.
-    float z1 = 0.f;
-    bool seen = false;
+    };
     if (vec) {
-        for (int c = threadIdx.x * 8; c < V; c += kRowThreads * 8) {
-            float f[8];
-            load8(xr + c, f);
+        // 8 logits per step: one max-compare for the group, then exp2 (MUFU) of
+        // each (f - m) * log2(e); the group's first maximum is left out when it
+        // becomes the running maximum.  ~5 instructions per logit instead of
+        // ~20 (the kernel was issue-bound at ~0.45 of HBM with expf per element).
+        constexpr float kL2e = 1.4426950408889634f;
+        constexpr int kU = 4;   // 16-byte loads in flight per thread
+        for (int c0 = threadIdx.x * 8; c0 < V; c0 += kU * kRowThreads * 8) {
+          uint4 raw[kU];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (!seen && f[i] == m) seen = true;
-                else z1 += expf(f[i] - m);
+          for (int u = 0; u < kU; ++u) {
+              const int c = c0 + u * kRowThreads * 8;
+              raw[u] = c < V ? *reinterpret_cast<const uint4*>(xr + c) : make_uint4(0xFF80FF80u, 0xFF80FF80u,
+                                                                                     0xFF80FF80u, 0xFF80FF80u);
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            float f[8];
+            unpack8(raw[u], f);   // past the row end: bf16 -inf, contributes nothing
+            float m8 = f[0];
+#pragma unroll
+            for (int i = 1; i < 8; ++i) m8 = fmaxf(m8, f[i]);
+            // NaN logits propagate through ex2 into the sum; fmaxf skips them, so
+            // only an all-NaN group seen before any other logit needs a case
+            if (m8 > m) {
+                const float mb = m8 * kL2e;
+                float t = (m > -INFINITY) ? (sacc + 1.f) * ex2f(fmaf(m, kL2e, -mb)) : sacc;   // 0 or NaN
+                bool skipped = false;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const bool skip = !skipped && f[i] == m8;
+                    skipped |= skip;
+                    t += skip ? 0.f : ex2f(fmaf(f[i], kL2e, -mb));
+                }
+                sacc = t;
+                m = m8;
+            } else if (m > -INFINITY) {
+                const float mb = m * kL2e;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) sacc += ex2f(fmaf(f[i], kL2e, -mb));
+            } else if (m8 != m8) {
+                sacc = m8;
             }
+          }
         }
     } else {
-        for (int c = threadIdx.x; c < V; c += kRowThreads) {
-            const float f = bf2f(xr[c]);
-            if (!seen && f == m) seen = true;
-            else z1 += expf(f - m);
-        }
+        for (int c = threadIdx.x; c < V; c += kRowThreads) upd(bf2f(xr[c]));
     }
-    z1 = block_sum(z1, red);
-    const float holders = block_sum(seen ? 1.f : 0.f, red);
+    const float mrow = block_max(m, red);
+    const bool holder = (m == mrow) && m > -INFINITY;
+    float z1 = block_sum(holder ? sacc : (m > -INFINITY ? (sacc + 1.f) * expf(m - mrow) : 0.f), red);
+    const float holders = block_sum(holder ? 1.f : 0.f, red);
     z1 += holders - 1.f;
+    m = mrow;
     if (threadIdx.x == 0) {
         const int64_t t = targets[row];
         const float lp = log1pf(z1);

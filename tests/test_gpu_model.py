@@ -347,3 +347,38 @@ def test_rmsnorm_bwd_ring_and_register_paths(T, H, offset):
             _lib.call("b200moe_rmsnorm_bwd", big[1:].data_ptr(), x.data_ptr(), rstd.data_ptr(), gain.data_ptr(),
                       dres.data_ptr(), T, H, dx.data_ptr(), dxb.data_ptr(), dgain.data_ptr(), ws.data_ptr(),
                       _lib.stream_ptr())
+
+
+@pytest.mark.parametrize("V", [1024, 1001, 128256])
+def test_cross_entropy_edge_rows(V):
+    """Fused CE forward on edge rows, against fp64 log-softmax of the same bf16
+    logits: a confident row (loss ~1e-30: kept by the exclude-one-max sum), a
+    row with -inf (masked) logits, a row whose maximum is tied, a row whose
+    first logits are NaN (loss NaN, as numpy), random rows."""
+    from paper_2412_09952_b200 import _lib
+    T = 8
+    g = torch.Generator(device="cuda").manual_seed(V)
+    lg = torch.randn(T, V, device="cuda", generator=g) * 3
+    lg[0] = -40.0
+    lg[0, 5] = 40.0                 # confident: target 5
+    lg[1, : V // 2] = float("-inf")
+    lg[2, 7] = lg[2, 900 % V] = 50.0
+    lg[3, :16] = float("nan")
+    lg = lg.to(torch.bfloat16)
+    tg = torch.tensor([5, V - 1, 7, 3, 0, 1, 2, V // 3], device="cuda")
+    nll, lse, loss = (torch.empty(T, device="cuda") for _ in range(3))
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("b200moe_cross_entropy_fwd", lg.data_ptr(), tg.data_ptr(), T, V, nll.data_ptr(), lse.data_ptr(),
+              loss.data_ptr(), err.data_ptr(), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    # fp64 reference with the maximum's exact 1.0 kept apart (as log_softmax does not)
+    xd = lg.double()
+    m, jm = xd.max(1, keepdim=True)
+    e = torch.exp(xd - m)
+    e.scatter_(1, jm, 0.0)
+    ref = (m.squeeze(1) - xd.gather(1, tg[:, None]).squeeze(1)) + torch.log1p(e.sum(1))
+    got = nll.double()
+    assert torch.isnan(got[3]), got[3]
+    keep = [0, 1, 2, 4, 5, 6, 7]
+    assert torch.allclose(got[keep], ref[keep], rtol=1e-5, atol=0), (got[keep], ref[keep])
+    assert float(got[0]) > 0 and abs(float(got[0]) / float(ref[0]) - 1) < 1e-2   # ~exp(-80), not rounded to 0
