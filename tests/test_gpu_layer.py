@@ -31,7 +31,7 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16).float().numpy()
 
 
-def make_params(T, H, F, E, identical, seed=10, wscale=(0.5, 0.1, 0.3)):
+def make_params(T, H, F, E, identical, seed=10, wscale=(0.5, 0.1, 0.3), skew=False):
     g = O.rng(seed, 0)
     wg = (g.standard_normal((H, E)) * wscale[0]).astype(np.float32)
     wn = (g.standard_normal((H, E)) * wscale[1]).astype(np.float32)
@@ -44,12 +44,16 @@ def make_params(T, H, F, E, identical, seed=10, wscale=(0.5, 0.1, 0.3)):
     x = O.rng(seed + 1, 0).standard_normal((T, H)).astype(np.float32)
     dy = O.rng(seed + 2, 0).standard_normal((T, H)).astype(np.float32)
     z = O.rng(seed + 3, 0).standard_normal((T, E)).astype(np.float32)
+    if skew:   # every token prefers experts 0 and 1: x has a positive mean, W_g favours those columns
+        x += 1.0
+        wg[:, 0] += 0.05
+        wg[:, 1] += 0.04
     return wg, wn, w1, w2, w3, x, dy, z
 
 
 def run_and_compare(T, H, F, E, rt, pol, cf, noise, identical=False, lam=0.37, seed=10, wscale=(0.5, 0.1, 0.3),
-                    k=2):
-    wg, wn, w1, w2, w3, x, dy, z = make_params(T, H, F, E, identical, seed, wscale)
+                    k=2, skew=False):
+    wg, wn, w1, w2, w3, x, dy, z = make_params(T, H, F, E, identical, seed, wscale, skew)
     dev = torch.device("cuda")
     W1 = torch.stack([torch.from_numpy(w.T.copy()) for w in w1]).to(dev, torch.bfloat16).requires_grad_()
     W2 = torch.stack([torch.from_numpy(w.T.copy()) for w in w2]).to(dev, torch.bfloat16).requires_grad_()
@@ -154,6 +158,20 @@ def test_identical_experts_mixtral_dropless_equals_dense_ffn():
     dense = B.ffn_forward(torch.from_numpy(x).to(dev), *ckw)
     assert out.stats.dropped == 0
     assert rel(out.output.float().cpu().numpy(), dense.float().cpu().numpy()) < 1e-2
+
+
+@pytest.mark.parametrize("cf,pol", [(None, "position"), (1.0, "position"), (1.0, "score"), (4.0, "position")])
+def test_skewed_routing_hot_experts(cf, pol):
+    """Load imbalance: nearly every token routes to experts 0 and 1, so two
+    segments hold ~T rows each (dropless / CF 4) or overflow heavily (CF 1) and
+    the other experts get few or no rows; routing bit-exact and values within
+    tolerance as for uniform load."""
+    out = run_and_compare(1536, 256, 512, 8, "mixtral", pol, cf, False, lam=0.01, skew=True,
+                          wscale=(0.05, 0.0, 0.05))
+    a = out.stats.assigned
+    assert a[0] + a[1] >= 0.9 * min(a.sum(), 2 * 1536) if cf is None else a[0] > 0
+    if cf == 1.0:
+        assert out.stats.dropped > 1000
 
 
 def test_capacity_drops_contribute_zero_and_determinism():
