@@ -177,6 +177,12 @@ int b200moe_expert_bwd1(const void* da, const void* db, const void* w1, const vo
 int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const void* da, const void* db,
                          const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows, int H,
                          int F, int E_local, void* dw1, void* dw2, void* dw3, cudaStream_t stream);
+/* Same, adding into dw1/dw2/dw3 (bf16, fp32 add, one rounding) when accumulate != 0:
+ * gradient accumulation over micro-batches without a separate add pass. */
+int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, const void* da, const void* db,
+                             const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                             int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate,
+                             cudaStream_t stream);
 int b200moe_gemm_set_cta_group(int cta_group); /* 2 (CTA pairs, default) or 1 */
 int b200moe_gemm_set_max_ctas(int n);          /* persistent grid size (default 148) */
 int b200moe_gemm_set_debug(int flags);         /* diagnostics: bit 0 skips wgrad stores */

@@ -51,6 +51,7 @@ SIGNATURES = {
     "b200moe_expert_bwd2": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P],
     "b200moe_expert_bwd1": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
     "b200moe_expert_wgrad": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
+    "b200moe_expert_wgrad_acc": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "b200moe_gemm_set_cta_group": [_I],
     "b200moe_gemm_set_max_ctas": [_I],
     "b200moe_gemm_set_debug": [_I],
@@ -109,7 +110,8 @@ KERNELS_PER_CALL = {
     "b200moe_router_fwd": 2, "b200moe_gate_from_logits": 1, "b200moe_dispatch": 1, "b200moe_permute": 1,
     "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 3, "b200moe_router_wgrad": 2,
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
-    "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_upcycle_copy": 3,
+    "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_expert_wgrad_acc": 1,
+    "b200moe_upcycle_copy": 3,
     "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 3,
     "b200moe_rmsnorm_fwd": 1, "b200moe_rmsnorm_bwd": 2, "b200moe_embedding_fwd": 1, "b200moe_embedding_bwd": 1,
     "b200moe_embedding_bwd_sorted": 1,

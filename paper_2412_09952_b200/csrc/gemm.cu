@@ -35,7 +35,15 @@
 
 namespace b200moe {
 
-enum GemmMode : int { kFwd1 = 0, kFwd2 = 1, kBwd2 = 2, kBwd1 = 3, kWgrad = 4, kWgradW = 5 };
+enum GemmMode : int { kFwd1 = 0, kFwd2 = 1, kBwd2 = 2, kBwd1 = 3, kWgrad = 4, kWgradW = 5, kWgradAcc = 6 };
+
+// kWgradAcc: WGRAD that adds into the existing bf16 gradients (gradient
+// accumulation over micro-batches).  Same tiles and mainloop as kWgrad; the
+// epilogue streams each 32 x 32 chunk of the old gradient into shared memory by
+// TMA (one chunk ahead, the first before the accumulator wait) and adds it in
+// fp32 before the single rounding to bf16.
+template <int kMode>
+__host__ __device__ constexpr bool is_wgrad1() { return kMode == kWgrad || kMode == kWgradAcc; }
 
 // kWgradW ("wide" WGRAD, CTA pairs only, opt-in -- see b200moe_expert_wgrad
 // for the measurement): each tile is two 256 x 256
@@ -75,6 +83,7 @@ struct GemmArgs {
     const __nv_bfloat16* in0;
     const __nv_bfloat16* in1;
     int debug;  // bit 0: skip wgrad epilogue stores (diagnostics only)
+    int acc;    // WGRAD: add into the existing bf16 gradients instead of overwriting them
 };
 
 template <int kCG>
@@ -107,9 +116,12 @@ struct Geo {
     static constexpr bool kWide = kWideStores && (kCG == 2) && (kMode == kFwd2 || kMode == kBwd1 || kMode == kWgrad);
     static constexpr int kStoreBytes = kWide ? 4096 : 2048;
     static constexpr bool kPairAcc = (kMode == kWgradW);   // two accumulators sharing one operand
+    static constexpr bool kAccLoads = (kMode == kWgradAcc);  // old-gradient TMA load ring (2 x 2 KB per warp)
     static constexpr int kStageBytes = kPairAcc ? 3 * 16384 : Cfg<kCG>::kStageBytes;
-    static constexpr int kStages = kPairAcc ? 4 : (kTmaEpiLoads ? 4 : (kWide ? 5 : Cfg<kCG>::kStages));
-    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? 4 * 2048 : 0) + kRing * kStoreBytes;
+    static constexpr int kStages = kPairAcc ? 4 : (kAccLoads ? (kCG == 2 ? 5 : 3)
+                                                             : (kTmaEpiLoads ? 4 : (kWide ? 5 : Cfg<kCG>::kStages)));
+    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? 4 * 2048 : 0) + (kAccLoads ? 2 * 2048 : 0) +
+                                         kRing * kStoreBytes;
     static constexpr int kSmemBytes = kStages * kStageBytes + kNumEpiWarps * kEpiWarpBytes +
                                       1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2);
 };
@@ -146,7 +158,7 @@ struct Sched {
                 ti.m_tile = r / (a.F / 512);
                 ti.n_tile = r % (a.F / 512);
             }
-        } else if constexpr (kMode == kWgrad) {
+        } else if constexpr (is_wgrad1<kMode>()) {
             const int tiles_w13 = (a.F / Cfg<kCG>::kTileM) * (a.H / kBN);
             if (r < 2 * tiles_w13) {
                 ti.sub = r / tiles_w13;
@@ -226,6 +238,7 @@ template <> struct Majors<kBwd2>  { static constexpr bool a = false, b = true; }
 template <> struct Majors<kBwd1>  { static constexpr bool a = false, b = true; };
 template <> struct Majors<kWgrad> { static constexpr bool a = true, b = true; };
 template <> struct Majors<kWgradW> { static constexpr bool a = true, b = true; };
+template <> struct Majors<kWgradAcc> { static constexpr bool a = true, b = true; };
 
 // kWgradW k-block (absolute row kb) into the three 16 KB pieces of a stage:
 //   sub 0: s0 = da[:, f], s1 = db[:, f], s2 = xp[:, h]   (MMA0: s0 x s2, MMA1: s1 x s2)
@@ -420,6 +433,25 @@ __device__ __forceinline__ void epi_load_take(EpiLoads& ld, int i, int lane, flo
     __syncwarp();  // every lane has read buffer i before it can be refilled
 }
 
+// Single-box variant (kWgradAcc): buffer i of the ring holds one 32 x 32 chunk.
+__device__ __forceinline__ void epi_load1_issue(EpiLoads& ld, const CUtensorMap* m, int col, int row0, int lane) {
+    if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(&ld.bar[ld.idx], kStageBufBytes);
+        ptx::tma_load_2d(m, &ld.bar[ld.idx], ld.base + ld.idx * kStageBufBytes, col, row0);
+    }
+    ld.idx ^= 1;
+}
+
+__device__ __forceinline__ void epi_load1_take(EpiLoads& ld, int i, int lane, float* v) {
+    ptx::mbar_wait(&ld.bar[i], (ld.phases >> i) & 1u);
+    ld.phases ^= 1u << i;
+    const uint4* r = reinterpret_cast<const uint4*>(ld.base + i * kStageBufBytes + lane * 64);
+    const int sw = (lane >> 1) & 3;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) unpack8(r[j ^ sw], v + 8 * j);
+    __syncwarp();  // every lane has read buffer i before it can be refilled
+}
+
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
 
 // One epilogue warp: TMEM lane quarter q (rows q*32..q*32+31 of this CTA's
@@ -438,12 +470,38 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
     uint32_t r0[32], r1[32];
     float v0[32], v1[32], v2[32];
     const uint32_t lane_addr = tmem_acc + ((uint32_t)(q * 32) << 16);
-    if constexpr (kMode == kWgrad) {
+    if constexpr (is_wgrad1<kMode>()) {
         const int e = ti.seg;
         const int orow = ti.m_tile * C::kTileM + rank * kRowsPerCta + q * 32;  // first output row of the warp
         const int smap = ti.sub == 0 ? 0 : (ti.sub == 1 ? 2 : 1);            // dW1, dW3, dW2
         const int grow = (ti.sub == 2 ? e * a.H : e * a.F) + orow;
         const int col0 = ti.n_tile * kBN;
+        if constexpr (kMode == kWgradAcc) {
+            __nv_bfloat16* const obase = ti.sub == 2 ? a.out1 : (ti.sub == 0 ? a.out0 : a.out2);
+            const size_t old_ld = ti.sub == 2 ? a.F : a.H;
+            const CUtensorMap* om = &tm.st[smap];
+            const int c0 = col0 + half * 128;
+            epi_load1_issue(ld, om, c0, grow, lane);   // chunk 0 of the old gradient, before the accumulator wait
+            ptx::mbar_wait(tfull, tphase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int cc = 0; cc < 4; ++cc) {
+                const int cur = ld.idx ^ 1;   // buffer holding chunk cc
+                if (cc + 1 < 4) epi_load1_issue(ld, om, c0 + (cc + 1) * 32, grow, lane);
+                if (!k_empty) ptx::tmem_ld_32x32b_x32(lane_addr + half * 128 + cc * 32, r0);
+                epi_load1_take(ld, cur, lane, v1);
+                if (!k_empty) {
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]) + v1[i];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v0[i] = v1[i];
+                }
+                emit32<kRing, kLsuStores>(ring, om, obase, old_ld, v0, lane, c0 + cc * 32, grow, a.debug);
+            }
+            return;
+        }
         ptx::mbar_wait(tfull, tphase);
         ptx::tc_fence_after();
         if constexpr (Geo<kMode, kCG>::kWide) {
@@ -465,6 +523,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                 if (!(a.debug & 1)) stage_store64<kRing>(ring, &tm.st[smap], w, lane, col0 + c, grow);
             }
         } else {
+            __nv_bfloat16* const obase = ti.sub == 2 ? a.out1 : (ti.sub == 0 ? a.out0 : a.out2);
             for (int c = half * 128; c < half * 128 + 128; c += 32) {
                 if (!k_empty) {
                     ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
@@ -476,7 +535,7 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     for (int i = 0; i < 32; ++i) v0[i] = 0.f;
                 }
                 if (!(a.debug & 1)) {
-                    __nv_bfloat16* base = ti.sub == 2 ? a.out1 : (ti.sub == 0 ? a.out0 : a.out2);
+                    __nv_bfloat16* base = obase;
                     emit32<kRing, kLsuStores>(ring, &tm.st[smap], base, ti.sub == 2 ? a.F : a.H, v0, lane,
                                               col0 + c, grow, a.debug);
                 }
@@ -799,7 +858,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
                 acc += per_e;
                 prefix[e + 1] = acc;
             }
-        } else if constexpr (kMode == kWgrad) {
+        } else if constexpr (is_wgrad1<kMode>()) {
             const int per_e = 2 * (a.F / C::kTileM) * (a.H / kBN) + (a.H / C::kTileM) * (a.F / kBN);
             for (int e = 0; e < a.E_local; ++e) {
                 acc += per_e;
@@ -837,7 +896,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
     Sched<kMode, kCG> sched;
     sched.prefix = prefix;
     sched.n_tiles = mode_n_tiles<kMode>(a);
-    constexpr bool kW = (kMode == kWgrad || kMode == kWgradW);
+    constexpr bool kW = (is_wgrad1<kMode>() || kMode == kWgradW);
     sched.total = prefix[kW ? a.E_local : a.nseg];
 
     if (warp == 0) {
@@ -888,7 +947,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
             uint32_t acc_phase = 0;
             for (int t = cid; t < sched.total; t += ncl) {
                 const TileInfo ti = sched.decode(t, a);
-                const int nkb = (kMode == kWgrad) ? wgrad_k_blocks(a, ti.seg) : mode_k_blocks<kMode>(a);
+                const int nkb = is_wgrad1<kMode>() ? wgrad_k_blocks(a, ti.seg) : mode_k_blocks<kMode>(a);
                 ptx::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t dtm = tmem_base + acc * kBN;
@@ -936,7 +995,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
         } else
         for (int t = cid; t < sched.total; t += ncl) {
             const TileInfo ti = sched.decode(t, a);
-            const bool k_empty = (kMode == kWgrad) ? (wgrad_k_blocks(a, ti.seg) == 0) : false;
+            const bool k_empty = is_wgrad1<kMode>() ? (wgrad_k_blocks(a, ti.seg) == 0) : false;
             epilogue_tile<kMode, kCG>(tm, a, ti, tmem_base + acc * kBN, q, half, lane, rank, k_empty, &tfull[acc],
                                       acc_phase, ring, ld);
             ptx::tc_fence_before();
@@ -1156,6 +1215,14 @@ int b200moe_expert_bwd1(const void* da, const void* db, const void* w1, const vo
 int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const void* da, const void* db,
                          const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows, int H,
                          int F, int E_local, void* dw1, void* dw2, void* dw3, cudaStream_t stream) {
+    return b200moe_expert_wgrad_acc(xp, h, dout, da, db, seg_base, seg_count, seg_expert, nseg, rows, H, F, E_local,
+                                    dw1, dw2, dw3, 0, stream);
+}
+
+int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, const void* da, const void* db,
+                             const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                             int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate,
+                             cudaStream_t stream) {
     B200_TRY(check_common(nseg, H, F, E_local));
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], dout, H, rows, H, true));
@@ -1169,6 +1236,8 @@ int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const 
     B200_TRY(make_map(&tm.st[2], dw3, H, (uint64_t)E_local * F, H, false, true, wide));
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dw1, (__nv_bfloat16*)dw2, (__nv_bfloat16*)dw3, nullptr, nullptr};
+    a.acc = accumulate != 0;
+    if (a.acc) return dispatch_launch<kWgradAcc>(tm, a, stream);
     // Wide tiles (shared-operand accumulator pairs) are opt-in (GemmArgs.debug
     // bit 8 = 256, CTA pairs, F % 512 == 0): bit-identical and 25% less operand
     // traffic, but measured inside the layer step WGRAD takes 2.36-2.41 ms vs

@@ -33,7 +33,8 @@ import torch.distributed as dist
 
 from . import _lib
 from .errors import ConfigError, ShapeError
-from .moe import (GateConfig, RoutingStats, SEG_PAD, _arange_i32, _dispatch_ws, _ep, _noise, expert_capacity)
+from .moe import (GateConfig, RoutingStats, SEG_PAD, _acc_targets, _arange_i32, _dispatch_ws, _ep, _noise,
+                  _wgrad_outputs, expert_capacity)
 
 
 @dataclass
@@ -192,6 +193,7 @@ class _EPFunction(torch.autograd.Function):
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_base,
                              gate_mass=gate_mass, importance=imp, stats=stats, err=err, recv_counts=rcounts)
         ctx.st = st
+        ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.splits = sp
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_base,
                               rcounts, xr, A, B, Hh, Os)
@@ -226,12 +228,12 @@ class _EPFunction(torch.autograd.Function):
         dB = torch.empty(Rs, F, **bf)
         _lib.call("b200moe_expert_bwd2", dOr.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(), rbase.data_ptr(),
                   rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(), dB.data_ptr(), s)
-        dW1 = torch.empty_like(W1)
-        dW2 = torch.empty_like(W2)
-        dW3 = torch.empty_like(W3)
-        _lib.call("b200moe_expert_wgrad", xr.data_ptr(), Hh.data_ptr(), dOr.data_ptr(), dA.data_ptr(), dB.data_ptr(),
-                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dW1.data_ptr(),
-                  dW2.data_ptr(), dW3.data_ptr(), s)
+        dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
+        _lib.call("b200moe_expert_wgrad_acc", xr.data_ptr(), Hh.data_ptr(), dOr.data_ptr(), dA.data_ptr(),
+                  dB.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El,
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), int(acc), s)
+        if acc:
+            dW1 = dW2 = dW3 = None
         dxr = torch.empty(Rs, H, **bf)
         _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
                   rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dxr.data_ptr(), s)
@@ -375,6 +377,7 @@ class _EPPeerFunction(torch.autograd.Function):
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_peer,
                              gate_mass=gate_mass, importance=imp, stats=stats, err=err, recv_counts=rcounts.clone())
         ctx.st = st
+        ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.pb = pb
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer,
                               A, B, Hh)
@@ -410,12 +413,12 @@ class _EPPeerFunction(torch.autograd.Function):
         _lib.call("b200moe_expert_bwd2", pb.do.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
                   rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(),
                   dB.data_ptr(), s)
-        dW1 = torch.empty_like(W1)
-        dW2 = torch.empty_like(W2)
-        dW3 = torch.empty_like(W3)
-        _lib.call("b200moe_expert_wgrad", pb.xr.data_ptr(), Hh.data_ptr(), pb.do.data_ptr(), dA.data_ptr(),
+        dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
+        _lib.call("b200moe_expert_wgrad_acc", pb.xr.data_ptr(), Hh.data_ptr(), pb.do.data_ptr(), dA.data_ptr(),
                   dB.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El,
-                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), int(acc), s)
+        if acc:
+            dW1 = dW2 = dW3 = None
         _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
                   rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, pb.dxp.data_ptr(), s)
         pb.barrier()                            # all input gradients are ready

@@ -405,6 +405,41 @@ class _Ctx:
         self.routing = None
 
 
+# Gradient-accumulation fusion (opt-in, for training over micro-batches): when
+# on and an expert weight leaf already holds a contiguous bf16 .grad, the
+# weight-gradient GEMM adds into it (fp32 add, one rounding) and the Function
+# returns None for that weight, so no separate gradient and no add pass over
+# the ~1.4 G expert parameters per layer exist.  The leaf's post-accumulate
+# hooks still fire (autograd runs AccumulateGrad with an undefined gradient),
+# after the WGRAD launch on the same stream.  Off by default: moe_forward then
+# returns expert gradients to autograd like any other op.
+_FUSE_GRAD_ACC = False
+
+
+def set_expert_grad_accumulation_fusion(on: bool) -> None:
+    global _FUSE_GRAD_ACC
+    _FUSE_GRAD_ACC = bool(on)
+
+
+def _acc_targets(W1, W2, W3):
+    """The expert weight leaves a fused accumulation may add into (or None)."""
+    ws = (W1, W2, W3)
+    if _FUSE_GRAD_ACC and all(w.is_leaf and w.requires_grad for w in ws):
+        return ws
+    return None
+
+
+def _wgrad_outputs(targets, W1, W2, W3):
+    """(dW1, dW2, dW3, accumulate): the leaves' existing gradients when every one
+    can take an in-place add, else fresh buffers."""
+    if targets is not None:
+        gs = [t.grad for t in targets]
+        if all(g is not None and g.dtype == torch.bfloat16 and g.is_contiguous() and g.shape == t.shape
+               for g, t in zip(gs, targets)):
+            return gs[0], gs[1], gs[2], True
+    return torch.empty_like(W1), torch.empty_like(W2), torch.empty_like(W3), False
+
+
 class _MoEFunction(torch.autograd.Function):
     """y, gates = MoE(x; W_g, W_noise, W1, W2, W3) with the whole forward and
     backward in the sm_100a kernels.  Inputs are already padded/cast:
@@ -455,6 +490,7 @@ class _MoEFunction(torch.autograd.Function):
         st.routing = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_base,
                           gate_mass=gate_mass, importance=imp, stats=stats, err=err, capacity=cap, rows=R)
         ctx.st = st
+        ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts,
                               seg_base, xp, A, B, Hh, O)
         return y, gates
@@ -487,12 +523,12 @@ class _MoEFunction(torch.autograd.Function):
         _lib.call("b200moe_expert_bwd2", dO.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
                   seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E, dA.data_ptr(),
                   dB.data_ptr(), s)
-        dW1 = torch.empty_like(W1)
-        dW2 = torch.empty_like(W2)
-        dW3 = torch.empty_like(W3)
-        _lib.call("b200moe_expert_wgrad", xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(), dB.data_ptr(),
-                  seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E, dW1.data_ptr(),
-                  dW2.data_ptr(), dW3.data_ptr(), s)
+        dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
+        _lib.call("b200moe_expert_wgrad_acc", xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(),
+                  dB.data_ptr(), seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E,
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), int(acc), s)
+        if acc:
+            dW1 = dW2 = dW3 = None
         dxp = torch.empty(R, H, **bf)
         _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
                   seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E, dxp.data_ptr(), s)

@@ -173,6 +173,58 @@ def test_wgrad_wide_tiles_match_one_accumulator_tiles(H, F, counts, owners):
         assert rel(dW2[e].float(), dO[r].float().t() @ Hh[r].float()) < 1e-2, ("dW2", e)
 
 
+@pytest.mark.parametrize("cg", [1, 2])
+def test_wgrad_accumulate_into_existing_gradients(cg):
+    """b200moe_expert_wgrad_acc: accumulate=0 is the plain WGRAD (bitwise);
+    accumulate=1 adds the new gradient to the bf16 values already in the
+    outputs (fp32 add, one rounding), empty experts keep their old values."""
+    dev = torch.device("cuda")
+    _lib.call("b200moe_gemm_set_cta_group", cg)
+    H, F, counts = 256, 512, [300, 0, 700]
+    E = len(counts)
+    base, cnt, sege, R = _segments(counts, dev)
+    xp = _fill_rows(R, H, base, cnt, dev, seed=1)
+    Hh = _fill_rows(R, F, base, cnt, dev, seed=2)
+    dO = _fill_rows(R, H, base, cnt, dev, seed=3)
+    dA = _fill_rows(R, F, base, cnt, dev, seed=4)
+    dB = _fill_rows(R, F, base, cnt, dev, seed=5)
+    bf = dict(dtype=torch.bfloat16, device=dev)
+    s = _lib.stream_ptr()
+    g = torch.Generator(device=dev).manual_seed(9)
+    old = [torch.randn(E, F, H, generator=g, device=dev).to(torch.bfloat16),
+           torch.randn(E, H, F, generator=g, device=dev).to(torch.bfloat16),
+           torch.randn(E, F, H, generator=g, device=dev).to(torch.bfloat16)]
+
+    def run(outs, acc):
+        _lib.call("b200moe_expert_wgrad_acc", xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(),
+                  dB.data_ptr(), base.data_ptr(), cnt.data_ptr(), sege.data_ptr(), E, R, H, F, E,
+                  outs[0].data_ptr(), outs[1].data_ptr(), outs[2].data_ptr(), acc, s)
+
+    plain = [torch.full_like(o, float("nan")) for o in old]
+    _lib.call("b200moe_expert_wgrad", xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(), dB.data_ptr(),
+              base.data_ptr(), cnt.data_ptr(), sege.data_ptr(), E, R, H, F, E, plain[0].data_ptr(),
+              plain[1].data_ptr(), plain[2].data_ptr(), s)
+    fresh = [torch.full_like(o, float("nan")) for o in old]
+    run(fresh, 0)
+    acc = [o.clone() for o in old]
+    run(acc, 1)
+    torch.cuda.synchronize()
+    _lib.call("b200moe_gemm_set_cta_group", 2)
+    for i in range(3):
+        assert torch.equal(fresh[i], plain[i]), i
+    for e in range(E):
+        r = _rows(base, cnt, e)
+        if len(r) == 0:
+            for i in range(3):
+                assert torch.equal(acc[i][e], old[i][e]), ("empty expert keeps its gradient", i)
+            continue
+        x = xp[r].float()
+        new = [dA[r].float().t() @ x, dO[r].float().t() @ Hh[r].float(), dB[r].float().t() @ x]
+        for i in range(3):
+            want = old[i][e].float() + new[i]
+            assert rel(acc[i][e].float(), want) < 1e-2, (i, e)
+
+
 # --------------------------------------------------------------------------
 # router: gate arithmetic bit-exact vs the reference goldens
 # --------------------------------------------------------------------------

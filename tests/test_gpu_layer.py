@@ -188,3 +188,38 @@ def test_capacity_drops_contribute_zero_and_determinism():
     kept_any = (a.routing["slot_rank"] >= 0).any(dim=1)
     assert a.stats.dropped > 0
     assert bool((a.output[~kept_any] == 0).all())
+
+
+def test_fused_expert_grad_accumulation_matches_autograd_adds():
+    """set_expert_grad_accumulation_fusion: over three backward passes the
+    expert gradients added inside WGRAD match autograd's accumulation (within
+    bf16 rounding of the running sum), the first pass still hands a fresh
+    gradient to autograd, other gradients are untouched, and the leaves'
+    post-accumulate hooks fire on every pass."""
+    wg, wn, w1, w2, w3, x, dy, z = make_params(512, 256, 512, 8, False, seed=40, wscale=(0.3, 0.0, 0.05))
+    dev = torch.device("cuda")
+    cfg = B.GateConfig(n_experts=8, top_k=2, capacity_factor=1.0)
+    res = {}
+    for fused in (False, True):
+        Ws = [torch.stack([torch.from_numpy(w.T.copy()) for w in ws]).to(dev, torch.bfloat16).requires_grad_()
+              for ws in (w1, w2, w3)]
+        wg_t = torch.from_numpy(wg).to(dev).requires_grad_()
+        layer = B.MoELayer.from_stacked(B.RouterParams(wg_t, torch.from_numpy(wn).to(dev)), *Ws)
+        fired = []
+        hooks = [W.register_post_accumulate_grad_hook(lambda t, i=i: fired.append(i)) for i, W in enumerate(Ws)]
+        B.moe.set_expert_grad_accumulation_fusion(fused)
+        try:
+            for p in range(3):
+                xt = (torch.from_numpy(x).to(dev) * (1 + 0.1 * p)).to(torch.bfloat16).requires_grad_()
+                out = B.moe_forward(xt, layer, cfg)
+                (out.output.float() * torch.from_numpy(dy).to(dev)).sum().backward()
+        finally:
+            B.moe.set_expert_grad_accumulation_fusion(False)
+            for h in hooks:
+                h.remove()
+        torch.cuda.synchronize()
+        assert sorted(fired) == [0, 0, 0, 1, 1, 1, 2, 2, 2]
+        res[fused] = [W.grad.float() for W in Ws] + [wg_t.grad]
+    for a, b in zip(res[False], res[True]):
+        assert rel(b.cpu().numpy(), a.cpu().numpy()) < 5e-3
+    assert torch.equal(res[False][3], res[True][3])   # router gradient path unchanged

@@ -258,7 +258,8 @@ def test_overlapped_optimizer_equals_serial_step(tiny):
         assert torch.equal(runs[0][name], runs[1][name]), name
 
 
-def test_micro_batch_accumulation_with_overlapped_optimizer(tiny):
+@pytest.mark.parametrize("fused", [False, True])
+def test_micro_batch_accumulation_with_overlapped_optimizer(tiny, fused):
     """Gradient accumulation as tools/model_bench.py --micro-batches runs it:
     the overlapped optimizer is armed only for the last micro-batch's backward,
     so its updates see the summed gradients -- equal, bit for bit, to two
@@ -278,6 +279,7 @@ def test_micro_batch_accumulation_with_overlapped_optimizer(tiny):
         return P.cross_entropy(fwd.logits, batch[1])
 
     runs, grads = [], []
+    P.moe.set_expert_grad_accumulation_fusion(fused)   # expert gradients added inside WGRAD
     for overlapped in (False, True):
         moe = _tiny_moe(cfg)
         state = TrainState(moe)
@@ -297,6 +299,7 @@ def test_micro_batch_accumulation_with_overlapped_optimizer(tiny):
             ov.finish()
         torch.cuda.synchronize()
         runs.append({n: m.detach().clone() for n, m in opt.master.items()})
+    P.moe.set_expert_grad_accumulation_fusion(False)
     for name in runs[0]:
         assert torch.equal(runs[0][name], runs[1][name]), name
     # the accumulated gradient vs one pass over the whole batch (same mean loss when halves are equal-sized)

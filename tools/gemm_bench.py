@@ -23,6 +23,7 @@ p.add_argument("--cg", type=int, default=2)
 p.add_argument("--only", default="")
 p.add_argument("--max-ctas", type=int, default=148)
 p.add_argument("--debug", type=int, default=0)
+p.add_argument("--wgrad-acc", action="store_true", help="WGRAD adding into the existing gradients")
 a = p.parse_args()
 _lib.call("b200moe_gemm_set_debug", a.debug)
 
@@ -44,7 +45,7 @@ xp = torch.randn(R, H, **bf)
 dO = torch.randn(R, H, **bf)
 A, B, Hh, dA, dB = (torch.randn(R, F, **bf) for _ in range(5))
 O, dxp = torch.empty(R, H, **bf), torch.empty(R, H, **bf)
-dW1, dW3, dW2 = torch.empty_like(W1), torch.empty_like(W3), torch.empty_like(W2)
+dW1, dW3, dW2 = torch.zeros_like(W1), torch.zeros_like(W3), torch.zeros_like(W2)
 s = _lib.stream_ptr()
 S = E * M
 modes = {
@@ -56,10 +57,10 @@ modes = {
     "bwd2": (2.0 * S * H * F, lambda: _lib.call("b200moe_expert_bwd2", dO.data_ptr(), W2.data_ptr(), A.data_ptr(),
                                                   B.data_ptr(), base.data_ptr(), cnt.data_ptr(), sege.data_ptr(), E, R,
                                                   H, F, E, dA.data_ptr(), dB.data_ptr(), s)),
-    "wgrad": (2.0 * S * 3 * H * F, lambda: _lib.call("b200moe_expert_wgrad", xp.data_ptr(), Hh.data_ptr(),
+    "wgrad": (2.0 * S * 3 * H * F, lambda: _lib.call("b200moe_expert_wgrad_acc", xp.data_ptr(), Hh.data_ptr(),
                                                        dO.data_ptr(), dA.data_ptr(), dB.data_ptr(), base.data_ptr(),
                                                        cnt.data_ptr(), sege.data_ptr(), E, R, H, F, E, dW1.data_ptr(),
-                                                       dW2.data_ptr(), dW3.data_ptr(), s)),
+                                                       dW2.data_ptr(), dW3.data_ptr(), int(a.wgrad_acc), s)),
     "bwd1": (2.0 * S * 2 * F * H, lambda: _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(),
                                                       W1.data_ptr(), W3.data_ptr(), base.data_ptr(), cnt.data_ptr(),
                                                       sege.data_ptr(), E, R, H, F, E, dxp.data_ptr(), s)),

@@ -5,7 +5,8 @@ parameter, on one GPU.  Weights are random-init on the device (synthetic), the
 batch is one sequence of `--seq` random token ids.  `--micro-batches M` runs M
 forward+backward passes per optimizer step (gradient accumulation, as the
 paper's global batch does over its micro-batches): gradients accumulate in the
-leaves' dtype, the data-parallel reduction and the overlapped optimizer act in
+leaves' dtype (expert weights inside the weight-gradient GEMM, fp32 add, unless
+--no-fused-acc), the data-parallel reduction and the overlapped optimizer act in
 the last backward only.
 
 Prints one JSON line: tokens/s, ms/step, model MFU with the reference's
@@ -65,6 +66,8 @@ def main():
     ap.add_argument("--no-shadows", action="store_true", help="cast fp32 GEMM weights per step instead")
     ap.add_argument("--transport", default="p2p", choices=("p2p", "nccl"))
     ap.add_argument("--micro-batches", type=int, default=1, help="forward+backward passes per optimizer step")
+    ap.add_argument("--no-fused-acc", action="store_true",
+                    help="accumulate expert gradients with autograd adds instead of inside the WGRAD GEMM")
     ap.add_argument("--serial-opt", action="store_true",
                     help="optimizer after the backward in one launch (default: overlapped with the backward)")
     a = ap.parse_args()
@@ -96,6 +99,7 @@ def main():
     dp = DataParallelGrads(state.leaves, group) if (world > 1 and ov is None) else None
     rng = np.random.default_rng(rank)
     M = a.micro_batches
+    P.moe.set_expert_grad_accumulation_fusion(M > 1 and not a.no_fused_acc)
     batches = []
     for _ in range(M):
         tokens = rng.integers(0, cfg.vocab, (a.batch, a.seq + 1))
@@ -173,7 +177,8 @@ def main():
         "mfu": {"measured_peak": round(flops / (ms * 1e-3) / (world * peaks["bf16_tflops"] * 1e12), 4),
                 "spec_2250": round(flops / (ms * 1e-3) / (world * 2250e12), 4), "flops_per_step": flops,
                 "convention": "6P (plan.py:forward_flops) with kept slots for the expert FFNs"},
-        "loss": float(loss.detach()) * world * M, "micro_batches": M, "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
+        "loss": float(loss.detach()) * world * M, "micro_batches": M,
+        "expert_grad_accumulation": "fused into WGRAD" if (M > 1 and not a.no_fused_acc) else "autograd", "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
         "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
                    "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": 8,
