@@ -355,9 +355,37 @@ dispatch_kernel(const float* __restrict__ gates, int T, int E, int capacity, int
     const int chunk = kDispThreads * kDispItems;
     const bool dropless = capacity < 0;
 
+    int nslots = 0, kept_total = 0;
+    float imp = 0.f, mass = 0.f;
+    if (T <= chunk && (dropless || policy == B200MOE_POLICY_POSITION)) {
+        // ---- one chunk, position policy: a kept slot's rank is its slot index, so one scan
+        // gives counts, ranks and the capacity cut (same per-thread and block summation
+        // order for importance and gate mass as the general path below)
+        float gv[kDispItems];
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < kDispItems; ++i) {
+            const int t = threadIdx.x * kDispItems + i;
+            gv[i] = (t < T) ? gates[(size_t)t * E + e] : 0.f;
+            imp += (t < T) ? gv[i] : 0.f;
+            c += gv[i] > 0.f;
+        }
+        int sp = block_excl_scan(c, sm_i, &nslots);
+#pragma unroll
+        for (int i = 0; i < kDispItems; ++i) {
+            const int t = threadIdx.x * kDispItems + i;
+            int r = -1;
+            if (gv[i] > 0.f) {
+                if (dropless || sp < capacity) { r = sp; mass += gv[i]; }
+                ++sp;
+            }
+            if (t < T) slot_rank[(size_t)t * E + e] = r;
+        }
+        kept_total = dropless ? nslots : min(nslots, capacity);
+        imp = block_sum_f(imp, sm_f);
+        mass = block_sum_f(mass, sm_f);
+    } else {
     // ---- pass 1: slot count and importance
-    int nslots = 0;
-    float imp = 0.f;
     for (int base = 0; base < T; base += chunk) {
         int c = 0;
         for (int i = 0; i < kDispItems; ++i) {
@@ -412,8 +440,7 @@ dispatch_kernel(const float* __restrict__ gates, int T, int E, int capacity, int
     }
 
     // ---- pass 2: kept flags and ranks in token order
-    int kept_total = 0, ties_seen = 0, slots_seen = 0;
-    float mass = 0.f;
+    int ties_seen = 0, slots_seen = 0;
     for (int base = 0; base < T; base += chunk) {
         float gv[kDispItems];
         int nslot = 0, ntie = 0;
@@ -455,6 +482,7 @@ dispatch_kernel(const float* __restrict__ gates, int T, int E, int capacity, int
         if (select) ties_seen += tot_tie;
     }
     mass = block_sum_f(mass, sm_f);
+    }
 
     if (threadIdx.x == 0) {
         counts[e] = kept_total;

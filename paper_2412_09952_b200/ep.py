@@ -34,7 +34,7 @@ import torch.distributed as dist
 from . import _lib
 from .errors import ConfigError, ShapeError
 from .moe import (GateConfig, RoutingStats, SEG_PAD, _acc_targets, _arange_i32, _dispatch_ws, _ep, _noise,
-                  _wgrad_outputs, expert_capacity)
+                  _wgrad_call, _wgrad_outputs, expert_capacity)
 
 
 @dataclass
@@ -229,9 +229,9 @@ class _EPFunction(torch.autograd.Function):
         _lib.call("b200moe_expert_bwd2", dOr.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(), rbase.data_ptr(),
                   rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(), dB.data_ptr(), s)
         dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
-        _lib.call("b200moe_expert_wgrad_acc", xr.data_ptr(), Hh.data_ptr(), dOr.data_ptr(), dA.data_ptr(),
+        _wgrad_call(acc, xr.data_ptr(), Hh.data_ptr(), dOr.data_ptr(), dA.data_ptr(),
                   dB.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El,
-                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), int(acc), s)
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
         if acc:
             dW1 = dW2 = dW3 = None
         dxr = torch.empty(Rs, H, **bf)
@@ -414,9 +414,9 @@ class _EPPeerFunction(torch.autograd.Function):
                   rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(),
                   dB.data_ptr(), s)
         dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
-        _lib.call("b200moe_expert_wgrad_acc", pb.xr.data_ptr(), Hh.data_ptr(), pb.do.data_ptr(), dA.data_ptr(),
+        _wgrad_call(acc, pb.xr.data_ptr(), Hh.data_ptr(), pb.do.data_ptr(), dA.data_ptr(),
                   dB.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El,
-                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), int(acc), s)
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
         if acc:
             dW1 = dW2 = dW3 = None
         _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),

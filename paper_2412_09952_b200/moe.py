@@ -429,6 +429,14 @@ def _acc_targets(W1, W2, W3):
     return None
 
 
+def _wgrad_call(acc: bool, *args) -> None:
+    """The weight-gradient GEMM: plain, or adding into the outputs (acc)."""
+    if acc:
+        _lib.call("b200moe_expert_wgrad_acc", *args[:-1], 1, args[-1])
+    else:
+        _lib.call("b200moe_expert_wgrad", *args)
+
+
 def _wgrad_outputs(targets, W1, W2, W3):
     """(dW1, dW2, dW3, accumulate): the leaves' existing gradients when every one
     can take an in-place add, else fresh buffers."""
@@ -524,9 +532,9 @@ class _MoEFunction(torch.autograd.Function):
                   seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E, dA.data_ptr(),
                   dB.data_ptr(), s)
         dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
-        _lib.call("b200moe_expert_wgrad_acc", xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(),
+        _wgrad_call(acc, xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(),
                   dB.data_ptr(), seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E,
-                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), int(acc), s)
+                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
         if acc:
             dW1 = dW2 = dW3 = None
         dxp = torch.empty(R, H, **bf)
