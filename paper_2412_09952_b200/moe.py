@@ -412,7 +412,9 @@ class _Ctx:
 # the ~1.4 G expert parameters per layer exist.  The leaf's post-accumulate
 # hooks still fire (autograd runs AccumulateGrad with an undefined gradient),
 # after the WGRAD launch on the same stream.  Off by default: moe_forward then
-# returns expert gradients to autograd like any other op.
+# returns expert gradients to autograd like any other op.  Only for
+# .backward()-style accumulation: torch.autograd.grad(...) w.r.t. the expert
+# weights would see no gradient while it is on.
 _FUSE_GRAD_ACC = False
 
 
