@@ -324,7 +324,7 @@ struct EpiRing {
 
 template <int kRing>
 __device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m, const float* v, int lane, int col,
-                                            int row0) {
+                                            int row0, bool evict_first = false) {
     uint8_t* buf = ring.base + ring.idx * kStageBufBytes;
     if (lane == 0) ptx::bulk_wait_read<kRing - 1>();  // the store that last used this buffer has read it
     __syncwarp();
@@ -335,7 +335,8 @@ __device__ __forceinline__ void stage_store(EpiRing& ring, const CUtensorMap* m,
     ptx::fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-        ptx::tma_store_2d(m, buf, col, row0);
+        if (evict_first) ptx::tma_store_2d_hint(m, buf, col, row0, ptx::policy_evict_first());
+        else ptx::tma_store_2d(m, buf, col, row0);
         ptx::bulk_commit();
     }
     ring.idx = (ring.idx + 1 == kRing) ? 0 : ring.idx + 1;
@@ -368,12 +369,19 @@ __device__ __forceinline__ void stage_store_lsu(uint8_t* buf, __nv_bfloat16* gds
 // slower for BWD1 (+6%) and neutral for FWD1/BWD2, so only WGRAD uses it
 // (kLsuStores); debug bits 4 / 8 force TMA / LSU for experiments.
 // GemmArgs.debug bit 2 (4) forces TMA stores, bit 3 (8) forces LSU stores.
+// Streaming (evict-first) stores for outputs nobody reads soon: WGRAD's weight
+// gradients always (bit 10 = 1024 turns it off for A/B runs; layer step, 5
+// interleaved runs of 40 steps each: 6.968 vs 7.017 ms mean), other LSU stores
+// with bit 7 (128); `evict_first` asks the same of TMA stores (FWD1's a/b with
+// bit 11 = 2048: 6.975 ms, no gain).
 template <int kRing, bool kLsuDefault = false>
 __device__ __forceinline__ void emit32(EpiRing& ring, const CUtensorMap* m, __nv_bfloat16* gbase, size_t ld,
-                                       const float* v, int lane, int col, int row0, int debug) {
+                                       const float* v, int lane, int col, int row0, int debug,
+                                       bool evict_first = false) {
     const bool lsu = (debug & 4) ? false : ((debug & 8) ? true : kLsuDefault);
-    if (lsu) stage_store_lsu(ring.base, gbase + (size_t)row0 * ld + col, ld, v, lane, debug & 128);
-    else stage_store<kRing>(ring, m, v, lane, col, row0);
+    const bool stream = kLsuDefault ? !(debug & 1024) : ((debug & 128) || evict_first);
+    if (lsu) stage_store_lsu(ring.base, gbase + (size_t)row0 * ld + col, ld, v, lane, stream);
+    else stage_store<kRing>(ring, m, v, lane, col, row0, evict_first);
 }
 
 // 32 rows x 64 columns (128-byte rows, SWIZZLE_128B: chunk j of row r at j ^ (r & 7)).
@@ -650,8 +658,10 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     v1[i] = bv;
                     v2[i] = av * sigmoidf_(av) * bv;
                 }
-                emit32<kRing>(ring, &tm.st[0], a.out0, a.F, v0, lane, col0 + c, row0, a.debug);
-                emit32<kRing>(ring, &tm.st[1], a.out1, a.F, v1, lane, col0 + c, row0, a.debug);
+                // a, b are read again only by BWD2 (after FWD2, combine and the loss); h by FWD2 next
+                const bool ef = a.debug & 2048;
+                emit32<kRing>(ring, &tm.st[0], a.out0, a.F, v0, lane, col0 + c, row0, a.debug, ef);
+                emit32<kRing>(ring, &tm.st[1], a.out1, a.F, v1, lane, col0 + c, row0, a.debug, ef);
                 emit32<kRing>(ring, &tm.st[2], a.out2, a.F, v2, lane, col0 + c, row0, a.debug);
             }
         } else if constexpr (Geo<kMode, kCG>::kWide) {  // kFwd2 / kBwd1, 64-column stores
@@ -753,7 +763,7 @@ __device__ __forceinline__ void epilogue_wide(const GemmArgs& a, const TileInfo&
         if (lane == 0) ptx::mbar_arrive_cluster(&tempty[slot], 0);
         if (!(a.debug & 1)) {
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) store_packed_lsu(buf, dst + cc * 32, ld, pk + 16 * cc, lane, a.debug & 128);
+            for (int cc = 0; cc < 4; ++cc) store_packed_lsu(buf, dst + cc * 32, ld, pk + 16 * cc, lane, !(a.debug & 1024));
         }
     }
 }
