@@ -328,7 +328,7 @@ def test_dispatch_prefix_rule_and_score_ties():
     assert B.dispatch(torch.from_numpy(gates).cuda(), 2, "score").kept[:, 0].cpu().tolist() == [True, False, True]
 
 
-@pytest.mark.parametrize("T", [1, 5, 9000, 20000])
+@pytest.mark.parametrize("T", [1, 5, 8192, 8193, 20000])   # one-chunk single-scan path up to 8192
 @pytest.mark.parametrize("pol", ["position", "score"])
 def test_dispatch_random_sizes(T, pol):
     rng = np.random.default_rng(T)
