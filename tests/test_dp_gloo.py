@@ -78,3 +78,50 @@ def test_data_parallel_grads_sum_replicated_only(world):
         assert g["layers.0.moe.router.wnoise"] is None
         torch.testing.assert_close(g["layers.0.moe.experts.W1"], torch.full((2, 4, 6), float(r + 1)))
         torch.testing.assert_close(g["embedding"], torch.full((7, 6), float(r + 1)))
+
+
+def _worker_mb(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2412_09952_b200.train import DataParallelGrads
+        torch.manual_seed(0)
+        w = torch.randn(4, 3, requires_grad=True)
+        dp = DataParallelGrads({"lm_head": w})
+        for mb in range(3):                      # three micro-batches, reduction armed for the last only
+            dp.enabled = mb == 2
+            x = torch.full((2, 4), float(rank + 1 + 10 * mb))
+            (x @ w).pow(2).sum().backward()
+        dp.wait()
+        dp.remove()
+        q.put((rank, w.grad.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_data_parallel_grads_micro_batches_reduce_once():
+    """Gradient accumulation (tools/model_bench.py --micro-batches): with the
+    reduction disarmed for all but the last backward, each rank's summed
+    micro-batch gradients are all-reduced exactly once."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_mb, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    torch.manual_seed(0)
+    w0 = torch.randn(4, 3)
+    want = torch.zeros(4, 3)
+    for r in range(world):
+        for mb in range(3):
+            w = w0.clone().requires_grad_(True)
+            (torch.full((2, 4), float(r + 1 + 10 * mb)) @ w).pow(2).sum().backward()
+            want += w.grad
+    for r in range(world):
+        torch.testing.assert_close(torch.from_numpy(res[r]), want, rtol=1e-5, atol=1e-4)
