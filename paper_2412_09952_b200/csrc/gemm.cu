@@ -83,7 +83,6 @@ struct GemmArgs {
     const __nv_bfloat16* in0;
     const __nv_bfloat16* in1;
     int debug;  // bit 0: skip wgrad epilogue stores (diagnostics only)
-    int acc;    // WGRAD: add into the existing bf16 gradients instead of overwriting them
 };
 
 template <int kCG>
@@ -1246,8 +1245,7 @@ int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, co
     B200_TRY(make_map(&tm.st[2], dw3, H, (uint64_t)E_local * F, H, false, true, wide));
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dw1, (__nv_bfloat16*)dw2, (__nv_bfloat16*)dw3, nullptr, nullptr};
-    a.acc = accumulate != 0;
-    if (a.acc) return dispatch_launch<kWgradAcc>(tm, a, stream);
+    if (accumulate) return dispatch_launch<kWgradAcc>(tm, a, stream);   // adds into the existing gradients
     // Wide tiles (shared-operand accumulator pairs) are opt-in (GemmArgs.debug
     // bit 8 = 256, CTA pairs, F % 512 == 0): bit-identical and 25% less operand
     // traffic, but measured inside the layer step WGRAD takes 2.36-2.41 ms vs
