@@ -507,6 +507,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
 
     H, F, E, K = B.H, B.F, B.E, B.K_TOP
     T = args.tokens
+    _lib.call("b200moe_gemm_set_debug", getattr(args, "gemm_debug", 0))
     if E % world:
         raise ConfigError(f"{E} experts cannot be split over {world} ranks")
     torch.manual_seed(0)  # same dense FFN on every rank (upcycling is rank-local copying)
