@@ -84,6 +84,17 @@ __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
                  : "memory");
 }
 
+// Two fp32 FMAs in one FFMA2 (sm_100 packed fp32 pipe): acc.{x,y} = fma(a.{x,y}, b.{x,y}, acc.{x,y}),
+// each rounded exactly like fmaf (no FTZ), so results are bit-identical to two scalar fmaf.
+__device__ __forceinline__ void ffma2(float2& acc, float2 a, float2 b) {
+    unsigned long long r, x, y;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(acc.x), "f"(acc.y));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(x), "l"(y));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(r));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

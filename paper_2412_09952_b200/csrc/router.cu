@@ -212,22 +212,24 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict_
                 for (int e4 = 0; e4 < EP / 4; ++e4) {
                     const float4 w = W[(j * (EP / 4) + e4) * HB + hb];
 #pragma unroll
-                    for (int tt = 0; tt < TT; ++tt) {
+                    for (int tt = 0; tt < TT; ++tt) {   // two FFMA2 per (token, 4 experts): same fmaf order
                         float* a = acc + tt * EP + e4 * 4;
-                        a[0] = fmaf(xv[tt][j], w.x, a[0]);
-                        a[1] = fmaf(xv[tt][j], w.y, a[1]);
-                        a[2] = fmaf(xv[tt][j], w.z, a[2]);
-                        a[3] = fmaf(xv[tt][j], w.w, a[3]);
+                        const float2 xx = make_float2(xv[tt][j], xv[tt][j]);
+                        float2 lo = make_float2(a[0], a[1]), hi = make_float2(a[2], a[3]);
+                        ffma2(lo, xx, make_float2(w.x, w.y));
+                        ffma2(hi, xx, make_float2(w.z, w.w));
+                        a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
                     }
                     if constexpr (kNoise) {
                         const float4 wn = __ldg(&wnsw[(j * (EP / 4) + e4) * HB + hb]);
 #pragma unroll
                         for (int tt = 0; tt < TT; ++tt) {
                             float* a = accn + tt * EP + e4 * 4;
-                            a[0] = fmaf(xv[tt][j], wn.x, a[0]);
-                            a[1] = fmaf(xv[tt][j], wn.y, a[1]);
-                            a[2] = fmaf(xv[tt][j], wn.z, a[2]);
-                            a[3] = fmaf(xv[tt][j], wn.w, a[3]);
+                            const float2 xx = make_float2(xv[tt][j], xv[tt][j]);
+                            float2 lo = make_float2(a[0], a[1]), hi = make_float2(a[2], a[3]);
+                            ffma2(lo, xx, make_float2(wn.x, wn.y));
+                            ffma2(hi, xx, make_float2(wn.z, wn.w));
+                            a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
                         }
                     }
                 }

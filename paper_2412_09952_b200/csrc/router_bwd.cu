@@ -186,15 +186,30 @@ router_dx_kernel(const __nv_bfloat16* __restrict__ dxp_local, const uint64_t* __
 #pragma unroll
             for (int e4 = 0; e4 < EP / 4; ++e4) {
                 const float4 w = __ldg(&wsw[(jh * (EP / 4) + e4) * HB + hb]);
+                if constexpr (TT % 2 == 0) {   // token pairs in one FFMA2 each, same fmaf order per token
 #pragma unroll
-                for (int tt = 0; tt < TT; ++tt) {
-                    const float* d = dhall + tt * EP + e4 * 4;
-                    float a = acc[tt][jh];
-                    a = fmaf(d[0], w.x, a);
-                    a = fmaf(d[1], w.y, a);
-                    a = fmaf(d[2], w.z, a);
-                    a = fmaf(d[3], w.w, a);
-                    acc[tt][jh] = a;
+                    for (int tt = 0; tt < TT; tt += 2) {
+                        const float* d0 = dhall + tt * EP + e4 * 4;
+                        const float* d1 = d0 + EP;
+                        float2 a2 = make_float2(acc[tt][jh], acc[tt + 1][jh]);
+                        ffma2(a2, make_float2(d0[0], d1[0]), make_float2(w.x, w.x));
+                        ffma2(a2, make_float2(d0[1], d1[1]), make_float2(w.y, w.y));
+                        ffma2(a2, make_float2(d0[2], d1[2]), make_float2(w.z, w.z));
+                        ffma2(a2, make_float2(d0[3], d1[3]), make_float2(w.w, w.w));
+                        acc[tt][jh] = a2.x;
+                        acc[tt + 1][jh] = a2.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int tt = 0; tt < TT; ++tt) {
+                        const float* d = dhall + tt * EP + e4 * 4;
+                        float a = acc[tt][jh];
+                        a = fmaf(d[0], w.x, a);
+                        a = fmaf(d[1], w.y, a);
+                        a = fmaf(d[2], w.z, a);
+                        a = fmaf(d[3], w.w, a);
+                        acc[tt][jh] = a;
+                    }
                 }
                 if constexpr (kNoise) {
                     const float4 wn = __ldg(&wnsw[(jh * (EP / 4) + e4) * HB + hb]);
@@ -363,7 +378,12 @@ router_wgrad_ring(const __grid_constant__ CUtensorMap xmap, const float* __restr
                     for (int e = 0; e < EP; ++e) {
                         const float dv = dr[e];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) acc[j][e] = fmaf(xv[j], dv, acc[j][e]);
+                        for (int j = 0; j < 8; j += 2) {   // (acc[j][e], acc[j+1][e]) in one FFMA2
+                            float2 a2 = make_float2(acc[j][e], acc[j + 1][e]);
+                            ffma2(a2, make_float2(xv[j], xv[j + 1]), make_float2(dv, dv));
+                            acc[j][e] = a2.x;
+                            acc[j + 1][e] = a2.y;
+                        }
                     }
                 }
             }
