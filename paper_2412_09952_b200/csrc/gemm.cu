@@ -104,6 +104,13 @@ struct Geo {
 #define B200_BWD2_TMA_EPI 1
 #endif
     static constexpr bool kTmaEpiLoads = B200_BWD2_TMA_EPI && (kMode == kBwd2) && (kCG == 2);
+    // BWD2's a/b load ring: one (a, b) buffer pair per epilogue warp, refilled right after the
+    // chunk is taken (the epilogue has slack: it waits on the accumulator a third of the time),
+    // which frees shared memory for a 5th operand stage.
+#ifndef B200_BWD2_LOAD_BUFS
+#define B200_BWD2_LOAD_BUFS 1
+#endif
+    static constexpr int kEpiLoadBufs = B200_BWD2_LOAD_BUFS;
     // Store-ring depth per epilogue warp (4 buffers + 5 stages measured no
     // better than 2 + 6 for WGRAD on B200).
     static constexpr int kRing = 2;
@@ -118,8 +125,9 @@ struct Geo {
     static constexpr bool kAccLoads = (kMode == kWgradAcc);  // old-gradient TMA load ring (2 x 2 KB per warp)
     static constexpr int kStageBytes = kPairAcc ? 3 * 16384 : Cfg<kCG>::kStageBytes;
     static constexpr int kStages = kPairAcc ? 4 : (kAccLoads ? (kCG == 2 ? 5 : 3)
-                                                             : (kTmaEpiLoads ? 4 : (kWide ? 5 : Cfg<kCG>::kStages)));
-    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? 4 * 2048 : 0) + (kAccLoads ? 2 * 2048 : 0) +
+                                                             : (kTmaEpiLoads ? (kEpiLoadBufs == 1 ? 5 : 4)
+                                                                             : (kWide ? 5 : Cfg<kCG>::kStages)));
+    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? kEpiLoadBufs * 2 * 2048 : 0) + (kAccLoads ? 2 * 2048 : 0) +
                                          kRing * kStoreBytes;
     static constexpr int kSmemBytes = kStages * kStageBytes + kNumEpiWarps * kEpiWarpBytes +
                                       1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2);
@@ -562,18 +570,27 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
             // experiment switches: debug & 32 skips the a/b loads, & 64 the stores
             const bool no_ld = a.debug & 32, no_st = a.debug & 64;
             const int col0 = ti.n_tile * kBN + half * 128;
-            if (live && !no_ld) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0, row0, lane);
+            if (live && !no_ld) {
+                if (Geo<kMode, kCG>::kEpiLoadBufs == 1) ld.idx = 0;
+                epi_load_issue(ld, &tm.m[2], &tm.m[3], col0, row0, lane);
+            }
             ptx::mbar_wait(tfull, tphase);
             ptx::tc_fence_after();
             if (!live) return;
+            constexpr bool kOneBuf = Geo<kMode, kCG>::kEpiLoadBufs == 1;
 #pragma unroll 1
             for (int cc = 0; cc < 4; ++cc) {
                 const int c = cc * 32;
-                const int cur = ld.idx ^ 1;  // buffer holding chunk cc
-                if (cc + 1 < 4 && !no_ld) epi_load_issue(ld, &tm.m[2], &tm.m[3], col0 + c + 32, row0, lane);
+                const int cur = kOneBuf ? 0 : (ld.idx ^ 1);  // buffer holding chunk cc
+                if (!kOneBuf && cc + 1 < 4 && !no_ld)
+                    epi_load_issue(ld, &tm.m[2], &tm.m[3], col0 + c + 32, row0, lane);
                 ptx::tmem_ld_32x32b_x32(lane_addr + half * 128 + c, r0);
                 if (!no_ld) {
                     epi_load_take(ld, cur, lane, v0, v1);
+                    if (kOneBuf && cc + 1 < 4) {   // refill the (now read) buffer with the next chunk
+                        ld.idx = 0;
+                        epi_load_issue(ld, &tm.m[2], &tm.m[3], col0 + c + 32, row0, lane);
+                    }
                 } else {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) { v0[i] = 0.5f; v1[i] = 0.25f; }
