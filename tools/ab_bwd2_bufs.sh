@@ -1,10 +1,10 @@
 #!/bin/bash
-# A/B of BWD2 load-buffer count: A = 1 buffer + 5 stages (default now), B = 2 buffers + 4 stages
+# A/B of a BWD2 variant: A = the built library, B = gemm.cu rebuilt with $AB_FLAGS (e.g. -DB200_BWD2_LOAD_BUFS=2 -DB200_BWD2_CHUNK16=0)
 cd ${GRAFT_REPO_ROOT:-.}
 L=paper_2412_09952_b200/lib
 cp $L/libb200moe.so $L/libb200moe_a.so
 cd paper_2412_09952_b200/csrc
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -ftz=false -prec-div=true -prec-sqrt=true -DB200_BWD2_LOAD_BUFS=2 -c gemm.cu -o /tmp/gemm_b.o
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -ftz=false -prec-div=true -prec-sqrt=true $AB_FLAGS -c gemm.cu -o /tmp/gemm_b.o
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../lib/libb200moe_b.so ../lib/obj/capi.o ../lib/obj/router.o ../lib/obj/permute.o ../lib/obj/router_bwd.o /tmp/gemm_b.o ../lib/obj/upcycle.o ../lib/obj/model.o ../lib/obj/crc32c.o
 cd ../..
 for r in 1 2 3 4; do for v in a b; do
