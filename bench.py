@@ -219,16 +219,24 @@ def layer_flops(T: int, S: int) -> float:
 
 
 def run_e2e(steps, T, x, dy, step):
-    """End-to-end through the public API: every step copies its inputs (x, dy)
-    from pinned host memory and reads the aux loss back.  The H2D copies of
-    step i+1 run on a copy stream while step i computes (double-buffered), as a
-    training loop's data prefetch would; every copy is inside the timed region."""
+    """End-to-end through the public API with HOST buffers: every step copies
+    its inputs (x, dy) from pinned host memory and copies its results -- the
+    layer output y, the input gradient dx and the aux loss -- back to pinned
+    host memory.  Inputs of step i+1 are prefetched on a copy stream while
+    step i computes (double-buffered, as a training loop's data prefetch); y
+    leaves on a second copy stream as soon as the forward is done (overlapping
+    the backward), dx and the loss right after the backward (overlapping the
+    next step).  Every copy is inside the timed region; the region ends when
+    the last D2H copy has landed."""
     import torch
     xh = x.detach().cpu().pin_memory()
     dyh = dy.cpu().pin_memory()
     res_h = torch.empty(steps + 2, dtype=torch.float32).pin_memory()
+    yh = [torch.empty(x.shape, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    dxh = [torch.empty(x.shape, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
     bufs = [(torch.empty_like(x), torch.empty_like(dy)) for _ in range(2)]
     cs = torch.cuda.Stream()
+    ds = torch.cuda.Stream()
     main = torch.cuda.current_stream()
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
@@ -250,9 +258,13 @@ def run_e2e(steps, T, x, dy, step):
                 prefetch(i + 1)
             b = i % 2
             main.wait_event(copied[b])
-            out, aux = step(bufs[b][0].detach().requires_grad_(), bufs[b][1])
+            xin = bufs[b][0].detach().requires_grad_()
+            out, aux = step(xin, bufs[b][1], lambda y, b=b: _d2h(ds, main, y, yh[b]))
             consumed[b].record(main)
-            res_h[i:i + 1].copy_(aux.detach().reshape(1), non_blocking=True)
+            _d2h(ds, main, xin.grad, dxh[b])
+            with torch.cuda.stream(ds):
+                res_h[i:i + 1].copy_(aux.detach().reshape(1), non_blocking=True)
+        main.wait_stream(ds)
 
     run(2)
     torch.cuda.synchronize()
@@ -263,9 +275,40 @@ def run_e2e(steps, T, x, dy, step):
     e1.record(main)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / steps
+    nb = x.numel() * 2
     return {"value": round(T / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
-            "h2d_bytes_per_step": xh.numel() * 2 + dyh.numel() * 2, "d2h_bytes_per_step": 4,
-            "ms_per_step": round(e2e_ms, 4), "h2d": "pinned host, copy stream double-buffered one step ahead"}
+            "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb + 4,
+            "ms_per_step": round(e2e_ms, 4),
+            "h2d": "x, dy from pinned host, copy stream double-buffered one step ahead",
+            "d2h": "y (after the forward, overlapping the backward), dx and the aux loss to pinned host every step"}
+
+
+def _d2h(ds, main, t, host):
+    """Copy device tensor t to pinned `host` on stream ds once `main` has
+    produced it; the caching allocator is told t is in use on ds."""
+    import torch
+    ev = torch.cuda.Event()
+    ev.record(main)
+    with torch.cuda.stream(ds):
+        ds.wait_event(ev)
+        host.copy_(t.detach(), non_blocking=True)
+        t.record_stream(ds)
+
+
+# Algorithmic HBM bytes per launch of the layer's non-GEMM kernels (reads +
+# writes that the op needs, bf16 activations, fp32 routing tensors; padding
+# rows excluded).  T tokens, S kept slots.
+def small_kernel_bytes(T: int, S: int) -> dict:
+    th, sh, te = T * H * 2, S * H * 2, T * E * 4
+    return {
+        "router_fwd": th + H * E * 4 + 3 * te,      # x, W_g; logits, gates, probs/noise
+        "dispatch": 2 * te + te,                   # gates in; slot_rank out (+ stats)
+        "permute": th + sh,                        # x in, kept rows out
+        "combine": sh + th + 2 * te,               # expert rows + gates/slots in, y out
+        "combine_bwd": th + 2 * sh + 3 * te,       # dy, o in; do, dg out
+        "router_bwd": sh + th + 4 * te,            # dxp rows in, dx out (+ dg, gates, dh)
+        "router_wgrad": th + te,                   # x, dh in
+    }
 
 
 def run_single(args, dev):
@@ -275,7 +318,8 @@ def run_single(args, dev):
     from paper_2412_09952_b200.upcycle import upcycle_experts, router_weights
 
     T = args.tokens
-    _lib.call("b200moe_gemm_set_debug", args.gemm_debug)
+    if args.gemm_debug:
+        _lib.call("b200moe_gemm_set_debug", args.gemm_debug)
     torch.manual_seed(0)
     # upcycled layer: one random-init dense SwiGLU FFN copied into 8 experts (K12)
     w1 = (torch.randn(H, F, device=dev) * 0.02).to(torch.bfloat16)
@@ -295,10 +339,12 @@ def run_single(args, dev):
     lam = torch.tensor(0.01, device=dev)
     params = [W1, W2, W3, wg, wn, x]
 
-    def step(xin, dyin):
+    def step(xin, dyin, on_forward=None):
         for p in params:
             p.grad = None
         out = B.moe_forward(xin, layer, gate)
+        if on_forward is not None:
+            on_forward(out.output)
         aux = B.importance_penalty(out.gates)
         torch.autograd.backward([out.output, aux], [dyin, lam])
         return out, aux
@@ -310,12 +356,10 @@ def run_single(args, dev):
     S = int(out.stats.assigned.sum())
 
     # ---- timed region (device time, CUDA events on the launching stream).  The
-    # per-entry-point events behind kernels_ms_per_step / roofline.achieved are
-    # recorded in a second pass of the same length right after it, so that the
-    # headline step time carries no per-call event records (BENCH_KERNEL_EVENTS=1
-    # puts them inside the timed region instead).
-    inline = os.environ.get("BENCH_KERNEL_EVENTS", "0") == "1"
-    prof = _lib.Profiler(events=inline)
+    # grouped-GEMM time is measured INSIDE the same steps: one event before FWD1
+    # and one after FWD2, one before BWD2 and one after BWD1 (the two contiguous
+    # GEMM runs of a step; _lib.GEMM_SPANS), 4 events per step.
+    prof = _lib.Profiler(spans=_lib.GEMM_SPANS)
     _lib.PROFILER = prof
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
@@ -328,31 +372,56 @@ def run_single(args, dev):
         torch.cuda.synchronize()
     _lib.PROFILER = None
     ms = s0.elapsed_time(s1) / args.steps
+    gemm_ms = prof.span_ms() / args.steps
     launches = prof.launches
+    assert len(prof.span_pairs) == 2 * args.steps and gemm_ms <= ms, (len(prof.span_pairs), gemm_ms, ms)
     # ---- e2e: through the public API with pinned host buffers, H2D + D2H inside
-    # (right after the timed region, before the profiling pass: same thermal state)
+    # (right after the timed region, before the attribution pass: same thermal state)
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args.steps, T, x, dy, step)
 
-    if not inline:
-        prof = _lib.Profiler(events=True)
-        _lib.PROFILER = prof
-        for _ in range(args.steps):
-            step(x, dy)
-        torch.cuda.synchronize()
-        _lib.PROFILER = None
-    ktimes = prof.times_ms()
+    # ---- attribution pass: per-entry-point events around every call, to split
+    # the step into kernels (its GEMM total is reported next to the timed one)
+    aprof = _lib.Profiler(events=True)
+    _lib.PROFILER = aprof
+    for _ in range(args.steps):
+        step(x, dy)
+    torch.cuda.synchronize()
+    _lib.PROFILER = None
+    ktimes = aprof.times_ms()
 
-    gemm_names = [n for n in ktimes if n.startswith("b200moe_expert_")]
-    gemm_ms = sum(ktimes[n][0] for n in gemm_names) / args.steps
     gemm_flops = 18.0 * H * F * S
     achieved_tf = gemm_flops / (gemm_ms * 1e-3) / 1e12
     peak = MEASURED["bf16_tflops"]
+    peak_s = MEASURED.get("bf16_tflops_sustained", peak)
+    hbm = MEASURED["hbm_gbs"]
     flops = layer_flops(T, S)
     tps = T / (ms * 1e-3)
     mfu_measured = flops / (ms * 1e-3) / (peak * 1e12)
     mfu_spec = flops / (ms * 1e-3) / 2.25e15
+    timed_ms = ms * args.steps
+    # Roofline denominator (B200_PROFILING.md): the burst figure for a timed
+    # region shorter than a second, the sustained (seconds-long loop) one beyond.
+    burst = timed_ms < 1000.0
+    roof_peak = peak if burst else peak_s
+    per_mode = {}
+    mode_flops = {"expert_fwd1": 4.0, "expert_fwd2": 2.0, "expert_bwd2": 2.0, "expert_wgrad": 6.0,
+                  "expert_bwd1": 4.0}
+    for n, f in mode_flops.items():
+        t = ktimes.get("b200moe_" + n)
+        if t:
+            tf = f * H * F * S / (t[0] / args.steps * 1e-3) / 1e12
+            per_mode[n] = {"ms": round(t[0] / args.steps, 4), "TFLOPs": round(tf, 1), "frac": round(tf / peak, 4)}
+    small = {}
+    for n, nbytes in small_kernel_bytes(T, S).items():
+        t = ktimes.get("b200moe_" + n)
+        if t:
+            t_ms = t[0] / args.steps
+            gbs = nbytes / (t_ms * 1e-3) / 1e9
+            small[n] = {"ms": round(t_ms, 4), "bytes": int(nbytes), "GBps": round(gbs, 1),
+                        "frac": round(gbs / hbm, 4)}
+    attr_gemm = sum(v[0] for k_, v in ktimes.items() if k_.startswith("b200moe_expert_")) / args.steps
 
     # ---- CPU baseline (oracle port) on a bounded sample, rank 0 / N=1 only
     cpu = None
@@ -363,15 +432,6 @@ def run_single(args, dev):
                          f"fp32 on {cores} threads, {cpu_model()}"}
 
     clocks = clk.summary()
-    # Roofline denominator (B200_PROFILING.md): the burst cuBLAS figure for a
-    # kernel timed alone, the sustained (power-capped, seconds-long loop) one for
-    # a kernel timed inside a long step.  The grouped GEMMs are never timed alone
-    # here: they run back to back inside the layer step for the whole timed
-    # region, at the power-capped 1.2-1.4 GHz of the sustained measurement, so
-    # the sustained figure is the denominator; the burst fraction is kept too.
-    timed_ms = ms * args.steps
-    peak_s = MEASURED.get("bf16_tflops_sustained", peak)
-    roof_peak = peak_s
     line = {
         "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 1), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
@@ -379,22 +439,28 @@ def run_single(args, dev):
         "config": {"workload": "Llama-3-8B-shape E8T2 MoE layer fwd+bwd (configs[1])", "hidden": H, "ffn": F,
                    "experts": E, "top_k": K_TOP, "tokens": T, "capacity_factor": args.cf, "router": args.router,
                    "drop_policy": args.policy, "kept_slots": S, "parallelism": "single GPU",
-                   "l2": "working set > L2: 2.8 GB of expert weights + 1.5 GB activations stream each step"},
+                   "l2": "inputs > L2, no flush: 2.8 GB of expert weights + ~1.5 GB of activations stream each step"},
         "mfu": {"measured_peak": round(mfu_measured, 4), "spec_2250": round(mfu_spec, 4),
                 "flops_per_step": flops},
         "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM, all 5 launches/step)", "bound": "tensor",
                      "achieved": round(achieved_tf, 1), "peak": roof_peak, "unit": "TFLOP/s",
                      "frac": round(achieved_tf / roof_peak, 4),
-                     "peak_kind": (f"measured sustained bf16 (MEASURED_PEAKS.json): the GEMMs run inside the "
-                                   f"layer step, back to back for the {timed_ms:.0f} ms timed region"),
-                     "frac_of_burst": round(achieved_tf / peak, 4), "burst_peak": peak, "sustained_peak": peak_s,
+                     "peak_kind": (f"measured {'burst' if burst else 'sustained'} bf16 (MEASURED_PEAKS.json): "
+                                   f"timed region {timed_ms:.0f} ms"),
+                     "frac_of_sustained": round(achieved_tf / peak_s, 4), "burst_peak": peak,
+                     "sustained_peak": peak_s,
                      "traffic": gemm_traffic(),
                      "traffic_unit": "DRAM bytes per step (5 launches), ncu --set full capture, profiles/",
                      "algorithmic_dram_bytes_per_step": gemm_min_bytes(S),
+                     "gemm_flops_per_step": gemm_flops,
                      "gemm_ms_per_step": round(gemm_ms, 4), "gemm_share_of_step": round(gemm_ms / ms, 4),
-                     "kernel_timing": ("CUDA events around each entry point on the launching stream, "
-                                       + ("inside the timed region" if inline else
-                                          f"second pass of {args.steps} steps right after the timed region"))},
+                     "kernel_timing": ("CUDA events on the launching stream around the two contiguous GEMM runs "
+                                       "of every timed step (before FWD1 / after FWD2, before BWD2 / after BWD1)")},
+        "kernels": {"gemm_modes": per_mode, "hbm_bound": small, "hbm_peak_gbs": hbm,
+                    "attribution_gemm_ms_per_step": round(attr_gemm, 4),
+                    "timing": f"attribution pass of {args.steps} steps after the timed region, events around every "
+                              f"entry point (TFLOPs/GBps from algorithmic FLOPs/bytes; frac vs burst bf16 / "
+                              f"measured HBM)"},
         "kernels_ms_per_step": {n.replace("b200moe_", ""): round(t / args.steps, 4) for n, (t, c) in ktimes.items()},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
     }

@@ -76,6 +76,23 @@ int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, co
 int b200moe_gate_from_logits(const float* logits, int T, int E, int k, int router_type, float* gates, float* probs,
                              uint8_t* topk_mask, int32_t* err_flag, cudaStream_t stream);
 
+/* Backward of the standalone gate functions (moe.py:171-186 through the
+ * softmax closure tensor.py:292-295, and the st mask product moe.py:186):
+ * dh = softmax'(dgates) over the kept k (mixtral) or over all E with the
+ * top-k mask (st, probs = full softmax).  gates/probs from
+ * b200moe_gate_from_logits. */
+int b200moe_gate_bwd(const float* dgates, const float* gates, const float* probs, int T, int E, int router_type,
+                     float* dh, cudaStream_t stream);
+
+/* Backward of the standalone router_logits (moe.py:136-149 through the
+ * matmul/softplus closures tensor.py:192-207, 220-227): given dh = dL/dlogits,
+ * dn = dh*z*sigmoid(noise_act) (noise only), dx = dh.W_g^T + dn.W_noise^T
+ * (bf16, NULL to skip), dW_g = x^T dh, dW_noise = x^T dn (fp32, NULL to skip).
+ * workspace: >= 2*H*32 + ceil(T/64)*H*E floats. */
+int b200moe_router_logits_bwd(const void* x, const float* dh, const float* w_g, const float* w_noise, const float* z,
+                              const float* noise_act, int T, int H, int E, void* dx, float* dw_g, float* dw_noise,
+                              float* dn, float* workspace, cudaStream_t stream);
+
 /* Capacity + dispatch (K1b).  Replaces moe.py:189-240 (expert_capacity is
  * evaluated by the host; capacity < 0 means dropless).  A slot exists iff
  * gate > 0; `position` keeps the earliest tokens, `score` the largest gates
@@ -183,9 +200,13 @@ int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, co
                              const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
                              int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate,
                              cudaStream_t stream);
+/* Diagnostics knobs for tests and A/B tools, NOT part of the product path:
+ * thread-local (they affect only GEMM launches issued by the calling thread;
+ * other threads always run the defaults), so the entry points above stay
+ * re-entrant.  Reset them before returning (tests use try/finally). */
 int b200moe_gemm_set_cta_group(int cta_group); /* 2 (CTA pairs, default) or 1 */
 int b200moe_gemm_set_max_ctas(int n);          /* persistent grid size (default 148) */
-int b200moe_gemm_set_debug(int flags);         /* diagnostics: bit 0 skips wgrad stores */
+int b200moe_gemm_set_debug(int flags);         /* experiment bits (0 = product kernels) */
 
 /* Online upcycling copy (K12), upcycle.py:104-112 / 216-224: replicate one
  * dense FFN ([in,out] layout: w1,w3 [H,F], w2 [F,H]; fp32 or bf16 source,

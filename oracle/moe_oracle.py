@@ -383,6 +383,64 @@ def moe_backward(cache: ForwardCache, dy, dgates=None):
 
 
 # --------------------------------------------------------------------------
+# sampled evaluation at full size (the closed form above, restricted to a
+# subset of token rows or of ffn columns).  At the Llama shape a whole oracle
+# fwd+bwd costs minutes of host time; these pieces recompute exactly the same
+# arithmetic for chosen rows / columns so the device can be checked at the
+# benchmarked size.  Same formulas as moe_forward / moe_backward
+# (moe.py:250-283, tensor.py:192-217, 292-295).
+# --------------------------------------------------------------------------
+
+def expert_rows(xe, dye, ge, w1, w2, w3):
+    """One expert on a set of its kept rows (moe.py:131-133, 272-280 and the
+    matmul/silu backward closures tensor.py:192-217).  xe, dye: [n, H];
+    ge: [n] gates.  Returns (ge*o [n,H], dg=<dy,o> [n], dx part [n,H])."""
+    ge = np.asarray(ge)[:, None]
+    a = xe @ w1
+    b = xe @ w3
+    sig = sigmoid(a)
+    m = (a * sig) * b
+    o = m @ w2
+    do = dye * ge
+    dm = do @ w2.T
+    da = dm * b * sig * (1.0 + a * (1.0 - sig))
+    db = dm * (a * sig)
+    return o * ge, (dye * o).sum(axis=1), da @ w1.T + db @ w3.T
+
+
+def expert_wgrad_columns(xe, dye, ge, w1_cols, w3_cols, w2_rows):
+    """Weight gradients of one expert restricted to a block J of ffn units:
+    dW1[:, J], dW3[:, J] ([H, |J|]) and dW2[J, :] ([|J|, H]) over ALL of the
+    expert's kept rows xe [M_e, H] (tensor.py:192-207: dB += A^T dC).  Only
+    the J columns of a, b, m and dm are needed, so the cost is O(M_e H |J|)."""
+    ge = np.asarray(ge)[:, None]
+    do = dye * ge
+    a = xe @ w1_cols
+    b = xe @ w3_cols
+    sig = sigmoid(a)
+    m = (a * sig) * b
+    dm = do @ w2_rows.T
+    da = dm * b * sig * (1.0 + a * (1.0 - sig))
+    db = dm * (a * sig)
+    return xe.T @ da, xe.T @ db, m.T @ do
+
+
+def router_bwd_rows(logits_rows, k, router_type, dg_rows, x_rows, wg, wn=None, z_rows=None, an_rows=None):
+    """Router backward for a subset of token rows (rows are independent):
+    softmax' (tensor.py:292-295) on the given gate gradients, then the router
+    contribution to dx and, with noise, the softplus-noise branch
+    (tensor.py:220-227).  Returns (dh rows, dx part rows, dn rows or None)."""
+    sub = gate(logits_rows, k, router_type)
+    dh = gate_bwd(sub, dg_rows)
+    dx = dh @ wg.T
+    dn = None
+    if z_rows is not None:
+        dn = dh * z_rows.astype(dh.dtype) * sigmoid(an_rows)
+        dx = dx + dn @ wn.T
+    return dh, dx, dn
+
+
+# --------------------------------------------------------------------------
 # dense init + upcycling (moefold/model.py:56-113, moefold/upcycle.py:46-227)
 # --------------------------------------------------------------------------
 

@@ -31,6 +31,8 @@ _F = ctypes.c_float
 SIGNATURES = {
     "b200moe_router_fwd": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "b200moe_gate_from_logits": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P],
+    "b200moe_gate_bwd": [_P, _P, _P, _I, _I, _I, _P, _P],
+    "b200moe_router_logits_bwd": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P],
     "b200moe_dispatch": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "b200moe_permute": [_P, _P, _P, _P, _I, _I, _I, _P, _P],
     "b200moe_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _P],
@@ -107,7 +109,7 @@ def exported_symbols() -> list[str]:
 
 # Kernel launches issued by each entry point (for the bench's gpu_launches).
 KERNELS_PER_CALL = {
-    "b200moe_router_fwd": 2, "b200moe_gate_from_logits": 1, "b200moe_dispatch": 1, "b200moe_permute": 1,
+    "b200moe_router_fwd": 2, "b200moe_gate_from_logits": 1, "b200moe_gate_bwd": 1, "b200moe_router_logits_bwd": 6, "b200moe_dispatch": 1, "b200moe_permute": 1,
     "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 3, "b200moe_router_wgrad": 2,
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_expert_wgrad_acc": 1,
@@ -123,16 +125,35 @@ KERNELS_PER_CALL = {
 class Profiler:
     """Optional per-entry-point accounting: launch counts and, with
     `events=True`, CUDA events recorded on the current stream around each call
-    (the stream the kernels are launched on)."""
+    (the stream the kernels are launched on).  With `spans=(starts, ends)`
+    only two events per contiguous group of calls are recorded -- one before a
+    call named in `starts`, one after a call named in `ends` -- so a timed
+    region can carry the GEMM time of its own steps at 4 events per step."""
 
-    def __init__(self, events: bool = False):
+    def __init__(self, events: bool = False, spans: tuple | None = None):
         self.events = events
+        self.spans = spans
         self.launches = 0
         self.calls: dict = {}
         self._pending: list = []
+        self._open = None
+        self.span_pairs: list = []
 
     def record(self, name, fn):
         self.launches += KERNELS_PER_CALL.get(name, 0)
+        self.calls[name] = self.calls.get(name, 0) + 1
+        if self.spans is not None:
+            import torch
+            if name in self.spans[0] and self._open is None:
+                self._open = torch.cuda.Event(enable_timing=True)
+                self._open.record()
+            rc = fn()
+            if name in self.spans[1] and self._open is not None:
+                b = torch.cuda.Event(enable_timing=True)
+                b.record()
+                self.span_pairs.append((self._open, b))
+                self._open = None
+            return rc
         if not self.events:
             return fn()
         import torch
@@ -152,6 +173,19 @@ class Profiler:
             t, n = out.get(name, (0.0, 0))
             out[name] = (t + a.elapsed_time(b), n + 1)
         return out
+
+    def span_ms(self) -> float:
+        """Sum of the recorded span durations (synchronises)."""
+        tot = 0.0
+        for a, b in self.span_pairs:
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        return tot
+
+
+# The grouped-GEMM launches of one layer step form two contiguous runs on the
+# stream: FWD1 -> FWD2 and BWD2 -> WGRAD -> BWD1.
+GEMM_SPANS = (("b200moe_expert_fwd1", "b200moe_expert_bwd2"), ("b200moe_expert_fwd2", "b200moe_expert_bwd1"))
 
 
 PROFILER: Profiler | None = None

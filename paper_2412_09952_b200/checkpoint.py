@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import json
 import os
+import warnings
 from dataclasses import asdict
 
 import numpy as np
@@ -30,7 +31,7 @@ from . import _lib
 from .errors import (ChecksumError, ConfigError, ManifestError, TruncatedFileError, UnknownVersionError)
 from .model import DenseCheckpoint, ModelConfig
 from .moe import GateConfig
-from .upcycle import EXPERT_DTYPE, DenseShard, MoECheckpoint, MoEShard
+from .upcycle import EXPERT_DTYPE, DenseShard, MoECheckpoint, MoEShard, _bf16_exact
 
 FORMAT_VERSION = 1
 ALIGNMENT = 64
@@ -284,12 +285,22 @@ def _model_from_json(d) -> ModelConfig:
 
 def _stack_experts(tensors: dict, layers, experts, device) -> dict:
     """Rebuild the bf16 kernel-layout stacks (W1, W3 [E,F,H], W2 [E,H,F]) from
-    per-expert [in, out] tensors with the K12 transpose kernel, and replace the
-    per-expert entries by views of the stacks (as upcycle_full produces)."""
+    per-expert [in, out] tensors with the K12 transpose kernel.  When every
+    expert tensor of a layer is f32 holding bf16-representable values (what
+    upcycle_full / save_checkpoint of this build produce) the per-expert entries
+    become views of the stacks, exactly as upcycle_full returns them.
+    Otherwise (f64 experts, or f32 values a bf16 copy would round) the loaded
+    full-precision tensors stay the checkpoint values -- load -> save
+    reproduces the file bytes -- and the stacks are separate bf16 compute
+    copies (a warning says so)."""
     stacked = {}
     experts = list(experts)
     for i in layers:
         p = f"layers.{i}.moe.experts"
+        exact = all(_bf16_exact(tensors[f"{p}.{e:03d}.{w}"]) for e in experts for w in ("w1", "w2", "w3"))
+        if not exact:
+            warnings.warn(f"layer {i}: expert weights are not bf16-representable f32; the B200 kernels compute "
+                          f"on bf16 copies, the checkpoint keeps the original values", RuntimeWarning, stacklevel=3)
         w1 = tensors[f"{p}.{experts[0]:03d}.w1"]
         H, F = w1.shape
         n = len(experts)
@@ -302,6 +313,8 @@ def _stack_experts(tensors: dict, layers, experts, device) -> dict:
             src = [s.to(torch.float32 if fp32 else torch.bfloat16).contiguous() for s in src]
             _lib.call("b200moe_upcycle_copy", src[0].data_ptr(), src[1].data_ptr(), src[2].data_ptr(), fp32, H, F, 1,
                       W1[j].data_ptr(), W2[j].data_ptr(), W3[j].data_ptr(), _lib.stream_ptr())
+            if not exact:
+                continue
             tensors[f"{p}.{e:03d}.w1"] = W1[j].t()
             tensors[f"{p}.{e:03d}.w2"] = W2[j].t()
             tensors[f"{p}.{e:03d}.w3"] = W3[j].t()

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <atomic>
 
 #include "../../include/b200moe.h"
 
@@ -39,6 +40,21 @@ int make_tmap_bf16_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
             return B200MOE_ERR_CUDA;                                                \
         }                                                                           \
     } while (0)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: set it once
+// per (kernel, device) the first time a launch lands on that device (thread-safe;
+// a process driving several GPUs sets it on each).
+template <class Kernel>
+inline cudaError_t ensure_smem_attr(Kernel kern, int bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 constexpr int kNumSMs = 148;     // B200
 constexpr int kSegPad = 128;     // expert segments are zero-padded to this many rows

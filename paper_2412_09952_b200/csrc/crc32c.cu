@@ -250,10 +250,10 @@ int b200moe_crc32c(const void* data, long long nbytes, unsigned int* out, void* 
     B200_CHECK_ARG(nbytes >= 0, B200MOE_ERR_SHAPE, "crc32c: negative length");
     B200_CHECK_ARG(nbytes == 0 || ((uintptr_t)data & 15) == 0, B200MOE_ERR_CONFIG,
                    "crc32c: buffer must be 16-byte aligned");
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(crc_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem);
-        attr = true;
+    static std::atomic<uint64_t> attr{0};
+    if (cudaError_t ae = ensure_smem_attr(crc_warp_kernel, (int)kCrcSmem, attr); ae != cudaSuccess) {
+        set_error("crc32c smem attribute: %s", cudaGetErrorString(ae));
+        return B200MOE_ERR_CUDA;
     }
     const long long body = nbytes & ~15LL;
     const int tail_len = (int)(nbytes - body);

@@ -1089,19 +1089,22 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ou
     return B200MOE_OK;
 }
 
-static int g_cta_group = 2;  // 2 = CTA-pair kernels (default), 1 = single-SM kernels
-static int g_max_ctas = kNumSMs;
-static int g_debug = 0;
+// Diagnostics knobs (tests and A/B tools only; the product path never sets
+// them).  Thread-local, so concurrent callers on other threads always get the
+// defaults: CTA pairs, one persistent CTA per SM, no debug flags.
+static thread_local int g_cta_group = 2;  // 2 = CTA-pair kernels (default), 1 = single-SM kernels
+static thread_local int g_max_ctas = kNumSMs;
+static thread_local int g_debug = 0;
 
 template <int kMode, int kCG>
 static int launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s) {
     using G = Geo<kMode, kCG>;
     static_assert(G::kSmemBytes <= 227 * 1024, "shared memory plan exceeds 227 KB");
     auto kern = moe_gemm_kernel<kMode, kCG>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmemBytes);
-        attr_done = true;
+    static std::atomic<uint64_t> attr_done{0};
+    if (cudaError_t ae = ensure_smem_attr(kern, G::kSmemBytes, attr_done); ae != cudaSuccess) {
+        set_error("moe_gemm_kernel<%d,%d> smem attribute: %s", kMode, kCG, cudaGetErrorString(ae));
+        return B200MOE_ERR_CUDA;
     }
     cudaLaunchConfig_t cfg = {};
     int grid = g_max_ctas - (g_max_ctas % kCG);

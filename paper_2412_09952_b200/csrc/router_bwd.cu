@@ -15,6 +15,7 @@
 // kept rows), then a bandwidth pass over [T, H] with 16-byte loads (8 hidden
 // units per lane per chunk) that gathers the expert rows and adds the router
 // term from an L1-resident swizzled copy of W.
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <math.h>
@@ -81,7 +82,7 @@ router_dh_kernel(const int32_t* __restrict__ slot_rank, const int32_t* __restric
             p[e] = pv;
             g[e] = geff;
             dot = fmaf(pv, geff, dot);
-            const int rk = slot_rank[i];
+            const int rk = slot_rank ? slot_rank[i] : -1;   // null: gate backward only (no expert rows)
             if (rk >= 0 && nrow < KM) {
 #pragma unroll
                 for (int j = 0; j < KM; ++j)
@@ -103,8 +104,18 @@ router_dh_kernel(const int32_t* __restrict__ slot_rank, const int32_t* __restric
             }
         }
     }
+    if (rows_out) {
 #pragma unroll
-    for (int j = 0; j < KM; ++j) rows_out[(size_t)t * KM + j] = rows[j];
+        for (int j = 0; j < KM; ++j) rows_out[(size_t)t * KM + j] = rows[j];
+    }
+}
+
+// dn = dh * z * sigmoid(a_n) for the standalone router-logits backward
+// (tensor.py:220-227 softplus' times the constant draw z, moe.py:149).
+__global__ void router_dn_kernel(const float* __restrict__ dh, const float* __restrict__ z,
+                                 const float* __restrict__ noise_act, size_t n, float* __restrict__ dn) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dn[i] = dh[i] * z[i] * (1.0f / (1.0f + expf(-noise_act[i])));
 }
 
 // ---- pass 2: warp per TT tokens, lane owns 8 hidden units per 256-wide chunk
@@ -146,7 +157,7 @@ router_dx_kernel(const __nv_bfloat16* __restrict__ dxp_local, const uint64_t* __
 #pragma unroll
     for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
-        for (int j = 0; j < KM; ++j) rr[tt][j] = (t0 + tt < T) ? rows_in[(size_t)(t0 + tt) * KM + j] : -1;
+        for (int j = 0; j < KM; ++j) rr[tt][j] = (rows_in && t0 + tt < T) ? rows_in[(size_t)(t0 + tt) * KM + j] : -1;
 
     for (int hb = lane; hb < HB; hb += 32) {
         float acc[TT][8];
@@ -589,6 +600,42 @@ int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, f
 }
 }  // namespace
 
+namespace {
+template <int EP>
+int router_logits_bwd_impl(const void* x, const float* dh, const float* w_g, const float* w_noise, const float* z,
+                           const float* noise_act, int T, int H, int E, void* dx, float* dw_g, float* dw_noise,
+                           float* dn, float* workspace, cudaStream_t stream) {
+    float4* wsw = reinterpret_cast<float4*>(workspace);
+    float4* wnsw = reinterpret_cast<float4*>(workspace + (size_t)H * EP);
+    float* part = workspace + (size_t)2 * H * EP;
+    const bool noise = z != nullptr;
+    if (noise) {
+        const size_t n = (size_t)T * E;
+        router_dn_kernel<<<(int)std::min<size_t>((n + 255) / 256, 4 * kNumSMs), 256, 0, stream>>>(dh, z, noise_act,
+                                                                                                  n, dn);
+    }
+    if (dx) {
+        swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
+        if (noise) swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
+        constexpr int TT = dx_tokens_per_warp(EP);
+        const int grid = ceil_div(ceil_div(T, TT), kDxThreads / 32);
+        if (noise)
+            router_dx_kernel<EP, 1, true><<<grid, kDxThreads, 0, stream>>>(nullptr, nullptr, nullptr, dh, dn, wsw,
+                                                                            wnsw, T, H, E, (__nv_bfloat16*)dx);
+        else
+            router_dx_kernel<EP, 1, false><<<grid, kDxThreads, 0, stream>>>(nullptr, nullptr, nullptr, dh, dn, wsw,
+                                                                             wnsw, T, H, E, (__nv_bfloat16*)dx);
+    }
+    if (dw_g) {
+        int rc = wgrad_impl<EP>(x, dh, T, H, E, dw_g, part, stream);
+        if (rc) return rc;
+    }
+    if (noise && dw_noise) return wgrad_impl<EP>(x, dn, T, H, E, dw_noise, part, stream);
+    B200_CHECK_LAUNCH("router_logits_bwd");
+    return B200MOE_OK;
+}
+}  // namespace
+
 extern "C" {
 
 static int router_bwd_any(const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
@@ -650,6 +697,38 @@ int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T,
     if (E <= 8) return CALL(8, dn, dw_noise);
     if (E <= 16) return CALL(16, dn, dw_noise);
     return CALL(32, dn, dw_noise);
+#undef CALL
+}
+
+int b200moe_gate_bwd(const float* dgates, const float* gates, const float* probs, int T, int E, int router_type,
+                     float* dh, cudaStream_t stream) {
+    B200_CHECK_ARG(T >= 1 && E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "bad T/E (%d, %d)", T, E);
+    B200_CHECK_ARG(router_type != B200MOE_ROUTER_ST || probs != nullptr, B200MOE_ERR_CONFIG, "st needs probs");
+#define CALL(EP) router_dh_kernel<EP, 1><<<ceil_div(T, 256), 256, 0, stream>>>(                                 \
+        nullptr, nullptr, dgates, nullptr, 0, 0, gates, probs, nullptr, nullptr, T, E, router_type, dh, nullptr, \
+        nullptr, 1)
+    if (E <= 4) CALL(4);
+    else if (E <= 8) CALL(8);
+    else if (E <= 16) CALL(16);
+    else CALL(32);
+#undef CALL
+    B200_CHECK_LAUNCH("gate_bwd");
+    return B200MOE_OK;
+}
+
+
+int b200moe_router_logits_bwd(const void* x, const float* dh, const float* w_g, const float* w_noise, const float* z,
+                              const float* noise_act, int T, int H, int E, void* dx, float* dw_g, float* dw_noise,
+                              float* dn, float* workspace, cudaStream_t stream) {
+    B200_CHECK_ARG(T >= 1 && E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "bad T/E (%d, %d)", T, E);
+    B200_CHECK_ARG(H >= 8 && H % 8 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 8, got %d", H);
+    B200_CHECK_ARG(z == nullptr || (w_noise && noise_act && dn), B200MOE_ERR_CONFIG, "noise args missing");
+#define CALL(EP) router_logits_bwd_impl<EP>(x, dh, w_g, w_noise, z, noise_act, T, H, E, dx, dw_g, dw_noise, dn, \
+                                            workspace, stream)
+    if (E <= 4) return CALL(4);
+    if (E <= 8) return CALL(8);
+    if (E <= 16) return CALL(16);
+    return CALL(32);
 #undef CALL
 }
 

@@ -33,7 +33,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .errors import ConfigError, ShapeError
-from .moe import (GateConfig, RoutingStats, SEG_PAD, _acc_targets, _arange_i32, _dispatch_ws, _ep, _noise,
+from .moe import (DeviceRoutingStats, GateConfig, SEG_PAD, _acc_targets, _arange_i32, _dispatch_ws, _ep, _noise,
                   _wgrad_call, _wgrad_outputs, expert_capacity)
 
 
@@ -285,6 +285,7 @@ class _PeerBuffers:
 
     def __init__(self, rows, H, n_counts, grp, device):
         import torch.distributed._symmetric_memory as symm
+        self.generation = 0   # bumped by every forward that (re)fills xr / O
         plane = rows * H * 2
         cnt_off = 4 * plane
         total = cnt_off + ((n_counts * 4 + 255) // 256) * 256
@@ -357,6 +358,7 @@ class _EPPeerFunction(torch.autograd.Function):
                   _dispatch_ws(dev).data_ptr(), s)
         seg_peer = plan.peer_seg_base(dev)      # row of (this rank, expert e) in e's owner buffer
         pb.barrier()                            # every rank is done with the previous use of the buffers
+        pb.generation += 1
         _lib.call("b200moe_permute_peer", x.data_ptr(), slot_rank.data_ptr(), seg_peer.data_ptr(),
                   counts.data_ptr(), T, H, E, El, plan.rank, pb.peer[0].data_ptr(), pb.peer_counts.data_ptr(), s)
         pb.barrier()                            # all tokens and counts have landed
@@ -379,6 +381,7 @@ class _EPPeerFunction(torch.autograd.Function):
         ctx.st = st
         ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.pb = pb
+        ctx.generation = pb.generation
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer,
                               A, B, Hh)
         return y, gates
@@ -388,6 +391,11 @@ class _EPPeerFunction(torch.autograd.Function):
         (x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer, A, B,
          Hh) = ctx.saved_tensors
         st, pb = ctx.st, ctx.pb
+        if pb.generation != ctx.generation:
+            # another forward on the same buffer slot overwrote the saved xr / O
+            raise RuntimeError(f"EP symmetric buffer slot {st.get('buffer_slot', 0)} was refilled by a later forward "
+                               f"before this backward; give layers that are alive in one graph distinct buffer_slot "
+                               f"values")
         cfg, plan, group = st["cfg"], st["plan"], st["group"]
         T, H = x.shape
         E = w_g.shape[1]
@@ -475,11 +483,28 @@ class ExpertParallelMoE:
             raise ConfigError("the B200 router supports up to 32 experts")
         self.w_g, self.w_noise, self.W1, self.W2, self.W3, self.cfg = w_g, w_noise, W1, W2, W3, cfg
         self.buffer_slot = buffer_slot
+        self._tokens_checked = set()
+
+    def _check_tokens(self, T: int, device) -> None:
+        """The p2p transport sizes every rank's receive segments from T_local
+        (EPPlan.cap_pad), so all ranks must agree on T.  Checked once per T with
+        one all_reduce (max of T and of -T) and a host read."""
+        if T in self._tokens_checked:
+            return
+        t = torch.tensor([T, -T], dtype=torch.int64, device=device if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        hi, lo = int(t[0]), -int(t[1])
+        if hi != T or lo != T:
+            raise ShapeError(f"expert-parallel ranks disagree on tokens per rank (this rank {T}, range [{lo}, {hi}]); "
+                             f"the p2p transport needs equal T_local on every rank")
+        self._tokens_checked.add(T)
 
     def forward(self, x: torch.Tensor, rng=None, training: bool = False, noise=None, reduce_router: bool = True):
         T, H = x.shape
         if H % 256 or self.W1.shape[1] % 256:
             raise ShapeError("the EP path needs hidden and ffn multiples of 256")
+        if self.transport == "p2p":
+            self._check_tokens(T, x.device)
         plan = EPPlan.make(self.world, self.rank, self.cfg.n_experts, T, self.cfg.capacity_factor)
         z = _noise(T, self.cfg.n_experts, x.device, self.cfg.noise_enabled and training, rng, noise)
         st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router, buffer_slot=self.buffer_slot)
@@ -489,7 +514,7 @@ class ExpertParallelMoE:
         r = st["routing"]
         from .moe import MoEForwardResult
         gates._b200_importance = (r["importance"], gates._version)
-        out = MoEForwardResult(output=y, stats=RoutingStats(r["counts"], r["stats"], r["gate_mass"], plan.capacity,
+        out = MoEForwardResult(output=y, stats=DeviceRoutingStats(r["counts"], r["stats"], r["gate_mass"], plan.capacity,
                                                             r["err"]), gates=gates)
         out.routing = r
         out.plan = plan
@@ -529,10 +554,12 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     lam = torch.tensor(0.01, device=dev)
     params = [W1, W2, W3, wg, wn, x]
 
-    def step(xin, dyin):
+    def step(xin, dyin, on_forward=None):
         for p in params:
             p.grad = None
         out = layer(xin)
+        if on_forward is not None:
+            on_forward(out.output)
         aux = P.importance_penalty(out.gates)
         torch.autograd.backward([out.output, aux], [dyin, lam])
         return out, aux
@@ -552,7 +579,8 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
         out, _ = step(x, dy)
     torch.cuda.synchronize()
     S = int(out.routing["recv_counts"].sum().item())
-    prof = _lib.Profiler(events=False)
+    # timed region: GEMM spans recorded inside the same steps (see bench.py)
+    prof = _lib.Profiler(spans=_lib.GEMM_SPANS)
     _lib.PROFILER = prof
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with B.ClockSampler(dev.index) as clk:
@@ -566,6 +594,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
         dist.barrier()
     _lib.PROFILER = None
     ms = e0.elapsed_time(e1) / args.steps
+    gemm_ms = prof.span_ms() / args.steps
     t = torch.tensor([ms, float(S)], device=dev, dtype=torch.float64)
     tmax = t.clone()
     dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
@@ -574,14 +603,13 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     ms_max = float(tmax[0])
     S_tot = float(ssum[0])
 
-    # e2e: host-resident x / dy copied in (copy stream, one step ahead), aux loss read back, every step
+    # e2e: host-resident x / dy copied in, y / dx / aux loss copied out, every step
     dist.barrier()
     e2e_rank = B.run_e2e(args.steps, T, x, dy, step)
     e2e_t = torch.tensor([e2e_rank["ms_per_step"]], device=dev, dtype=torch.float64)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     clocks = clk.summary()
-    # GEMM roofline on this rank: per-entry-point CUDA events on the launching
-    # stream over a few extra steps (the timed region above runs without them)
+    # attribution pass on this rank: per-entry-point events (exchange kernels)
     kp = _lib.Profiler(events=True)
     _lib.PROFILER = kp
     n_prof = 3
@@ -590,7 +618,6 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     torch.cuda.synchronize()
     _lib.PROFILER = None
     kt = kp.times_ms()
-    gemm_ms = sum(v[0] for k_, v in kt.items() if k_.startswith("b200moe_expert_")) / n_prof
     achieved = 18.0 * H * F * S / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     # NVLink side of the fused exchange (p2p): bytes each peer kernel moves to or
     # from other ranks' buffers per step -- (R-1)/R of this rank's kept rows
@@ -610,11 +637,24 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                     "ms": round(t_ms, 4), "nvlink_bytes": int(nbytes),
                     "GBps": round(nbytes / (t_ms * 1e-3) / 1e9, 1),
                     "frac_of_770": round(nbytes / (t_ms * 1e-3) / 1e9 / 770.0, 3)}
+    # CPU baseline: the oracle on the R rank-local batches, run
+    # one after the other on rank 0's host cores, each a bounded sample of
+    # cpu_tokens tokens; tokens/s = R * sample / total time.
+    cpu = None
+    if not getattr(args, "no_cpu_baseline", False) and rank == 0:
+        times, cores = B.cpu_sample(args.cpu_tokens, args.cf, args.router, args.policy, world)
+        cpu = {"value": round(world * args.cpu_tokens / sum(times), 3), "unit": "tokens/s", "cores": cores,
+               "kind": "port",
+               "sample": f"{world} rank-local batches of {args.cpu_tokens} tokens, fwd+bwd at the Llama-3 shape run "
+                         f"sequentially, numpy/OpenBLAS fp32 on {cores} threads, {B.cpu_model()}"}
+    dist.barrier()
     if rank == 0:
         tps = world * T / (ms_max * 1e-3)
         flops = 18.0 * H * F * S_tot + 6.0 * world * T * H * E
         peak = measured["bf16_tflops"]
-        roof_peak = measured.get("bf16_tflops_sustained", peak)   # GEMMs inside the step: see bench.py
+        peak_s = measured.get("bf16_tflops_sustained", peak)
+        burst = ms_max * args.steps < 1000.0
+        roof_peak = peak if burst else peak_s
         line = {
             "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 1), "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4),
@@ -627,20 +667,24 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                                 "(device barriers) + NCCL all_reduce(dW_g)" if args.transport == "p2p" else
                                 "NCCL all_to_all_single (exact splits) + all_reduce(dW_g)"),
                        "transport": args.transport,
-                       "l2": "working set > L2 (expert weights + activations)"},
+                       "l2": "inputs > L2, no flush (expert weights + activations)"},
             "mfu": {"measured_peak": round(flops / (ms_max * 1e-3) / (world * peak * 1e12), 4),
                     "spec_2250": round(flops / (ms_max * 1e-3) / (world * 2.25e15), 4)},
             "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM, rank 0's 5 launches/step)", "bound": "tensor",
                          "achieved": None if achieved is None else round(achieved, 1), "peak": roof_peak,
                          "unit": "TFLOP/s", "frac": None if achieved is None else round(achieved / roof_peak, 4),
-                         "peak_kind": "measured sustained bf16 (GEMMs inside the layer step)",
-                         "frac_of_burst": None if achieved is None else round(achieved / peak, 4),
-                         "traffic": None, "gemm_ms_per_step": round(gemm_ms, 4),
-                         "gemm_share_of_step": round(gemm_ms / ms_max, 4)},
+                         "peak_kind": f"measured {'burst' if burst else 'sustained'} bf16",
+                         "frac_of_sustained": None if achieved is None else round(achieved / peak_s, 4),
+                         "traffic": None,
+                         "traffic_note": "no multi-GPU ncu capture; N=1 capture in profiles/",
+                         "algorithmic_dram_bytes_per_step": B.gemm_min_bytes(S),
+                         "gemm_ms_per_step": round(gemm_ms, 4), "gemm_share_of_step": round(gemm_ms / ms, 4),
+                         "kernel_timing": "events around the two GEMM runs of every timed step (rank 0)"},
             "e2e": {"value": round(world * T / (float(e2e_t[0]) * 1e-3), 1), "unit": "tokens/s",
-                    "h2d_bytes_per_step": world * e2e_rank["h2d_bytes_per_step"], "d2h_bytes_per_step": 4 * world,
-                    "h2d": e2e_rank["h2d"]},
-            "cpu_baseline": None, "clocks": clocks, "gpu_launches": prof.launches,
+                    "h2d_bytes_per_step": world * e2e_rank["h2d_bytes_per_step"],
+                    "d2h_bytes_per_step": world * e2e_rank["d2h_bytes_per_step"],
+                    "h2d": e2e_rank["h2d"], "d2h": e2e_rank["d2h"]},
+            "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": prof.launches,
             "exchange": exchange,
         }
         print(json.dumps(line), flush=True)

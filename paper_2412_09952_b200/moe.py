@@ -121,13 +121,11 @@ class MoELayer:
         return cls(router=router, experts=experts, stacked=(W1, W2, W3))
 
     def stacked_weights(self):
-        """(W1, W2, W3) in kernel layout; differentiable w.r.t. the experts."""
+        """(W1, W2, W3) in kernel layout (bf16 for ExpertFFN-list layers);
+        differentiable w.r.t. the experts."""
         if self.stacked is not None:
             return self.stacked
-        W1 = torch.stack([ex.w1.t() for ex in self.experts])
-        W2 = torch.stack([ex.w2.t() for ex in self.experts])
-        W3 = torch.stack([ex.w3.t() for ex in self.experts])
-        return W1, W2, W3
+        return _StackExperts.apply(self, *[getattr(ex, w) for ex in self.experts for w in ("w1", "w2", "w3")])
 
     def expert_grad(self, e: int, name: str):
         """Gradient of expert e's `name` ('w1'|'w2'|'w3') in the reference shape."""
@@ -137,12 +135,71 @@ class MoELayer:
         return None if W.grad is None else W.grad[e].t()
 
 
-class RoutingStats:
-    """Per-batch routing outcome (moe.py:95-116).  Backed by device tensors and
-    materialised to numpy on first access (one device->host copy), so the
-    forward pass never synchronises the host."""
+class _StackExperts(torch.autograd.Function):
+    """Per-expert [in, out] parameters (a reference caller's
+    MoELayer(router, [ExpertFFN, ...]), model.py:177-188) -> the stacked bf16
+    kernel layout W1, W3 [E,F,H], W2 [E,H,F].  The stacks are cached on the
+    layer and rebuilt only when an expert tensor changed (its version counter
+    moves on every in-place update, e.g. an optimizer step), so repeated
+    forwards with the same weights copy nothing.  Backward hands each expert
+    the transposed slice of the stacked gradient in its own dtype."""
 
-    def __init__(self, counts, stats, gate_mass, capacity, err_flag=None):
+    @staticmethod
+    def forward(ctx, layer, *ws):
+        key = tuple((t.data_ptr(), t._version, t.dtype, tuple(t.shape), tuple(t.stride())) for t in ws)
+        cache = layer.__dict__.get("_stack_cache")
+        if cache is None or cache[0] != key:
+            n = len(ws) // 3
+            stacks = tuple(torch.stack([ws[3 * e + j].detach().t() for e in range(n)]).to(torch.bfloat16).contiguous()
+                           for j in range(3))
+            cache = (key, stacks)
+            layer.__dict__["_stack_cache"] = cache
+        ctx.dtypes = [t.dtype for t in ws]
+        return tuple(s.detach() for s in cache[1])
+
+    @staticmethod
+    def backward(ctx, g1, g2, g3):
+        out = [None]
+        n = len(ctx.dtypes) // 3
+        for e in range(n):
+            for j, g in enumerate((g1, g2, g3)):
+                out.append(None if g is None else g[e].t().to(ctx.dtypes[3 * e + j]))
+        return tuple(out)
+
+
+@dataclass
+class RoutingStats:
+    """Per-batch routing outcome for one MoE layer (moe.py:95-116): same
+    fields and constructor as the reference."""
+
+    assigned: np.ndarray          # [N] kept slots per expert
+    dropped: int                  # slots excluded by capacity
+    total_slots: int              # slots with a positive gate
+    gate_mass: np.ndarray         # [N] summed gate values of kept slots
+    capacity: int | None
+
+    @property
+    def drop_rate(self) -> float:
+        return self.dropped / self.total_slots if self.total_slots else 0.0
+
+    @property
+    def load_entropy(self) -> float:
+        """Entropy (nats) of the kept-slot distribution over experts."""
+        a = self.assigned
+        total = int(a.sum())
+        if total == 0:
+            return 0.0
+        p = a[a > 0] / total
+        return float(-(p * np.log(p)).sum())
+
+
+class DeviceRoutingStats(RoutingStats):
+    """RoutingStats backed by the dispatch kernel's device tensors and
+    materialised to numpy on first access (one device->host copy), so the
+    forward pass never synchronises the host.  A GateError recorded by the
+    router (all-masked softmax row) surfaces on that first access."""
+
+    def __init__(self, counts, stats, gate_mass, capacity, err_flag=None):  # noqa: D107 (no dataclass init)
         self._dev = (counts, stats, gate_mass, err_flag)
         self._host = None
         self.capacity = capacity
@@ -153,8 +210,7 @@ class RoutingStats:
             if err is not None and int(err.item()) != 0:
                 raise GateError("softmax row with all entries masked")
             st = stats.cpu().numpy()
-            self._host = (counts.cpu().numpy().astype(np.int64), int(st[0]), int(st[1]),
-                          mass.cpu().numpy())
+            self._host = (counts.cpu().numpy().astype(np.int64), int(st[0]), int(st[1]), mass.cpu().numpy())
         return self._host
 
     @property
@@ -173,22 +229,13 @@ class RoutingStats:
     def gate_mass(self) -> np.ndarray:
         return self._materialize()[3]
 
-    @property
-    def drop_rate(self) -> float:
-        return self.dropped / self.total_slots if self.total_slots else 0.0
-
-    @property
-    def load_entropy(self) -> float:
-        a = self.assigned
-        total = int(a.sum())
-        if total == 0:
-            return 0.0
-        p = a[a > 0] / total
-        return float(-(p * np.log(p)).sum())
+    def to_host(self) -> RoutingStats:
+        """A plain (reference-type) RoutingStats with the same values."""
+        return RoutingStats(self.assigned, self.dropped, self.total_slots, self.gate_mass, self.capacity)
 
     def __repr__(self):
-        return (f"RoutingStats(assigned={self.assigned.tolist()}, dropped={self.dropped}, "
-                f"total_slots={self.total_slots}, capacity={self.capacity})")
+        return (f"RoutingStats(assigned={self.assigned!r}, dropped={self.dropped}, total_slots={self.total_slots}, "
+                f"gate_mass={self.gate_mass!r}, capacity={self.capacity})")
 
 
 @dataclass
@@ -251,13 +298,15 @@ def _arange_i32(n: int, device) -> torch.Tensor:
     return t
 
 
-def _as_logits(h) -> torch.Tensor:
+def _as_logits(h, keep_graph: bool = False) -> torch.Tensor:
     if isinstance(h, np.ndarray):
         h = torch.from_numpy(np.ascontiguousarray(h, dtype=np.float32)).cuda()
     _require_cuda(h, "logits")
     if h.dim() == 1:
         h = h[None, :]
-    return h.detach().to(torch.float32).contiguous()
+    if not keep_graph:
+        h = h.detach()
+    return h.to(torch.float32).contiguous()
 
 
 def expert_capacity(tokens_per_batch: int, n_experts: int, cf: float | None) -> int | None:
@@ -313,38 +362,106 @@ def _checked(gates, err):
     return gates
 
 
+class _GateFunction(torch.autograd.Function):
+    """gates = gate_{mixtral,st}(h, k) on K1's gate core; backward = the masked
+    softmax' of tensor.py:292-295 (b200moe_gate_bwd)."""
+
+    @staticmethod
+    def forward(ctx, h, k: int, router_type: str):
+        g, probs, _, err = _gate(h, k, router_type)
+        _checked(g, err)    # the reference raises GateError at call time (tensor.py:283-284)
+        ctx.router_type = router_type
+        ctx.save_for_backward(g, probs)
+        return g
+
+    @staticmethod
+    def backward(ctx, dg):
+        g, probs = ctx.saved_tensors
+        T, E = g.shape
+        dgc = dg.to(torch.float32).contiguous()
+        dh = torch.empty_like(g)
+        _lib.call("b200moe_gate_bwd", dgc.data_ptr(), g.data_ptr(), _lib.ptr(probs), T, E, _lib.ROUTER[ctx.router_type],
+                  dh.data_ptr(), _lib.stream_ptr())
+        return dh, None, None
+
+
+def _gate_fn(h, k: int, router_type: str) -> torch.Tensor:
+    squeeze = getattr(h, "ndim", 2) == 1
+    g = _GateFunction.apply(_as_logits(h, keep_graph=True), k, router_type)
+    return g[0] if squeeze else g
+
+
 def gate_mixtral(h, k: int) -> torch.Tensor:
-    """Top-k mask first, then softmax over the survivors; rows sum to 1."""
-    g, _, _, err = _gate(h, k, "mixtral")
-    return _checked(g, err)
+    """Top-k mask first, then softmax over the survivors; rows sum to 1
+    (moe.py:171-173).  Differentiable w.r.t. h."""
+    return _gate_fn(h, k, "mixtral")
 
 
 def gate_st(h, k: int) -> torch.Tensor:
-    """Softmax over all experts, then top-k (on the logits) without renormalization."""
-    g, _, _, err = _gate(h, k, "st")
-    return _checked(g, err)
+    """Softmax over all experts, then top-k (on the logits) without
+    renormalization (moe.py:176-186).  Differentiable w.r.t. h."""
+    return _gate_fn(h, k, "st")
+
+
+class _RouterLogitsFunction(torch.autograd.Function):
+    """h = x.W_g (+ z * softplus(x.W_noise)) on K1 (b200moe_router_fwd); the
+    backward (b200moe_router_logits_bwd) gives dx, dW_g and, with noise,
+    dW_noise -- the matmul/softplus closures of tensor.py:192-207, 220-227."""
+
+    @staticmethod
+    def forward(ctx, xb, wg, wn, z):
+        T, H = xb.shape
+        E = wg.shape[1]
+        dev = xb.device
+        logits = torch.empty(T, E, dtype=torch.float32, device=dev)
+        gates = torch.empty_like(logits)
+        na = torch.empty_like(logits) if z is not None else None
+        ws = torch.empty(2 * H * _ep(E), dtype=torch.float32, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("b200moe_router_fwd", xb.data_ptr(), wg.data_ptr(), wn.data_ptr(), _lib.ptr(z), T, H, E, 1, 0,
+                  logits.data_ptr(), gates.data_ptr(), None, _lib.ptr(na), ws.data_ptr(), err.data_ptr(),
+                  _lib.stream_ptr())
+        ctx.save_for_backward(xb, wg, wn, z, na)
+        return logits
+
+    @staticmethod
+    def backward(ctx, dlogits):
+        xb, wg, wn, z, na = ctx.saved_tensors
+        T, H = xb.shape
+        E = wg.shape[1]
+        dev = xb.device
+        dh = dlogits.to(torch.float32).contiguous()
+        want_x, want_g, want_n = ctx.needs_input_grad[0], ctx.needs_input_grad[1], ctx.needs_input_grad[2]
+        noise = z is not None
+        dx = torch.empty(T, H, dtype=torch.bfloat16, device=dev) if want_x else None
+        dwg = torch.empty(H, E, dtype=torch.float32, device=dev) if want_g else None
+        dwn = torch.empty(H, E, dtype=torch.float32, device=dev) if (want_n and noise) else None
+        dn = torch.empty(T, E, dtype=torch.float32, device=dev) if noise else None
+        ws = torch.empty(2 * H * _ep(E) + (T + 63) // 64 * H * E, dtype=torch.float32, device=dev)
+        _lib.call("b200moe_router_logits_bwd", xb.data_ptr(), dh.data_ptr(), wg.data_ptr(), wn.data_ptr(),
+                  _lib.ptr(z), _lib.ptr(na), T, H, E, _lib.ptr(dx), _lib.ptr(dwg), _lib.ptr(dwn), _lib.ptr(dn),
+                  ws.data_ptr(), _lib.stream_ptr())
+        return dx, dwg, dwn, None
 
 
 def router_logits(x: torch.Tensor, p: RouterParams, noise_enabled: bool, rng: Rng | None = None,
                   noise: torch.Tensor | None = None) -> torch.Tensor:
-    """Per-token expert logits x @ W_g (+ z * softplus(x @ W_noise)), fp32.
-    Forward-only view of K1; the differentiable path is moe_forward."""
+    """Per-token expert logits x @ W_g (+ z * softplus(x @ W_noise)), fp32
+    (moe.py:136-149).  Differentiable w.r.t. x, W_g and (with noise) W_noise;
+    x enters the kernel as bf16 (the layer's compute dtype)."""
     _require_cuda(x, "x")
     T, H = x.shape
     E = p.w_g.shape[1]
     z = _noise(T, E, x.device, noise_enabled, rng, noise)
-    xb = x.detach().to(torch.bfloat16).contiguous()
-    wg = p.w_g.detach().to(torch.float32).contiguous()
-    wn = p.w_noise.detach().to(torch.float32).contiguous()
-    logits = torch.empty(T, E, dtype=torch.float32, device=x.device)
-    gates = torch.empty_like(logits)
-    na = torch.empty_like(logits) if z is not None else None
-    ws = torch.empty(2 * H * _ep(E), dtype=torch.float32, device=x.device)
-    err = torch.zeros(1, dtype=torch.int32, device=x.device)
-    _lib.call("b200moe_router_fwd", xb.data_ptr(), wg.data_ptr(), wn.data_ptr(), _lib.ptr(z), T, H, E, 1, 0,
-              logits.data_ptr(), gates.data_ptr(), None, _lib.ptr(na), ws.data_ptr(), err.data_ptr(),
-              _lib.stream_ptr())
-    return logits
+    xb = x.to(torch.bfloat16)
+    wg = p.w_g.to(torch.float32)
+    wn = p.w_noise.to(torch.float32)
+    Hp = _pad_to(H, GEMM_ALIGN)
+    if Hp != H:   # zero hidden columns add +0 (the router kernels tile H by 256)
+        xb = torch.nn.functional.pad(xb, (0, Hp - H))
+        wg = torch.nn.functional.pad(wg, (0, 0, 0, Hp - H))
+        wn = torch.nn.functional.pad(wn, (0, 0, 0, Hp - H))
+    return _RouterLogitsFunction.apply(xb.contiguous(), wg.contiguous(), wn.contiguous(), z)
 
 
 def _noise(T, E, device, enabled, rng, noise):
@@ -389,7 +506,7 @@ def dispatch(gates, capacity: int | None, drop_policy: str = "position") -> Disp
     kept = slot_rank >= 0
     dropped = (g > 0) & ~kept
     return DispatchResult(kept=kept, dropped=dropped,
-                          stats=RoutingStats(counts, stats, gate_mass, capacity), slot_rank=slot_rank)
+                          stats=DeviceRoutingStats(counts, stats, gate_mass, capacity), slot_rank=slot_rank)
 
 
 # --------------------------------------------------------------------------
@@ -498,7 +615,8 @@ class _MoEFunction(torch.autograd.Function):
                   H, E, y.data_ptr(), s)
 
         st.routing = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_base,
-                          gate_mass=gate_mass, importance=imp, stats=stats, err=err, capacity=cap, rows=R)
+                          gate_mass=gate_mass, importance=imp, stats=stats, err=err, capacity=cap, rows=R,
+                          noise_act=noise_act)
         ctx.st = st
         ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts,
@@ -559,6 +677,8 @@ class _MoEFunction(torch.autograd.Function):
         wsw = torch.empty((T + 63) // 64 * H * E, **f32)
         _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), _lib.ptr(dn), T, H, E, dwg.data_ptr(),
                   _lib.ptr(dwn), wsw.data_ptr(), s)
+        if st.routing is not None:   # router-logit gradients, for inspection (out.routing["dh"])
+            st.routing["dh"], st.routing["dn"] = dh, dn
         return dx, dwg, dwn, dW1, dW2, dW3, None, None
 
 
@@ -605,7 +725,7 @@ def moe_forward(x: torch.Tensor, layer: MoELayer, cfg: GateConfig, rng: Rng | No
         y = y[:, :H]
     r = st.routing
     gates._b200_importance = (r["importance"], gates._version)
-    stats = RoutingStats(r["counts"], r["stats"], r["gate_mass"], r["capacity"], r["err"])
+    stats = DeviceRoutingStats(r["counts"], r["stats"], r["gate_mass"], r["capacity"], r["err"])
     out = MoEForwardResult(output=y, stats=stats, gates=gates)
     out.routing = r  # device-side routing tensors (slot_rank, counts, logits, ...) for inspection
     return out
@@ -640,6 +760,12 @@ class _ImportanceFunction(torch.autograd.Function):
             imp = torch.empty(E, dtype=torch.float32, device=g.device)
             _lib.call("b200moe_importance_fwd", g.data_ptr(), T, E, imp.data_ptr(), loss.data_ptr(), err.data_ptr(),
                       _lib.stream_ptr())
+            # Arbitrary gates: raise GateError at call time like the reference
+            # (tensor.py:512-513), at the cost of one host sync.  Gates straight
+            # from moe_forward skip it: every row there holds a positive top-1
+            # gate (or the router already flagged the row), so mean > 0.
+            if int(err.item()) != 0:
+                raise GateError("importance penalty needs positive total gate mass")
         ctx.save_for_backward(imp)
         ctx.shape = (T, E)
         ctx.err = err
@@ -657,7 +783,7 @@ class _ImportanceFunction(torch.autograd.Function):
 
 def importance_penalty(gates: torch.Tensor) -> torch.Tensor:
     """Squared coefficient of variation of per-expert gate mass; zero when
-    balanced.  GateError (checked lazily via .err) if the total mass is <= 0."""
+    balanced (tensor.py:503-521).  GateError if the total mass is <= 0."""
     _require_cuda(gates, "gates")
     if gates.dim() != 2:
         raise ShapeError("importance penalty needs a [T, E] gate matrix")

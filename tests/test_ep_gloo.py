@@ -110,3 +110,46 @@ def test_ep_plan_layout_rules():
     assert EPPlan.make(2, 0, 8, 300, None).cap_pad == 384         # dropless: T rows per expert segment
     with pytest.raises(ConfigError):
         EPPlan.make(3, 0, 8, 64, 1.0)
+
+
+def _tokens_worker(rank, world, port, same, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2412_09952_b200 import GateConfig
+        from paper_2412_09952_b200.errors import ShapeError
+        from paper_2412_09952_b200.ep import ExpertParallelMoE
+        E, H, F = 4, 256, 256
+        layer = ExpertParallelMoE(torch.zeros(H, E), torch.zeros(H, E), torch.zeros(E // world, F, H),
+                                  torch.zeros(E // world, H, F), torch.zeros(E // world, F, H),
+                                  GateConfig(n_experts=E, top_k=2, capacity_factor=1.0))
+        T = 64 if same or rank == 0 else 32
+        try:
+            layer._check_tokens(T, torch.device("cpu"))
+            out_q.put((rank, "ok"))
+        except ShapeError as e:
+            out_q.put((rank, "shape:" + str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("same", [True, False])
+def test_p2p_transport_rejects_unequal_tokens_per_rank(same):
+    """the p2p receive segments are sized from T_local on every rank,
+    so ranks with different T must raise ShapeError instead of writing past a
+    smaller peer's buffer."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tokens_worker, args=(r, world, port, same, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    if same:
+        assert res == {0: "ok", 1: "ok"}
+    else:
+        assert all(v.startswith("shape:") and "disagree on tokens" in v for v in res.values()), res

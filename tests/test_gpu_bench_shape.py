@@ -1,0 +1,211 @@
+"""Parity at the benchmarked shape: BASELINE.json configs[1] exactly
+(T=8192 tokens, hidden 4096, ffn 14336, E=8, top-2), the configuration
+bench.py measures.
+
+A whole fp32 oracle fwd+bwd at this size costs minutes of host time, so the
+checks split the layer into pieces the oracle can recompute exactly
+(oracle/moe_oracle.py `expert_rows`, `expert_wgrad_columns`,
+`router_bwd_rows`), each on the device's own intermediate where the parity
+rule says so:
+
+  (a) router logits over ALL tokens vs the fp32 oracle
+      h = bf16(x).W_g + z * softplus(bf16(x).W_noise)          moe.py:136-149,
+      and the noise pre-activation a_n = bf16(x).W_noise        tensor.py:220-236
+      -- bound: |dh| <= 1e-5 * (sum_j |x_j w_j| + |z| softplus) + 1e-6 per entry
+         (fp32 accumulation-order slack of a 4096-term dot product);
+  (b) routing over ALL tokens bit-exact vs the oracle fed the device logits
+      (gates, kept/dropped, slot order, counts, drop stats)     moe.py:171-240;
+  (c) y and dx on 256 sampled tokens, rel. Frobenius <= 1.5e-2  moe.py:250-283;
+      dh (router-logit gradient) on the same tokens <= 2e-2    tensor.py:292-295;
+      dW_g / dW_noise = x^T dh (device dh) <= 1e-4 (fp32 reduction order);
+      dW1 / dW3 / dW2 on a sampled block of 128 ffn units of every expert,
+      over all of the expert's kept rows, <= 2e-2               tensor.py:192-207;
+  (d) importance-penalty loss value rel <= 1e-5, gate_mass rel <= 1e-5
+                                                                tensor.py:503-521.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+T, H, F, E, K = 8192, 4096, 14336, 8, 2
+TOL_Y = 1.5e-2
+TOL_W = 2e-2
+LAM = 0.01
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16)
+
+
+@pytest.fixture(scope="module")
+def inputs():
+    """configs[1] recipe: x = Rng(123,0), dy = Rng(124,0),
+    z = Rng(5,0) draws, router = router_weights(seed 1, layer 0) (moefold
+    upcycle.py:72-81); W_noise ~ N(0, 0.02) from Rng(6,0) so that the noise
+    branch is not trivially softplus(0)."""
+    x = _bf16(O.rng(123, 0).standard_normal((T, H)))
+    dy = _bf16(O.rng(124, 0).standard_normal((T, H)))
+    z = O.rng(5, 0).standard_normal((T, E)).astype(np.float32)
+    wg, _ = O.router_weights(H, E, 0, 1, np.float32)
+    wn = (O.rng(6, 0).standard_normal((H, E)) * 0.02).astype(np.float32)
+    return dict(x=x, dy=dy, z=z, wg=wg, wn=wn)
+
+
+def _experts(upcycled: bool, seed: int):
+    """Expert weights in kernel layout (W1, W3 [E,F,H], W2 [E,H,F]) bf16: either
+    the bench's upcycled layer (one N(0, 0.02) dense FFN copied by K12) or
+    distinct random experts (catches any expert-index mix-up)."""
+    import paper_2412_09952_b200 as B  # noqa: F401
+    from paper_2412_09952_b200.upcycle import upcycle_experts
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    if upcycled:
+        w1 = (torch.randn(H, F, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+        w2 = (torch.randn(F, H, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+        w3 = (torch.randn(H, F, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+        return upcycle_experts(w1, w2, w3, E)
+    Ws = []
+    for shape in ((E, F, H), (E, H, F), (E, F, H)):
+        W = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+        for e in range(E):
+            W[e] = (torch.randn(shape[1:], device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+        Ws.append(W)
+    return tuple(Ws)
+
+
+def _host_expert(W1, W2, W3, e):
+    """Expert e in the reference [in, out] shapes, fp32 (exact bf16 values)."""
+    return (W1[e].t().float().cpu().numpy(), W2[e].t().float().cpu().numpy(), W3[e].t().float().cpu().numpy())
+
+
+CASES = [
+    # (router, policy, cf, noise, upcycled)
+    ("mixtral", "position", 1.0, False, True),    # exactly the bench.py workload
+    ("mixtral", "position", 1.0, True, False),
+    ("st", "score", 2.0, True, False),
+    ("st", "score", 1.0, False, False),
+    ("mixtral", "position", 2.0, False, False),
+]
+
+
+@pytest.mark.parametrize("rt,pol,cf,noise,upcycled", CASES)
+def test_bench_shape_parity(inputs, rt, pol, cf, noise, upcycled):
+    import paper_2412_09952_b200 as B
+    dev = torch.device("cuda")
+    torch.cuda.empty_cache()
+    W1, W2, W3 = (w.requires_grad_() for w in _experts(upcycled, seed=11 if upcycled else 12))
+    wg_t = torch.from_numpy(inputs["wg"]).to(dev).requires_grad_()
+    wn_np = inputs["wn"] if noise else np.zeros_like(inputs["wn"])
+    wn_t = torch.from_numpy(wn_np).to(dev).requires_grad_()
+    layer = B.MoELayer.from_stacked(B.RouterParams(wg_t, wn_t), W1, W2, W3)
+    x_t = inputs["x"].to(dev).requires_grad_()
+    dy_t = inputs["dy"].to(dev)
+    z = inputs["z"]
+    cfg = B.GateConfig(n_experts=E, top_k=K, router_type=rt, noise_enabled=noise, capacity_factor=cf,
+                       drop_policy=pol)
+    out = B.moe_forward(x_t, layer, cfg, training=True, noise=torch.from_numpy(z).to(dev) if noise else None)
+    aux = B.importance_penalty(out.gates)
+    torch.autograd.backward([out.output, aux], [dy_t, torch.tensor(LAM, device=dev)])
+    torch.cuda.synchronize()
+
+    x = inputs["x"].float().numpy()
+    dy = inputs["dy"].float().numpy()
+    wg = inputs["wg"]
+    r = out.routing
+
+    # ---- (a) logits vs the fp32 oracle, all tokens
+    h_dev = r["logits"].cpu().numpy()
+    h_ref, an_ref = O.router_logits(x, wg, wn_np, z if noise else None)
+    slack = np.abs(x) @ np.abs(wg)
+    if noise:
+        an_dev = r["noise_act"].cpu().numpy()
+        slack_n = np.abs(x) @ np.abs(wn_np)
+        assert np.all(np.abs(an_dev - an_ref) <= 1e-5 * slack_n + 1e-6)
+        slack = slack + np.abs(z) * (O.softplus(an_ref) + slack_n)
+    bad = np.abs(h_dev - h_ref) > 1e-5 * slack + 1e-6
+    assert not bad.any(), (np.argwhere(bad)[:5], h_dev[bad][:5], h_ref[bad][:5])
+
+    # ---- (b) routing, all tokens, bit-exact from the device logits
+    gt = O.gate(h_dev, K, rt)
+    g_dev = out.gates.detach().cpu().numpy()
+    assert g_dev.tobytes() == gt.gates.tobytes(), "gates differ"
+    cap = O.expert_capacity(T, E, cf)
+    disp = O.dispatch(gt.gates, cap, pol)
+    slot_dev = r["slot_rank"].cpu().numpy()
+    assert np.array_equal(slot_dev, disp.rows())
+    assert np.array_equal(out.stats.assigned, disp.assigned)
+    assert out.stats.dropped == disp.n_dropped and out.stats.total_slots == disp.total_slots
+    assert out.stats.capacity == cap
+    mass_ref = (gt.gates * disp.kept).sum(axis=0)
+    assert rel(out.stats.gate_mass, mass_ref) <= 1e-5
+
+    # ---- (d) importance-penalty value and gradient row
+    loss_ref, dimp = O.importance_penalty(gt.gates)
+    assert abs(float(aux) - loss_ref) <= 1e-5 * abs(loss_ref), (float(aux), loss_ref)
+
+    # ---- (c) sampled tokens: y, dx, dh
+    idx = np.sort(O.rng(80, 0).choice(T, 256, replace=False))
+    kept = disp.kept
+    y_ref = np.zeros((idx.size, H), np.float64)
+    dx_ref = np.zeros((idx.size, H), np.float64)
+    dg = np.zeros((idx.size, E), np.float64)
+    wblocks = {}
+    cols = np.sort(O.rng(81, 0).choice(F, 128, replace=False))
+    for e in range(E):
+        w1, w2, w3 = _host_expert(W1, W2, W3, e)
+        rows = np.flatnonzero(kept[idx, e])
+        if rows.size:
+            t = idx[rows]
+            yc, dgc, dxc = O.expert_rows(x[t], dy[t], gt.gates[t, e], w1, w2, w3)
+            y_ref[rows] += yc
+            dg[rows, e] = dgc
+            dx_ref[rows] += dxc
+        allrows = np.flatnonzero(kept[:, e])
+        if allrows.size:
+            wblocks[e] = O.expert_wgrad_columns(x[allrows], dy[allrows], gt.gates[allrows, e],
+                                                w1[:, cols], w3[:, cols], w2[cols, :])
+        del w1, w2, w3
+    dg = dg + LAM * dimp[None, :]
+    dh_ref, dxr, dn_ref = O.router_bwd_rows(h_dev[idx], K, rt, dg, x[idx], wg, wn_np,
+                                            z[idx] if noise else None, an_ref[idx] if noise else None)
+    dx_ref += dxr
+    y_dev = out.output.detach().float().cpu().numpy()
+    assert rel(y_dev[idx], y_ref) < TOL_Y, rel(y_dev[idx], y_ref)
+    full_drop = ~kept.any(axis=1)
+    assert np.all(y_dev[full_drop] == 0.0)
+    dx_dev = x_t.grad.float().cpu().numpy()[idx]
+    assert rel(dx_dev, dx_ref) < TOL_Y, rel(dx_dev, dx_ref)
+    dh_dev = r["dh"].cpu().numpy()
+    assert rel(dh_dev[idx], dh_ref) < TOL_W, rel(dh_dev[idx], dh_ref)
+    # router weight gradients = x^T dh over all tokens, from the device's dh
+    assert rel(wg_t.grad.cpu().numpy(), x.T @ dh_dev) < 1e-4
+    if noise:
+        dn_dev = r["dn"].cpu().numpy()
+        assert rel(dn_dev[idx], dn_ref) < TOL_W
+        assert rel(wn_t.grad.cpu().numpy(), x.T @ dn_dev) < 1e-4
+
+    # ---- (c) expert weight gradients on a block of ffn units, every expert
+    for e in range(E):
+        g1 = W1.grad[e][cols].float().cpu().numpy()        # [|J|, H] = dW1[:, J]^T
+        g3 = W3.grad[e][cols].float().cpu().numpy()
+        g2 = W2.grad[e][:, cols].float().cpu().numpy()     # [H, |J|] = dW2[J, :]^T
+        if e not in wblocks:
+            assert not g1.any() and not g2.any() and not g3.any()
+            continue
+        r1, r3, r2 = wblocks[e]
+        assert rel(g1, r1.T) < TOL_W, (e, "dW1", rel(g1, r1.T))
+        assert rel(g3, r3.T) < TOL_W, (e, "dW3", rel(g3, r3.T))
+        assert rel(g2, r2.T) < TOL_W, (e, "dW2", rel(g2, r2.T))
+    del out, aux, W1, W2, W3, layer
+    torch.cuda.empty_cache()

@@ -86,6 +86,31 @@ def test_moe_checkpoint_bytes_match_reference_and_round_trip(tmp_path):
     assert torch.equal(y0, y1)
 
 
+@pytest.mark.parametrize("case,dt", [("moe_f64", torch.float64), ("moe_f32_raw", torch.float32)])
+def test_full_precision_moe_checkpoint_bytes_and_round_trip(tmp_path, case, dt):
+    """Experts the bf16 stacks cannot hold exactly (f64, unrounded f32): the
+    checkpoint keeps full-precision expert copies and a router in the source
+    dtype, like the reference (upcycle.py:104-112), so the files match its bytes;
+    load -> save reproduces them (the stacks are separate bf16 compute copies)."""
+    import paper_2412_09952_b200 as P
+    from paper_2412_09952_b200.checkpoint import load_checkpoint, save_checkpoint
+    u = CK["upcycle"]
+    dense = P.init_dense(P.ModelConfig(**CK["tiny"]), seed=7, dtype=dt)
+    moe = P.upcycle_full(dense, u["n_experts"], u["top_k"], moe_layers=tuple(u["moe_layers"]),
+                         router_seed=u["router_seed"], capacity_factor=u["capacity_factor"])
+    assert moe.tensors["layers.1.moe.router.wg"].dtype == dt
+    save_checkpoint(moe, str(tmp_path / "m"))
+    assert _dir_case(tmp_path / "m") == CK["cases"][case]
+    with pytest.warns(RuntimeWarning, match="bf16"):
+        back = load_checkpoint(str(tmp_path / "m"))
+    assert P.verify_equivalence(moe, back).equal
+    save_checkpoint(back, str(tmp_path / "b"))
+    assert _dir_case(tmp_path / "b") == CK["cases"][case]
+    x = torch.randn(64, CK["tiny"]["hidden"], device="cuda")
+    assert torch.equal(P.moe_forward(x, moe.layer(1), moe.gate).output,
+                       P.moe_forward(x, back.layer(1), back.gate).output)
+
+
 def test_shards_bytes_match_reference_and_gather(tmp_path):
     import paper_2412_09952_b200 as P
     from paper_2412_09952_b200.checkpoint import load_shard, save_shard
@@ -123,3 +148,51 @@ def test_corrupted_payload_raises_checksum_error(tmp_path):
     with pytest.raises(ChecksumError, match="layers.1.attn.wk"):
         load_checkpoint(str(tmp_path / "a"))
     assert load_checkpoint(str(tmp_path / "a"), verify=False) is not None
+
+
+# --------------------------------------------------------------------------
+# gather_moe integrity errors (reference tests/test_upcycle.py:152-168,
+# behaviour upcycle.py:240-254, 273-283)
+# --------------------------------------------------------------------------
+
+def _tiny_shards(tp, ep):
+    import paper_2412_09952_b200 as P
+    dense = P.init_dense(P.ModelConfig(**CK["tiny"]), seed=7)
+    return [P.upcycle_shard(s, 4, 2, router_seed=5) for s in P.shard_dense(dense, tp, ep)]
+
+
+def test_gather_missing_tile_names_rank():
+    import paper_2412_09952_b200 as P
+    from paper_2412_09952_b200.errors import IntegrityError
+    shards = _tiny_shards(2, 2)
+    with pytest.raises(IntegrityError, match="rank 2"):
+        P.gather_moe([s for s in shards if s.rank != 2])
+
+
+def test_gather_replica_mismatch():
+    import paper_2412_09952_b200 as P
+    from paper_2412_09952_b200.errors import IntegrityError
+    shards = _tiny_shards(1, 2)
+    shards[1].tensors["layers.0.moe.router.wg"].data[0, 0] += 1.0
+    with pytest.raises(IntegrityError, match="replica mismatch"):
+        P.gather_moe(shards)
+
+
+def test_gather_duplicate_rank():
+    import paper_2412_09952_b200 as P
+    from paper_2412_09952_b200.errors import IntegrityError
+    shards = _tiny_shards(1, 2)
+    with pytest.raises(IntegrityError, match="duplicate"):
+        P.gather_moe([shards[0], shards[0]])
+
+
+def test_gather_equals_full_bitwise_grid():
+    """Reference test_upcycle.py:140-148 over tp {1,2} x ep {1,2,4}."""
+    import paper_2412_09952_b200 as P
+    dense = P.init_dense(P.ModelConfig(**CK["tiny"]), seed=7)
+    full = P.upcycle_full(dense, n_experts=4, top_k=2, router_seed=5)
+    for tp in (1, 2):
+        for ep in (1, 2, 4):
+            shards = [P.upcycle_shard(s, n_experts=4, top_k=2, router_seed=5) for s in P.shard_dense(dense, tp, ep)]
+            rep = P.verify_equivalence(full, P.gather_moe(shards))
+            assert rep.equal, (tp, ep, str(rep))

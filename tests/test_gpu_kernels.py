@@ -18,6 +18,17 @@ if torch.cuda.is_available():
 from oracle import moe_oracle as O
 
 
+@pytest.fixture(autouse=True)
+def _reset_gemm_knobs():
+    """Tests below flip the (thread-local) GEMM diagnostics knobs; put the
+    product defaults back after every test, passed or failed."""
+    yield
+    if torch.cuda.is_available():
+        _lib.call("b200moe_gemm_set_cta_group", 2)
+        _lib.call("b200moe_gemm_set_debug", 0)
+        _lib.call("b200moe_gemm_set_max_ctas", 148)
+
+
 def bits_equal(a, b):
     a = np.ascontiguousarray(a)
     b = np.ascontiguousarray(b)

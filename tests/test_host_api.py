@@ -122,3 +122,20 @@ def test_moe_schema_and_dense_schema():
     assert "layers.0.ffn.w1" in s and "layers.1.ffn.w1" not in s
     assert s["layers.1.moe.experts.003.w2"] == (32, 16)
     assert s["layers.1.moe.router.wg"] == (16, 4)
+
+
+def test_routing_stats_reference_constructor_and_properties():
+    """RoutingStats keeps the reference dataclass constructor (moe.py:95-116);
+    the device-backed variant the layer returns is a subclass of it."""
+    import dataclasses
+    from paper_2412_09952_b200 import RoutingStats
+    from paper_2412_09952_b200.moe import DeviceRoutingStats
+    s = RoutingStats(assigned=np.array([3, 1, 0, 0]), dropped=2, total_slots=6,
+                     gate_mass=np.array([1.5, 0.5, 0.0, 0.0], np.float32), capacity=3)
+    assert [f.name for f in dataclasses.fields(RoutingStats)] == ["assigned", "dropped", "total_slots", "gate_mass",
+                                                                   "capacity"]
+    assert s.drop_rate == 2 / 6
+    assert abs(s.load_entropy - float(-(0.75 * np.log(0.75) + 0.25 * np.log(0.25)))) < 1e-15
+    assert RoutingStats(np.zeros(4, np.int64), 0, 0, np.zeros(4), None).drop_rate == 0.0
+    assert RoutingStats(np.zeros(4, np.int64), 0, 0, np.zeros(4), None).load_entropy == 0.0
+    assert issubclass(DeviceRoutingStats, RoutingStats)
