@@ -20,8 +20,8 @@ rule says so:
       dW_g / dW_noise = x^T dh (device dh) <= 1e-4 (fp32 reduction order);
       dW1 / dW3 / dW2 on a sampled block of 128 ffn units of every expert,
       over all of the expert's kept rows, <= 2e-2               tensor.py:192-207;
-  (d) importance-penalty loss value rel <= 1e-5, gate_mass rel <= 1e-5
-                                                                tensor.py:503-521.
+  (d) gate_mass rel <= 1e-5; importance-penalty loss value against fp64
+      within the fp32-summation bound derived in the test       tensor.py:503-521.
 """
 
 import numpy as np
@@ -86,7 +86,7 @@ def _experts(upcycled: bool, seed: int):
 
 def _host_expert(W1, W2, W3, e):
     """Expert e in the reference [in, out] shapes, fp32 (exact bf16 values)."""
-    return (W1[e].t().float().cpu().numpy(), W2[e].t().float().cpu().numpy(), W3[e].t().float().cpu().numpy())
+    return tuple(W[e].detach().t().float().cpu().numpy() for W in (W1, W2, W3))
 
 
 CASES = [
@@ -150,9 +150,20 @@ def test_bench_shape_parity(inputs, rt, pol, cf, noise, upcycled):
     mass_ref = (gt.gates * disp.kept).sum(axis=0)
     assert rel(out.stats.gate_mass, mass_ref) <= 1e-5
 
-    # ---- (d) importance-penalty value and gradient row
+    # ---- (d) importance-penalty value and gradient row.  CV^2 = var/mean^2 of
+    # near-equal per-expert masses is ill-conditioned in the masses: an error
+    # d_e in imp_e moves the loss by dL/dimp_e * d_e.  numpy sums the 8192
+    # fp32 gates per expert sequentially (tensor.py:509), the device in a fixed
+    # tree order, so both are compared with the fp64 value under the bound
+    # sum_e |dL/dimp_e| * 2e-6 * imp_e + 1e-6 * L (2e-6: fp32 summation slack).
     loss_ref, dimp = O.importance_penalty(gt.gates)
-    assert abs(float(aux) - loss_ref) <= 1e-5 * abs(loss_ref), (float(aux), loss_ref)
+    g64 = gt.gates.astype(np.float64)
+    loss64, dimp64 = O.importance_penalty(g64)
+    imp64 = g64.sum(axis=0)
+    bound = float(np.sum(np.abs(dimp64) * 2e-6 * imp64) + 1e-6 * loss64)
+    loss_dev = float(aux.detach())
+    assert abs(loss_dev - loss64) <= bound, (loss_dev, loss64, bound)
+    assert abs(float(loss_ref) - loss64) <= bound, (float(loss_ref), loss64, bound)   # the reference's own slack
 
     # ---- (c) sampled tokens: y, dx, dh
     idx = np.sort(O.rng(80, 0).choice(T, 256, replace=False))
