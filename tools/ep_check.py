@@ -82,6 +82,75 @@ def case(rank, world, dev, T, H, F, router, policy, cf, noise, transport, E=8, k
     return ok
 
 
+def oracle_case(rank, world, dev, T, H, F, router, policy, cf, noise, transport, E=8, k=2, lam=0.1):
+    """EP layer against the CPU ORACLE (oracle/moe_oracle.py, the reference's
+    closed form, moefold/moe.py:250-283) on each rank's own batch: routing
+    bit-exact from the device logits, y / dx within the layer tolerances, and
+    the owned experts' / router gradients against the oracle gradients summed
+    over every rank's batch (rank-local capacity: SURVEY 8(e))."""
+    import numpy as np
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import moe_oracle as O
+    El = E // world
+    g = O.rng(31, 0)
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).float().numpy()  # noqa
+    w1 = [bf(g.standard_normal((H, F)) * 0.05) for _ in range(E)]
+    w2 = [bf(g.standard_normal((F, H)) * 0.05) for _ in range(E)]
+    w3 = [bf(g.standard_normal((H, F)) * 0.05) for _ in range(E)]
+    wg = (g.standard_normal((H, E)) * 0.1).astype(np.float32)
+    wn = (g.standard_normal((H, E)) * 0.05).astype(np.float32)
+    x = bf(O.rng(123, rank).standard_normal((T, H)))
+    dy = bf(O.rng(124, rank).standard_normal((T, H)))
+    z = O.rng(5, rank).standard_normal((T, E)).astype(np.float32)
+    cfg = P.GateConfig(n_experts=E, top_k=k, router_type=router, noise_enabled=noise, capacity_factor=cf,
+                       drop_policy=policy)
+    own = range(rank * El, (rank + 1) * El)
+    stack = lambda ws: torch.stack([torch.from_numpy(ws[e].T.copy()) for e in own]).to(dev, torch.bfloat16)  # noqa
+    lw = [torch.from_numpy(wg).to(dev).requires_grad_(), torch.from_numpy(wn).to(dev).requires_grad_()]
+    lw += [stack(ws).requires_grad_() for ws in (w1, w2, w3)]
+    ep = ExpertParallelMoE(*lw, cfg, transport=transport)
+    xe = torch.from_numpy(x).to(dev, torch.bfloat16).requires_grad_()
+    out = ep(xe, training=True, noise=torch.from_numpy(z).to(dev) if noise else None)
+    aux = P.importance_penalty(out.gates)
+    torch.autograd.backward([out.output, aux], [torch.from_numpy(dy).to(dev, torch.bfloat16),
+                                                torch.tensor(lam, device=dev)])
+    torch.cuda.synchronize()
+
+    logits = out.routing["logits"].cpu().numpy()
+    ocfg = O.LayerCfg(n_experts=E, top_k=k, router_type=router, noise=noise, capacity_factor=cf, drop_policy=policy)
+    y_o, g_o, cache = O.moe_forward(x, wg, wn, w1, w2, w3, ocfg, z=z if noise else None, logits=logits)
+    _, dimp = O.importance_penalty(g_o)
+    gr = O.moe_backward(cache, dy, dgates=lam * dimp)
+    relnp = lambda a, b: float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))  # noqa
+    ok, msgs = True, []
+
+    def check(name, cond):
+        nonlocal ok
+        if not cond:
+            ok = False
+            msgs.append(name)
+
+    check("gates", out.gates.detach().cpu().numpy().tobytes() == g_o.tobytes())
+    check("slot_rank", np.array_equal(out.routing["slot_rank"].cpu().numpy(), cache.disp.rows()))
+    check("assigned", np.array_equal(out.stats.assigned, cache.disp.assigned))
+    check("y", relnp(out.output.detach().float().cpu().numpy(), y_o) < 1.5e-2)
+    check("dx", relnp(xe.grad.float().cpu().numpy(), gr["dx"]) < 1.5e-2)
+    # weight gradients: oracle per rank, summed over ranks (the EP owner sums every source's rows)
+    for i, name in ((2, "dw1"), (3, "dw2"), (4, "dw3")):
+        ref = torch.from_numpy(np.ascontiguousarray(np.stack([gr[name][e].T for e in range(E)]), np.float32)).to(dev)
+        dist.all_reduce(ref)
+        check(name, relnp(lw[i].grad.float().cpu().numpy(), ref[rank * El:(rank + 1) * El].cpu().numpy()) < 2e-2)
+    for i, name in ((0, "dwg"), (1, "dwn")):
+        if name == "dwn" and not noise:
+            continue
+        ref = torch.from_numpy(np.ascontiguousarray(gr[name], np.float32)).to(dev)
+        dist.all_reduce(ref)
+        check(name, relnp(lw[i].grad.cpu().numpy(), ref.cpu().numpy()) < 2e-2)
+    tag = f"[{transport} vs ORACLE] T={T} H={H} F={F} E={E} k={k} {router} {policy} cf={cf} noise={noise}"
+    print(f"rank {rank}: {'PASS' if ok else 'FAIL ' + ','.join(msgs)} {tag}", flush=True)
+    return ok
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -100,6 +169,9 @@ def main():
         # one expert per rank, as EP8 runs E8T2 (E_local = 1: every segment of the local expert GEMMs
         # comes from a different source rank)
         ok &= case(rank, world, dev, 1024, 512, 512, "mixtral", "position", 1.0, False, transport, E=world, k=2)
+        # against the CPU oracle directly (not the single-GPU CUDA layer)
+        ok &= oracle_case(rank, world, dev, 512, 256, 512, "mixtral", "position", 1.0, True, transport)
+        ok &= oracle_case(rank, world, dev, 384, 256, 256, "st", "score", None, False, transport)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     dist.destroy_process_group()
