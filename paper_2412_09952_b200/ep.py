@@ -283,20 +283,33 @@ class _PeerBuffers:
             cls._cache[key] = b
         return b
 
+    GUARD = 4096          # canary bytes before, between and after the planes
+    CANARY = 0xA5
+
     def __init__(self, rows, H, n_counts, grp, device):
         import torch.distributed._symmetric_memory as symm
         self.generation = 0   # bumped by every forward that (re)fills xr / O
+        G = self.GUARD
         plane = rows * H * 2
-        cnt_off = 4 * plane
-        total = cnt_off + ((n_counts * 4 + 255) // 256) * 256
+        offs = [G + i * (plane + G) for i in range(4)]
+        cnt_off = offs[3] + plane + G
+        cnt_bytes = ((n_counts * 4 + 255) // 256) * 256
+        total = cnt_off + cnt_bytes + G
         self.raw = symm.empty(total, dtype=torch.uint8, device=device)
+        self.raw.fill_(self.CANARY)
         self.handle = symm.rendezvous(self.raw, grp.group_name)
-        self.views = [self.raw[i * plane:(i + 1) * plane].view(torch.bfloat16).view(rows, H) for i in range(4)]
+        self.views = [self.raw[o:o + plane].view(torch.bfloat16).view(rows, H) for o in offs]
         self.counts = self.raw[cnt_off:cnt_off + n_counts * 4].view(torch.int32)
+        self._guards = [(0, G)] + [(o + plane, G) for o in offs] + [(cnt_off + cnt_bytes, G)]
         ptrs = list(self.handle.buffer_ptrs)
         mk = lambda off: torch.tensor([p + off for p in ptrs], dtype=torch.int64, device=device)  # noqa: E731
-        self.peer = [mk(i * plane) for i in range(4)]   # xr, O, dO, dxp base pointers on every rank
+        self.peer = [mk(o) for o in offs]   # xr, O, dO, dxp base pointers on every rank
         self.peer_counts = mk(cnt_off)
+
+    def guards_intact(self) -> bool:
+        """True if no kernel (local or a peer's, over NVLink) wrote into the
+        canary bands around this rank's planes (checked by tools/ep_check.py)."""
+        return all(bool((self.raw[o:o + n] == self.CANARY).all()) for o, n in self._guards)
 
     def barrier(self):
         self.handle.barrier(channel=0)

@@ -172,6 +172,14 @@ def main():
         # against the CPU oracle directly (not the single-GPU CUDA layer)
         ok &= oracle_case(rank, world, dev, 512, 256, 512, "mixtral", "position", 1.0, True, transport)
         ok &= oracle_case(rank, world, dev, 384, 256, 256, "st", "score", None, False, transport)
+    # canary bands around every symmetric receive plane (written by peers over NVLink) untouched
+    from paper_2412_09952_b200.ep import _PeerBuffers
+    torch.cuda.synchronize()
+    dist.barrier()
+    guards = all(pb.guards_intact() for pb in _PeerBuffers._cache.values())
+    print(f"rank {rank}: {'PASS' if guards else 'FAIL'} symmetric-buffer guard bands "
+          f"({len(_PeerBuffers._cache)} buffer sets)", flush=True)
+    ok &= guards
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     dist.destroy_process_group()
