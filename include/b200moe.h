@@ -65,7 +65,8 @@ int b200moe_version(void);
  * h = x.W_g (+ z * softplus(x.W_noise) when z != NULL).  gates are bit-exact
  * with numpy float32 given the same logits.  probs (router_type st): full
  * softmax s; may be NULL for mixtral.  noise_act = x.W_noise (needed by the
- * backward; NULL when z == NULL).  workspace: >= 2*H*E floats. */
+ * backward; NULL when z == NULL).  workspace: >= 2*H*E_pad floats; on return
+ * it holds the swizzled W_g (and W_noise) tables b200moe_router_bwd can reuse. */
 int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E,
                        int k, int router_type, float* logits, float* gates, float* probs, float* noise_act,
                        float* workspace, int32_t* err_flag, cudaStream_t stream);
@@ -99,10 +100,18 @@ int b200moe_router_logits_bwd(const void* x, const float* dh, const float* w_g, 
  * (stable, position breaks ties).  Outputs slot_rank [T,E], counts [E]
  * (= RoutingStats.assigned), seg_base [E], gate_mass [E] (sum of kept gates),
  * importance [E] (sum of all gates, the aux-loss input), stats[2] =
- * {dropped, total_slots} (int64).  workspace: >= 64 ints, zeroed once. */
+ * {dropped, total_slots} (int64).  importance_loss (nullable, [1] fp32): the
+ * importance penalty var/mean^2 of `importance` (tensor.py:503-521), with
+ * importance_err (nullable int32) set when mean <= 0.  workspace:
+ * b200moe_dispatch_workspace_words(T) int32 words, zeroed once before first
+ * use (the kernel leaves it reusable; one workspace per stream).
+ * Position policy and dropless run a multi-CTA decoupled look-back scan over
+ * 256-token tiles; score with a capacity selects per expert. */
 int b200moe_dispatch(const float* gates, int T, int E, int capacity, int policy, int layout, int seg_stride,
                      int32_t* slot_rank, int32_t* counts, int32_t* seg_base, float* gate_mass, float* importance,
-                     int64_t* stats, int32_t* workspace, cudaStream_t stream);
+                     int64_t* stats, float* importance_loss, int32_t* importance_err, int32_t* workspace,
+                     cudaStream_t stream);
+size_t b200moe_dispatch_workspace_words(int T);
 
 /* Token permute (K2): xp[seg_base[e] + slot_rank[t,e]] = x[t] for every kept
  * (t,e); pad rows of each segment up to a multiple of 128 are zeroed.
@@ -127,12 +136,15 @@ int b200moe_combine_bwd(const void* dy, const void* o, const float* gates, const
  * dx[t] = sum_{kept e ascending} dxp[row] + dh.W_g^T (+ dn.W_noise^T with
  * dn = dh*z*sigmoid(noise_act)).  Writes dx (bf16), dh, dn (fp32, dn only with
  * noise).  Replaces tensor.py:292-295, 224, 375-378 and moe.py's router matmuls.
+ * wg_swz / wn_swz (nullable): the swizzled W_g / W_noise tables that
+ * b200moe_router_fwd left in the first 2*H*E_pad floats of its workspace
+ * (E_pad = E rounded up to 4/8/16/32); passing them skips re-swizzling.
  * workspace: >= 2*H*32 + T*32 floats. */
 int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
                        const float* dgates_ext, int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates,
                        const float* probs, const float* w_g, const float* w_noise, const float* z,
-                       const float* noise_act, int T, int H, int E, int k, int router_type, void* dx, float* dh,
-                       float* dn, float* workspace, cudaStream_t stream);
+                       const float* noise_act, const float* wg_swz, const float* wn_swz, int T, int H, int E, int k,
+                       int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream);
 
 /* ---- Expert parallelism fused with the exchange (NVLink peer memory) ----
  * The *_peer variants address expert e's rows in the buffer of its owner rank
@@ -156,7 +168,8 @@ int b200moe_combine_bwd_peer(const void* dy, const uint64_t* o_bufs, const float
 int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
                             const int32_t* seg_base, const float* dg, const float* dgates_ext,
                             int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates, const float* probs,
-                            const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T,
+                            const float* w_g, const float* w_noise, const float* z, const float* noise_act,
+                            const float* wg_swz, const float* wn_swz, int T,
                             int H, int E, int k, int router_type, void* dx, float* dh, float* dn, float* workspace,
                             cudaStream_t stream);
 

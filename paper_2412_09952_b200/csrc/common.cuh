@@ -117,6 +117,22 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Importance (CV^2) loss from the per-expert gate masses (tensor.py:509-514):
+// mean, population variance, var / mean^2; err_flag (nullable) set when mean <= 0.
+__device__ __forceinline__ void importance_cv2(const volatile float* imp, int E, float* loss, int32_t* err_flag) {
+    float mean = 0.f;
+    for (int e = 0; e < E; ++e) mean += imp[e];
+    mean /= (float)E;
+    float var = 0.f;
+    for (int e = 0; e < E; ++e) {
+        const float dd = imp[e] - mean;
+        var += dd * dd;
+    }
+    var /= (float)E;
+    if (!(mean > 0.f) && err_flag) atomicExch(err_flag, 1);
+    loss[0] = var / (mean * mean);
+}
+
 // Segment table: where each expert segment of the permuted activation buffer
 // lives.  base[s] = first row, count[s] = valid rows (device), expert[s] =
 // local expert index.  Rows [count, round_up(count,128)) are zero-filled.

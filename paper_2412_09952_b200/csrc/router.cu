@@ -148,7 +148,8 @@ constexpr int kRouterThreads = 512;
 
 template <int EP, bool kNoise, bool kSmemW>
 __global__ void __launch_bounds__(kRouterThreads, 1)
-router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict__ wsw, const float4* __restrict__ wnsw,
+router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ w_g, float4* __restrict__ wsw,
+                  const float4* __restrict__ wnsw,
                   const float* __restrict__ z, int T, int H, int E, int k, int router_type,
                   float* __restrict__ logits, float* __restrict__ gates, float* __restrict__ probs,
                   float* __restrict__ noise_act, int32_t* __restrict__ err_flag) {
@@ -168,17 +169,41 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict_
                                                  : make_uint4(0, 0, 0, 0);
     const float4* W = wsw;
     if constexpr (kSmemW) {
-        // the swizzled W table (H*EP floats) arrives with one bulk async copy
-        // (a float4 load loop here cost ~16 dependent L2 round trips per block)
-        __shared__ uint64_t wbar;
-        if (threadIdx.x == 0) {
-            ptx::mbar_init(&wbar, 1);
-            ptx::fence_mbar_init();
-            ptx::mbar_arrive_expect_tx(&wbar, (uint32_t)(nvec * 16));
-            ptx::bulk_load_1d(smem_w, wsw, (uint32_t)(nvec * 16), &wbar);
+        // Every block swizzles W_g [H, E] straight into shared memory (no
+        // separate swizzle launch): all loads of a thread are issued before any
+        // store, and each block also writes its 1/gridDim slice of the table to
+        // `wsw`, where the router backward reuses it.
+        constexpr int kPer = 8;
+        const int nb = gridDim.x;
+        const int s0 = (int)((long long)nvec * blockIdx.x / nb), s1 = (int)((long long)nvec * (blockIdx.x + 1) / nb);
+        for (int i0 = threadIdx.x; i0 < nvec; i0 += kPer * blockDim.x) {
+            float4 v[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int i = i0 + u * blockDim.x;
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (i < nvec) {
+                    const int hb = i % HB, rest = i / HB, e4 = rest % (EP / 4), j = rest / (EP / 4);
+                    const float* src = w_g + (size_t)(hb * 8 + j) * E + e4 * 4;
+                    if (E % 4 == 0) v[u] = __ldg(reinterpret_cast<const float4*>(src));
+                    else {
+                        float t[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) t[c] = (e4 * 4 + c < E) ? __ldg(src + c) : 0.f;
+                        v[u] = make_float4(t[0], t[1], t[2], t[3]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < nvec) {
+                    smem_w[i] = v[u];
+                    if (i >= s0 && i < s1) wsw[i] = v[u];
+                }
+            }
         }
         __syncthreads();
-        ptx::mbar_wait(&wbar, 0);
         W = smem_w;
     }
 
@@ -514,6 +539,203 @@ dispatch_kernel(const float* __restrict__ gates, int T, int E, int capacity, int
     }
 }
 
+__global__ void importance_loss_kernel_fwd(const float* __restrict__ imp, int E, float* __restrict__ loss,
+                                           int32_t* __restrict__ err_flag) {
+    if (threadIdx.x == 0) importance_cv2(imp, E, loss, err_flag);
+}
+
+// ---------------------------------------------------------------- K1b fast path
+// Position policy (and dropless): a kept slot's rank is its index among the
+// expert's slots in token order, so capacity needs only a prefix count over
+// tokens.  One CTA per 256-token tile (tile ids taken from an atomic counter,
+// so tiles start in order): each thread holds one token's row of gates
+// (coalesced), a block scan gives in-tile slot ranks for all experts at once
+// (four 16-bit counters per 64-bit word), and a decoupled look-back over the
+// tiles' published per-expert aggregates / inclusive prefixes gives the
+// cross-tile offset.  Per-tile sums of gates (importance) and kept gates
+// (gate mass) are reduced in fixed tile order by the last CTA, which also
+// writes counts, seg_base, drop stats and the importance (CV^2) loss.
+// Workspace (int32 words, zero-initialised once): [0] ticket, [1] tile counter,
+// [2] epoch, [8..8+40) per-expert slot totals, then status words (uint64,
+// [tile][EP]) and per-tile partial sums (float2, [tile][EP]).
+constexpr int kScanTile = 256;
+constexpr int kWsStatus = 64;   // int32 offset of the status words (8-byte aligned)
+
+__host__ __device__ constexpr size_t dispatch_ws_words(int T) {
+    return (size_t)kWsStatus + (size_t)((T + kScanTile - 1) / kScanTile) * kMaxE * 4;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+template <int EP>
+__global__ void __launch_bounds__(kScanTile)
+dispatch_scan_kernel(const float* __restrict__ gates, int T, int E, int capacity, int layout, int seg_stride,
+                     int32_t* __restrict__ slot_rank, int32_t* __restrict__ counts, int32_t* __restrict__ seg_base,
+                     float* __restrict__ gate_mass, float* __restrict__ importance, int64_t* __restrict__ stats,
+                     float* __restrict__ imp_loss, int32_t* __restrict__ imp_err, int32_t* __restrict__ ws) {
+    constexpr int NW = EP / 4;                      // 64-bit words of four 16-bit counters
+    constexpr int kWarps = kScanTile / 32;
+    __shared__ unsigned long long wsum[kWarps][NW];
+    __shared__ int excl_sh[EP];
+    __shared__ float red_sh[2][kWarps][EP];
+    __shared__ int tile_sh;
+    __shared__ bool last_sh;
+    const int ntiles = (T + kScanTile - 1) / kScanTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + kWsStatus);
+    float2* part = reinterpret_cast<float2*>(status + (size_t)ntiles * EP);
+    if (threadIdx.x == 0) tile_sh = atomicAdd(&ws[1], 1);
+    __syncthreads();
+    const int tile = tile_sh;
+    const unsigned epoch = ((volatile unsigned*)ws)[2];
+    const int t = tile * kScanTile + threadIdx.x;
+    const bool dropless = capacity < 0;
+
+    // ---- this token's gates (E contiguous floats) and slot flags
+    float g[EP];
+#pragma unroll
+    for (int e = 0; e < EP; ++e) g[e] = 0.f;
+    if (t < T) {
+        if (E == EP) {
+#pragma unroll
+            for (int q = 0; q < EP / 4; ++q) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(gates + (size_t)t * E) + q);
+                g[4 * q] = v.x; g[4 * q + 1] = v.y; g[4 * q + 2] = v.z; g[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < EP; ++e) g[e] = (e < E) ? __ldg(gates + (size_t)t * E + e) : 0.f;
+        }
+    }
+    unsigned long long f[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        f[w] = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) f[w] |= (unsigned long long)(g[4 * w + c] > 0.f) << (16 * c);
+    }
+    // ---- block exclusive scan of the packed counters
+    unsigned long long inc[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        inc[w] = f[w];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long n = __shfl_up_sync(0xffffffffu, inc[w], o);
+            if (lane >= o) inc[w] += n;
+        }
+        if (lane == 31) wsum[warp][w] = inc[w];
+    }
+    __syncthreads();
+    unsigned long long pre[NW], tot[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        pre[w] = 0;
+        tot[w] = 0;
+        for (int i = 0; i < kWarps; ++i) {
+            if (i < warp) pre[w] += wsum[i][w];
+            tot[w] += wsum[i][w];
+        }
+        pre[w] += inc[w] - f[w];
+    }
+    // ---- decoupled look-back, one thread per expert: flag 1 = aggregate, 2 = inclusive prefix
+    if (threadIdx.x < E) {
+        const int e = threadIdx.x;
+        const unsigned long long agg = (tot[e >> 2] >> (16 * (e & 3))) & 0xFFFFull;
+        const unsigned long long tag = (unsigned long long)epoch << 34;
+        unsigned long long* my = status + (size_t)tile * EP + e;
+        long long excl = 0;
+        if (tile == 0) {
+            st_release_u64(my, tag | (2ull << 32) | agg);
+        } else {
+            st_release_u64(my, tag | (1ull << 32) | agg);
+            for (int j = tile - 1; j >= 0; --j) {
+                unsigned long long v;
+                do {
+                    v = ld_acquire_u64(status + (size_t)j * EP + e);
+                } while ((v >> 34) != (unsigned long long)epoch || ((v >> 32) & 3ull) == 0);
+                excl += (long long)(v & 0xFFFFFFFFull);
+                if (((v >> 32) & 3ull) == 2) break;
+            }
+            st_release_u64(my, tag | (2ull << 32) | (unsigned long long)(excl + (long long)agg));
+        }
+        excl_sh[e] = (int)excl;
+        if (tile == ntiles - 1) ws[8 + e] = (int)(excl + (long long)agg);   // total slots of expert e
+    }
+    __syncthreads();
+    // ---- ranks, kept flags, per-thread sums
+    float imp_e[EP], mass_e[EP];
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+        const int r = excl_sh[e < E ? e : 0] + (int)((pre[e >> 2] >> (16 * (e & 3))) & 0xFFFFull);
+        const bool slot = g[e] > 0.f;
+        const bool kept = slot && (dropless || r < capacity);
+        if (t < T && e < E) slot_rank[(size_t)t * E + e] = kept ? r : -1;
+        imp_e[e] = g[e];
+        mass_e[e] = kept ? g[e] : 0.f;
+    }
+    // fixed-order block sums: warp butterflies, then warps in order (thread e < E)
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+        const float a = warp_sum(imp_e[e]), b = warp_sum(mass_e[e]);
+        if (lane == 0) { red_sh[0][warp][e] = a; red_sh[1][warp][e] = b; }
+    }
+    __syncthreads();
+    if (threadIdx.x < E) {
+        const int e = threadIdx.x;
+        float a = 0.f, b = 0.f;
+        for (int i = 0; i < kWarps; ++i) { a += red_sh[0][i][e]; b += red_sh[1][i][e]; }
+        part[(size_t)tile * EP + e] = make_float2(a, b);
+    }
+    // ---- last CTA: fixed-order reduction over tiles, counts, stats, seg_base, loss
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last_sh = (atomicAdd(&ws[0], 1) == ntiles - 1);
+    __syncthreads();
+    if (!last_sh) return;
+    __threadfence();
+    if (threadIdx.x < E) {
+        const int e = threadIdx.x;
+        float a = 0.f, b = 0.f;
+        const volatile float2* vp = part;
+        for (int j = 0; j < ntiles; ++j) {
+            a += vp[(size_t)j * EP + e].x;
+            b += vp[(size_t)j * EP + e].y;
+        }
+        importance[e] = a;
+        gate_mass[e] = b;
+        const int tot_e = ((volatile int32_t*)ws)[8 + e];
+        counts[e] = dropless ? tot_e : min(tot_e, capacity);
+    }
+    __syncthreads();
+    __threadfence();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        long long dropped = 0, total = 0;
+        for (int i = 0; i < E; ++i) {
+            const int c = ((volatile int32_t*)counts)[i];
+            const int s = ((volatile int32_t*)ws)[8 + i];
+            seg_base[i] = (layout == B200MOE_LAYOUT_FIXED) ? i * seg_stride : acc;
+            acc += round_up(c, kSegPad);
+            dropped += s - c;
+            total += s;
+        }
+        stats[0] = dropped;
+        stats[1] = total;
+        if (imp_loss) importance_cv2(importance, E, imp_loss, imp_err);
+        ws[0] = 0;          // ticket
+        ws[1] = 0;          // tile counter
+        ws[2] = (int)((epoch + 1) & 0x3FFFFFFFu);
+    }
+}
+
 }  // namespace b200moe
 
 using namespace b200moe;
@@ -525,11 +747,11 @@ int router_fwd_impl(const void* x, const float* w_g, const float* w_noise, const
                     float* workspace, int32_t* err_flag, cudaStream_t stream) {
     float4* wsw = reinterpret_cast<float4*>(workspace);
     float4* wnsw = reinterpret_cast<float4*>(workspace + (size_t)H * EP);
-    swizzle_w_kernel<EP><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
+    const size_t wbytes = (size_t)H * EP * sizeof(float);
+    const bool smem_w = wbytes <= 160 * 1024;   // else the kernel reads the table from L2
+    if (!smem_w) swizzle_w_kernel<EP><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
     const bool noise = z != nullptr;
     if (noise) swizzle_w_kernel<EP><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
-    const size_t wbytes = (size_t)H * EP * sizeof(float);
-    const bool smem_w = wbytes <= 160 * 1024;
     constexpr int TT = 32 / EP;
     const int warps_needed = ceil_div(T, TT);
     int grid = ceil_div(warps_needed, kRouterThreads / 32);
@@ -540,7 +762,7 @@ int router_fwd_impl(const void* x, const float* w_g, const float* w_noise, const
         auto kern = router_fwd_kernel<EP, NZ, SM>;                                                            \
         const size_t sh = SM ? wbytes : 0;                                                                    \
         if (SM) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);             \
-        kern<<<grid, kRouterThreads, sh, stream>>>((const __nv_bfloat16*)x, wsw, wnsw, z, T, H, E, k,         \
+        kern<<<grid, kRouterThreads, sh, stream>>>((const __nv_bfloat16*)x, w_g, wsw, wnsw, z, T, H, E, k,    \
                                                    router_type, logits, gates, probs, noise_act, err_flag);   \
     } while (0)
     if (noise) {
@@ -601,17 +823,37 @@ int b200moe_gate_from_logits(const float* logits, int T, int E, int k, int route
     return gate_impl<32>(logits, T, E, k, router_type, gates, probs, topk_mask, err_flag, stream);
 }
 
+size_t b200moe_dispatch_workspace_words(int T) { return dispatch_ws_words(T < 1 ? 1 : T); }
+
 int b200moe_dispatch(const float* gates, int T, int E, int capacity, int policy, int layout, int seg_stride,
                      int32_t* slot_rank, int32_t* counts, int32_t* seg_base, float* gate_mass, float* importance,
-                     int64_t* stats, int32_t* workspace, cudaStream_t stream) {
+                     int64_t* stats, float* importance_loss, int32_t* importance_err, int32_t* workspace,
+                     cudaStream_t stream) {
     B200_CHECK_ARG(T >= 1, B200MOE_ERR_CONFIG, "tokens_per_batch must be >= 1, got %d", T);
     B200_CHECK_ARG(E >= 1 && E <= kMaxE, B200MOE_ERR_CONFIG, "n_experts %d", E);
     B200_CHECK_ARG(policy == B200MOE_POLICY_POSITION || policy == B200MOE_POLICY_SCORE, B200MOE_ERR_CONFIG,
                    "drop_policy must be one of ('position', 'score')");
     B200_CHECK_ARG(layout == B200MOE_LAYOUT_COMPACT || (layout == B200MOE_LAYOUT_FIXED && seg_stride % kSegPad == 0),
                    B200MOE_ERR_CONFIG, "fixed layout needs a segment stride multiple of %d", kSegPad);
-    dispatch_kernel<<<E, kDispThreads, 0, stream>>>(gates, T, E, capacity, policy, layout, seg_stride, slot_rank,
-                                                    counts, seg_base, gate_mass, importance, stats, workspace);
+    if (policy == B200MOE_POLICY_POSITION || capacity < 0) {
+        const int ntiles = ceil_div(T, kScanTile);
+#define SCAN(EP) dispatch_scan_kernel<EP><<<ntiles, kScanTile, 0, stream>>>(                                     \
+        gates, T, E, capacity, layout, seg_stride, slot_rank, counts, seg_base, gate_mass, importance, stats,     \
+        importance_loss, importance_err, workspace)
+        if (E <= 4) SCAN(4);
+        else if (E <= 8) SCAN(8);
+        else if (E <= 16) SCAN(16);
+        else SCAN(32);
+#undef SCAN
+        B200_CHECK_LAUNCH("dispatch");
+        return B200MOE_OK;
+    }
+    // score policy with a capacity: per-expert radix select (one CTA per expert)
+    dispatch_kernel<<<E, kDispThreads, 0, stream>>>(gates, T, E, capacity, B200MOE_POLICY_SCORE, layout, seg_stride,
+                                                    slot_rank, counts, seg_base, gate_mass, importance, stats,
+                                                    workspace);
+    if (importance_loss) importance_loss_kernel_fwd<<<1, 32, 0, stream>>>(importance, E, importance_loss,
+                                                                          importance_err);
     B200_CHECK_LAUNCH("dispatch");
     return B200MOE_OK;
 }

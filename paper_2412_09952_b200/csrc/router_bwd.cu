@@ -444,17 +444,7 @@ __global__ void reduce_partials(const float* __restrict__ part, int nchunks, siz
 __global__ void importance_loss_kernel(const float* __restrict__ imp, int E, float* __restrict__ loss,
                                        int32_t* __restrict__ err_flag) {
     if (threadIdx.x != 0) return;
-    float mean = 0.f;
-    for (int e = 0; e < E; ++e) mean += imp[e];
-    mean /= (float)E;
-    float var = 0.f;
-    for (int e = 0; e < E; ++e) {
-        const float dd = imp[e] - mean;
-        var += dd * dd;
-    }
-    var /= (float)E;
-    if (!(mean > 0.f)) atomicExch(err_flag, 1);
-    loss[0] = var / (mean * mean);
+    importance_cv2(imp, E, loss, err_flag);
 }
 
 // Importance penalty forward: one block of 1024 threads; thread i sums the
@@ -532,15 +522,22 @@ template <int EP, int KM>
 int router_bwd_impl(const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
                     const int32_t* seg_base, const float* dg,
                     const float* dgx, int64_t sx_t, int64_t sx_e, const float* gates, const float* probs,
-                    const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T, int H,
+                    const float* w_g, const float* w_noise, const float* z, const float* noise_act,
+                    const float* wg_swz, const float* wn_swz, int T, int H,
                     int E, int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
-    // workspace: swizzled W_g [H*EP], W_noise [H*EP], rows [T*KM] (int32)
+    // workspace: swizzled W_g [H*EP], W_noise [H*EP], rows [T*KM] (int32).  The
+    // router forward leaves the same swizzled tables in its workspace; when
+    // they are passed in (wg_swz / wn_swz) the swizzle launches are skipped.
     float4* wsw = reinterpret_cast<float4*>(workspace);
     float4* wnsw = reinterpret_cast<float4*>(workspace + (size_t)H * EP);
     int32_t* rows = reinterpret_cast<int32_t*>(workspace + (size_t)2 * H * EP);
     const bool noise = z != nullptr;
-    swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
-    if (noise) swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
+    if (wg_swz) wsw = reinterpret_cast<float4*>(const_cast<float*>(wg_swz));
+    else swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_g, H, E, wsw);
+    if (noise) {
+        if (wn_swz) wnsw = reinterpret_cast<float4*>(const_cast<float*>(wn_swz));
+        else swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
+    }
     router_dh_kernel<EP, KM><<<ceil_div(T, 256), 256, 0, stream>>>(slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates,
                                                                     probs, z, noise_act, T, E, router_type, dh,
                                                                     noise ? dn : nullptr, rows, e_per_rank);
@@ -562,11 +559,12 @@ template <int EP>
 int router_bwd_k(int k, const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
                  const int32_t* seg_base, const float* dg,
                  const float* dgx, int64_t sx_t, int64_t sx_e, const float* gates, const float* probs,
-                 const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T, int H, int E,
+                 const float* w_g, const float* w_noise, const float* z, const float* noise_act, const float* wg_swz,
+                 const float* wn_swz, int T, int H, int E,
                  int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
 #define CALL(KM) router_bwd_impl<EP, KM>(dxp, dxp_bufs, e_per_rank, slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates, \
-                                         probs, w_g, w_noise, z, noise_act, T, H, E, router_type, dx, dh, dn,        \
-                                         workspace, stream)
+                                         probs, w_g, w_noise, z, noise_act, wg_swz, wn_swz, T, H, E, router_type, dx, \
+                                         dh, dn, workspace, stream)
     if (k <= 2) return CALL(2);
     if (k <= 4 || EP == 4) return CALL((EP < 4 ? EP : 4));
     return CALL(EP);
@@ -641,7 +639,8 @@ extern "C" {
 static int router_bwd_any(const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
                           const int32_t* seg_base, const float* dg, const float* dgates_ext, int64_t dgates_stride_t,
                           int64_t dgates_stride_e, const float* gates, const float* probs, const float* w_g,
-                          const float* w_noise, const float* z, const float* noise_act, int T, int H, int E, int k,
+                          const float* w_noise, const float* z, const float* noise_act, const float* wg_swz,
+                          const float* wn_swz, int T, int H, int E, int k,
                           int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
     B200_CHECK_ARG(T >= 1 && E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "bad T/E (%d, %d)", T, E);
     B200_CHECK_ARG(k >= 1 && k <= E, B200MOE_ERR_CONFIG, "top-k out of range: k=%d, n=%d", k, E);
@@ -651,8 +650,8 @@ static int router_bwd_any(const void* dxp, const uint64_t* dxp_bufs, int e_per_r
     B200_CHECK_ARG(e_per_rank >= 1 && E % e_per_rank == 0 && E / e_per_rank <= 32, B200MOE_ERR_CONFIG,
                    "experts per rank %d does not divide %d", e_per_rank, E);
 #define CALL(EP) router_bwd_k<EP>(k, dxp, dxp_bufs, e_per_rank, slot_rank, seg_base, dg, dgates_ext,              \
-                                  dgates_stride_t, dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, T, H, \
-                                  E, router_type, dx, dh, dn, workspace, stream)
+                                  dgates_stride_t, dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, wg_swz, \
+                                  wn_swz, T, H, E, router_type, dx, dh, dn, workspace, stream)
     if (E <= 4) return CALL(4);
     if (E <= 8) return CALL(8);
     if (E <= 16) return CALL(16);
@@ -663,23 +662,24 @@ static int router_bwd_any(const void* dxp, const uint64_t* dxp_bufs, int e_per_r
 int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t* seg_base, const float* dg,
                        const float* dgates_ext, int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates,
                        const float* probs, const float* w_g, const float* w_noise, const float* z,
-                       const float* noise_act, int T, int H, int E, int k, int router_type, void* dx, float* dh,
-                       float* dn, float* workspace, cudaStream_t stream) {
+                       const float* noise_act, const float* wg_swz, const float* wn_swz, int T, int H, int E, int k,
+                       int router_type, void* dx, float* dh, float* dn, float* workspace, cudaStream_t stream) {
     return router_bwd_any(dxp, nullptr, E, slot_rank, seg_base, dg, dgates_ext, dgates_stride_t, dgates_stride_e,
-                          gates, probs, w_g, w_noise, z, noise_act, T, H, E, k, router_type, dx, dh, dn, workspace,
-                          stream);
+                          gates, probs, w_g, w_noise, z, noise_act, wg_swz, wn_swz, T, H, E, k, router_type, dx, dh,
+                          dn, workspace, stream);
 }
 
 int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
                             const int32_t* seg_base, const float* dg, const float* dgates_ext,
                             int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates, const float* probs,
-                            const float* w_g, const float* w_noise, const float* z, const float* noise_act, int T,
+                            const float* w_g, const float* w_noise, const float* z, const float* noise_act,
+                            const float* wg_swz, const float* wn_swz, int T,
                             int H, int E, int k, int router_type, void* dx, float* dh, float* dn, float* workspace,
                             cudaStream_t stream) {
     B200_CHECK_ARG(dxp_bufs != nullptr, B200MOE_ERR_CONFIG, "peer buffers required");
     return router_bwd_any(nullptr, dxp_bufs, e_per_rank, slot_rank, seg_base, dg, dgates_ext, dgates_stride_t,
-                          dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, T, H, E, k, router_type, dx, dh,
-                          dn, workspace, stream);
+                          dgates_stride_e, gates, probs, w_g, w_noise, z, noise_act, wg_swz, wn_swz, T, H, E, k,
+                          router_type, dx, dh, dn, workspace, stream);
 }
 
 int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T, int H, int E, float* dw_g,

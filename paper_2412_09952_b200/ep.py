@@ -34,7 +34,7 @@ import torch.distributed as dist
 from . import _lib
 from .errors import ConfigError, ShapeError
 from .moe import (DeviceRoutingStats, GateConfig, SEG_PAD, _acc_targets, _arange_i32, _dispatch_ws, _ep, _noise,
-                  _wgrad_call, _wgrad_outputs, expert_capacity)
+                  _swizzled, _wgrad_call, _wgrad_outputs, expert_capacity)
 
 
 @dataclass
@@ -153,7 +153,8 @@ class _EPFunction(torch.autograd.Function):
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
         err = torch.zeros(1, dtype=torch.int32, device=dev)
-        ws = torch.empty(2 * H * _ep(E), **f32)
+        ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
+        ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
                   cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),
                   ws.data_ptr(), err.data_ptr(), s)
@@ -162,11 +163,12 @@ class _EPFunction(torch.autograd.Function):
         seg_base = torch.empty(E, dtype=torch.int32, device=dev)
         gate_mass = torch.empty(E, **f32)
         imp = torch.empty(E, **f32)
+        imp_loss = torch.empty(1, **f32)
         stats = torch.empty(2, dtype=torch.int64, device=dev)
         _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if plan.capacity is None else plan.capacity,
                   _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_COMPACT, 0, slot_rank.data_ptr(),
                   counts.data_ptr(), seg_base.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),
-                  _dispatch_ws(dev).data_ptr(), s)
+                  imp_loss.data_ptr(), None, _dispatch_ws(dev, T).data_ptr(), s)
         # exact splits: the compact layout keeps each destination's experts
         # contiguous; one host round trip fetches both count vectors
         rcounts = plan.exchange_counts(counts, group)
@@ -191,7 +193,8 @@ class _EPFunction(torch.autograd.Function):
         _lib.call("b200moe_combine", Os.data_ptr(), gates.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), T,
                   H, E, y.data_ptr(), s)
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_base,
-                             gate_mass=gate_mass, importance=imp, stats=stats, err=err, recv_counts=rcounts)
+                             gate_mass=gate_mass, importance=imp, importance_loss=imp_loss, stats=stats, err=err,
+                             recv_counts=rcounts)
         ctx.st = st
         ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.splits = sp
@@ -248,7 +251,8 @@ class _EPFunction(torch.autograd.Function):
         ws = torch.empty(2 * H * _ep(E) + T * _ep(E), **f32)
         _lib.call("b200moe_router_bwd", dxs.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), dg.data_ptr(),
                   _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(), w_noise.data_ptr(),
-                  _lib.ptr(z), _lib.ptr(noise_act), T, H, E, cfg.top_k, _lib.ROUTER[cfg.router_type],
+                  _lib.ptr(z), _lib.ptr(noise_act), *_swizzled(ctx, H, E, z), T, H, E, cfg.top_k,
+                  _lib.ROUTER[cfg.router_type],
                   dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
         dwg = torch.empty(H, E, **f32)
         dwn = torch.empty(H, E, **f32) if z is not None else None
@@ -355,7 +359,8 @@ class _EPPeerFunction(torch.autograd.Function):
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
         err = torch.zeros(1, dtype=torch.int32, device=dev)
-        ws = torch.empty(2 * H * _ep(E), **f32)
+        ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
+        ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
                   cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),
                   ws.data_ptr(), err.data_ptr(), s)
@@ -364,11 +369,12 @@ class _EPPeerFunction(torch.autograd.Function):
         seg_local = torch.empty(E, dtype=torch.int32, device=dev)
         gate_mass = torch.empty(E, **f32)
         imp = torch.empty(E, **f32)
+        imp_loss = torch.empty(1, **f32)
         stats = torch.empty(2, dtype=torch.int64, device=dev)
         _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if plan.capacity is None else plan.capacity,
                   _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_FIXED, plan.cap_pad, slot_rank.data_ptr(),
                   counts.data_ptr(), seg_local.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),
-                  _dispatch_ws(dev).data_ptr(), s)
+                  imp_loss.data_ptr(), None, _dispatch_ws(dev, T).data_ptr(), s)
         seg_peer = plan.peer_seg_base(dev)      # row of (this rank, expert e) in e's owner buffer
         pb.barrier()                            # every rank is done with the previous use of the buffers
         pb.generation += 1
@@ -390,7 +396,8 @@ class _EPPeerFunction(torch.autograd.Function):
         _lib.call("b200moe_combine_peer", pb.peer[1].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
                   seg_peer.data_ptr(), T, H, E, y.data_ptr(), s)
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_peer,
-                             gate_mass=gate_mass, importance=imp, stats=stats, err=err, recv_counts=rcounts.clone())
+                             gate_mass=gate_mass, importance=imp, importance_loss=imp_loss, stats=stats, err=err,
+                             recv_counts=rcounts.clone())
         ctx.st = st
         ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.pb = pb
@@ -453,8 +460,8 @@ class _EPPeerFunction(torch.autograd.Function):
         ws = torch.empty(2 * H * _ep(E) + T * _ep(E), **f32)
         _lib.call("b200moe_router_bwd_peer", pb.peer[3].data_ptr(), El, slot_rank.data_ptr(), seg_peer.data_ptr(),
                   dg.data_ptr(), _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(),
-                  w_noise.data_ptr(), _lib.ptr(z), _lib.ptr(noise_act), T, H, E, cfg.top_k,
-                  _lib.ROUTER[cfg.router_type], dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
+                  w_noise.data_ptr(), _lib.ptr(z), _lib.ptr(noise_act), *_swizzled(ctx, H, E, z), T, H, E,
+                  cfg.top_k, _lib.ROUTER[cfg.router_type], dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
         dwg = torch.empty(H, E, **f32)
         dwn = torch.empty(H, E, **f32) if z is not None else None
         wsw = torch.empty((T + 63) // 64 * H * E, **f32)
@@ -526,7 +533,7 @@ class ExpertParallelMoE:
                             self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)
         r = st["routing"]
         from .moe import MoEForwardResult
-        gates._b200_importance = (r["importance"], gates._version)
+        gates._b200_importance = (r["importance"], gates._version, r["importance_loss"])
         out = MoEForwardResult(output=y, stats=DeviceRoutingStats(r["counts"], r["stats"], r["gate_mass"], plan.capacity,
                                                             r["err"]), gates=gates)
         out.routing = r

@@ -280,11 +280,15 @@ def _ep(E: int) -> int:
     return 4 if E <= 4 else 8 if E <= 8 else 16 if E <= 16 else 32
 
 
-def _dispatch_ws(device) -> torch.Tensor:
+def _dispatch_ws(device, T: int) -> torch.Tensor:
+    """The dispatch kernel's reusable workspace (ticket, tile counter, epoch,
+    look-back status words): zeroed once, one per (device, stream), grown for
+    larger T (a fresh zeroed buffer)."""
     key = ("disp_ws", device, torch.cuda.current_stream(device).cuda_stream)
+    need = int(_lib.load().b200moe_dispatch_workspace_words(int(T)))
     ws = _CACHE.get(key)
-    if ws is None:
-        ws = torch.zeros(64, dtype=torch.int32, device=device)
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(need, dtype=torch.int32, device=device)
         _CACHE[key] = ws
     return ws
 
@@ -490,11 +494,12 @@ def _run_dispatch(gates: torch.Tensor, capacity: int | None, drop_policy: str, l
     gate_mass = torch.empty(E, dtype=torch.float32, device=dev)
     imp = torch.empty(E, dtype=torch.float32, device=dev)
     stats = torch.empty(2, dtype=torch.int64, device=dev)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)     # importance penalty of these gates
     _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if capacity is None else int(capacity),
               _lib.POLICY[drop_policy], layout, seg_stride, slot_rank.data_ptr(), counts.data_ptr(),
-              seg_base.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),
-              _dispatch_ws(dev).data_ptr(), _lib.stream_ptr())
-    return slot_rank, counts, seg_base, gate_mass, imp, stats
+              seg_base.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(), loss.data_ptr(), None,
+              _dispatch_ws(dev, T).data_ptr(), _lib.stream_ptr())
+    return slot_rank, counts, seg_base, gate_mass, (imp, loss), stats
 
 
 def dispatch(gates, capacity: int | None, drop_policy: str = "position") -> DispatchResult:
@@ -502,7 +507,7 @@ def dispatch(gates, capacity: int | None, drop_policy: str = "position") -> Disp
     if drop_policy not in DROP_POLICIES:
         raise ConfigError(f"drop_policy must be one of {DROP_POLICIES}, got {drop_policy!r}")
     g = _as_logits(gates)
-    slot_rank, counts, seg_base, gate_mass, imp, stats = _run_dispatch(g, capacity, drop_policy)
+    slot_rank, counts, seg_base, gate_mass, _, stats = _run_dispatch(g, capacity, drop_policy)
     kept = slot_rank >= 0
     dropped = (g > 0) & ~kept
     return DispatchResult(kept=kept, dropped=dropped,
@@ -591,12 +596,13 @@ class _MoEFunction(torch.autograd.Function):
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
         err = torch.zeros(1, dtype=torch.int32, device=dev)
-        ws = torch.empty(2 * H * _ep(E), **f32)
+        ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
+        ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E, k,
                   rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act), ws.data_ptr(),
                   err.data_ptr(), s)
         cap = expert_capacity(T, E, cfg.capacity_factor)
-        slot_rank, counts, seg_base, gate_mass, imp, stats = _run_dispatch(gates, cap, cfg.drop_policy)
+        slot_rank, counts, seg_base, gate_mass, (imp, imp_loss), stats = _run_dispatch(gates, cap, cfg.drop_policy)
         R = _rows_bound(T, E, k, cap)
         seg_e = _arange_i32(E, dev)
         xp = torch.empty(R, H, **bf)
@@ -615,7 +621,8 @@ class _MoEFunction(torch.autograd.Function):
                   H, E, y.data_ptr(), s)
 
         st.routing = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_base,
-                          gate_mass=gate_mass, importance=imp, stats=stats, err=err, capacity=cap, rows=R,
+                          gate_mass=gate_mass, importance=imp, importance_loss=imp_loss, stats=stats, err=err,
+                          capacity=cap, rows=R,
                           noise_act=noise_act)
         ctx.st = st
         ctx.acc_targets = _acc_targets(W1, W2, W3)
@@ -670,7 +677,8 @@ class _MoEFunction(torch.autograd.Function):
         ws = torch.empty(2 * H * _ep(E) + T * _ep(E), **f32)
         _lib.call("b200moe_router_bwd", dxp.data_ptr(), slot_rank.data_ptr(), seg_base.data_ptr(), dg.data_ptr(),
                   _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(), w_noise.data_ptr(),
-                  _lib.ptr(z), _lib.ptr(noise_act), T, H, E, cfg.top_k, _lib.ROUTER[cfg.router_type],
+                  _lib.ptr(z), _lib.ptr(noise_act), *_swizzled(ctx, H, E, z), T, H, E, cfg.top_k,
+                  _lib.ROUTER[cfg.router_type],
                   dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
         dwg = torch.empty(H, E, **f32)
         dwn = torch.empty(H, E, **f32) if z is not None else None
@@ -680,6 +688,15 @@ class _MoEFunction(torch.autograd.Function):
         if st.routing is not None:   # router-logit gradients, for inspection (out.routing["dh"])
             st.routing["dh"], st.routing["dn"] = dh, dn
         return dx, dwg, dwn, dW1, dW2, dW3, None, None
+
+
+def _swizzled(ctx, H: int, E: int, z):
+    """Device pointers of the swizzled W_g / W_noise tables the router forward
+    left in its workspace (ctx.router_ws), for b200moe_router_bwd."""
+    ws = getattr(ctx, "router_ws", None)
+    if ws is None:
+        return None, None
+    return ws.data_ptr(), (ws.data_ptr() + H * _ep(E) * 4 if z is not None else None)
 
 
 def _pad_to(n: int, a: int) -> int:
@@ -724,7 +741,7 @@ def moe_forward(x: torch.Tensor, layer: MoELayer, cfg: GateConfig, rng: Rng | No
     if Hp != H:
         y = y[:, :H]
     r = st.routing
-    gates._b200_importance = (r["importance"], gates._version)
+    gates._b200_importance = (r["importance"], gates._version, r["importance_loss"])
     stats = DeviceRoutingStats(r["counts"], r["stats"], r["gate_mass"], r["capacity"], r["err"])
     out = MoEForwardResult(output=y, stats=stats, gates=gates)
     out.routing = r  # device-side routing tensors (slot_rank, counts, logits, ...) for inspection
@@ -751,10 +768,14 @@ class _ImportanceFunction(torch.autograd.Function):
         err = torch.zeros(1, dtype=torch.int32, device=gates.device)
         cached = getattr(gates, "_b200_importance", None)
         if cached is not None and cached[1] == gates._version:
-            # gates straight from moe_forward: the dispatch kernel already reduced them
+            # gates straight from moe_forward: the dispatch kernel already reduced
+            # them and evaluated the penalty (no launch here)
             imp = cached[0]
-            _lib.call("b200moe_importance_loss", imp.data_ptr(), E, loss.data_ptr(), err.data_ptr(),
-                      _lib.stream_ptr())
+            if len(cached) > 2 and cached[2] is not None:
+                loss = cached[2]
+            else:
+                _lib.call("b200moe_importance_loss", imp.data_ptr(), E, loss.data_ptr(), err.data_ptr(),
+                          _lib.stream_ptr())
         else:
             g = gates.detach().to(torch.float32).contiguous()
             imp = torch.empty(E, dtype=torch.float32, device=g.device)

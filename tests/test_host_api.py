@@ -41,7 +41,8 @@ def test_version_and_error_strings():
 def test_argument_errors_map_to_reference_exceptions():
     # invalid arguments are rejected before any device work (no GPU needed)
     with pytest.raises(ConfigError):
-        _lib.call("b200moe_dispatch", None, 4, 8, 1, 7, 0, 0, None, None, None, None, None, None, None, None)
+        _lib.call("b200moe_dispatch", None, 4, 8, 1, 7, 0, 0, None, None, None, None, None, None, None, None, None,
+                  None)
     with pytest.raises(ConfigError):
         _lib.call("b200moe_router_fwd", None, None, None, None, 4, 64, 8, 9, 0, None, None, None, None, None, None,
                   None)

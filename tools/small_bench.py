@@ -32,7 +32,7 @@ s = _lib.stream_ptr()
 _lib.call("b200moe_router_fwd", x.data_ptr(), wg.data_ptr(), wn.data_ptr(), None, T, H, E, k, 0, logits.data_ptr(),
           gates.data_ptr(), None, None, ws.data_ptr(), err.data_ptr(), s)
 cap = P.expert_capacity(T, E, 1.0)
-slot_rank, counts, seg_base, gate_mass, imp, stats = P.moe._run_dispatch(gates, cap, "position")
+slot_rank, counts, seg_base, gate_mass, (imp, _), stats = P.moe._run_dispatch(gates, cap, "position")
 torch.cuda.synchronize()
 R = P.moe._rows_bound(T, E, k, cap)
 xp = torch.zeros(R, H, **bf)
@@ -64,7 +64,8 @@ cases = {
                                                           s)),
     "router_bwd": (MB + S * H * 2, lambda: _lib.call("b200moe_router_bwd", dxp.data_ptr(), slot_rank.data_ptr(),
                                                      seg_base.data_ptr(), dg.data_ptr(), None, 0, 0, gates.data_ptr(),
-                                                     None, wg.data_ptr(), wn.data_ptr(), None, None, T, H, E, k, 0,
+                                                     None, wg.data_ptr(), wn.data_ptr(), None, None, None, None, T, H,
+                                                     E, k, 0,
                                                      dx.data_ptr(), dh.data_ptr(), None, ws.data_ptr(), s)),
     "router_wgrad": (MB, lambda: _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), None, T, H, E,
                                            dwg.data_ptr(), None, wsw.data_ptr(), s)),
