@@ -65,7 +65,9 @@ int b200moe_version(void);
  * h = x.W_g (+ z * softplus(x.W_noise) when z != NULL).  gates are bit-exact
  * with numpy float32 given the same logits.  probs (router_type st): full
  * softmax s; may be NULL for mixtral.  noise_act = x.W_noise (needed by the
- * backward; NULL when z == NULL).  workspace: >= 2*H*E_pad floats; on return
+ * backward; NULL when z == NULL).  err_flag (nullable): set to 1 on a GateError
+ * row (callers of the layer read it from the dispatch stats instead).
+ * workspace: >= 2*H*E_pad floats; on return
  * it holds the swizzled W_g (and W_noise) tables b200moe_router_bwd can reuse. */
 int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E,
                        int k, int router_type, float* logits, float* gates, float* probs, float* noise_act,
@@ -99,8 +101,9 @@ int b200moe_router_logits_bwd(const void* x, const float* dh, const float* w_g, 
  * gate > 0; `position` keeps the earliest tokens, `score` the largest gates
  * (stable, position breaks ties).  Outputs slot_rank [T,E], counts [E]
  * (= RoutingStats.assigned), seg_base [E], gate_mass [E] (sum of kept gates),
- * importance [E] (sum of all gates, the aux-loss input), stats[2] =
- * {dropped, total_slots} (int64).  importance_loss (nullable, [1] fp32): the
+ * importance [E] (sum of all gates, the aux-loss input), stats[3] =
+ * {dropped, total_slots, gate_error} (int64; gate_error = 1 if some token row
+ * has no positive gate, i.e. the router hit an all-masked softmax row).  importance_loss (nullable, [1] fp32): the
  * importance penalty var/mean^2 of `importance` (tensor.py:503-521), with
  * importance_err (nullable int32) set when mean <= 0.  workspace:
  * b200moe_dispatch_workspace_words(T) int32 words, zeroed once before first

@@ -290,7 +290,7 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__
                 if (e == e_mine) { ge = g[e]; pe = p[e]; }
             gates[(size_t)t_mine * E + e_mine] = ge;
             if (probs) probs[(size_t)t_mine * E + e_mine] = pe;
-            if (!ok && e_mine == 0) atomicExch(err_flag, 1);
+            if (!ok && e_mine == 0 && err_flag) atomicExch(err_flag, 1);
         }
     }
 }
@@ -521,6 +521,16 @@ dispatch_kernel(const float* __restrict__ gates, int T, int E, int capacity, int
         am_last = (ticket == (int)gridDim.x - 1);
     }
     __syncthreads();
+    if (am_last) {   // GateError rows (all gates zero) over the whole batch, for stats[2]
+        bool zero = false;
+        for (int t = threadIdx.x; t < T; t += blockDim.x) {
+            bool z = true;
+            for (int i = 0; i < E; ++i) z &= !(gates[(size_t)t * E + i] > 0.f);
+            zero |= z;
+        }
+        zero = __syncthreads_or(zero);
+        if (threadIdx.x == 0) stats[2] = zero ? 1 : 0;
+    }
     if (am_last && threadIdx.x == 0) {
         __threadfence();
         int acc = 0;
@@ -645,31 +655,55 @@ dispatch_scan_kernel(const float* __restrict__ gates, int T, int E, int capacity
         }
         pre[w] += inc[w] - f[w];
     }
-    // ---- decoupled look-back, one thread per expert: flag 1 = aggregate, 2 = inclusive prefix
+    // ---- decoupled look-back (flag 1 = aggregate, 2 = inclusive prefix).  Every
+    // expert's aggregate is published first; then warp w looks back for experts
+    // w, w + 8, ...: lane l polls tile (base - l), so a window of 32
+    // predecessors costs one round trip, and the nearest inclusive prefix in the
+    // window ends the walk.
+    const unsigned long long tag = (unsigned long long)epoch << 34;
     if (threadIdx.x < E) {
         const int e = threadIdx.x;
         const unsigned long long agg = (tot[e >> 2] >> (16 * (e & 3))) & 0xFFFFull;
-        const unsigned long long tag = (unsigned long long)epoch << 34;
-        unsigned long long* my = status + (size_t)tile * EP + e;
+        st_release_u64(status + (size_t)tile * EP + e, tag | ((tile == 0 ? 2ull : 1ull) << 32) | agg);
+    }
+    for (int e = warp; e < E; e += kWarps) {
+        const unsigned long long agg = (tot[e >> 2] >> (16 * (e & 3))) & 0xFFFFull;
         long long excl = 0;
-        if (tile == 0) {
-            st_release_u64(my, tag | (2ull << 32) | agg);
-        } else {
-            st_release_u64(my, tag | (1ull << 32) | agg);
-            for (int j = tile - 1; j >= 0; --j) {
-                unsigned long long v;
+        int base = tile - 1;
+        while (base >= 0) {
+            const int j = base - lane;
+            unsigned long long v = 0;
+            if (j >= 0) {
                 do {
                     v = ld_acquire_u64(status + (size_t)j * EP + e);
                 } while ((v >> 34) != (unsigned long long)epoch || ((v >> 32) & 3ull) == 0);
-                excl += (long long)(v & 0xFFFFFFFFull);
-                if (((v >> 32) & 3ull) == 2) break;
             }
-            st_release_u64(my, tag | (2ull << 32) | (unsigned long long)(excl + (long long)agg));
+            const unsigned pmask = __ballot_sync(0xffffffffu, j >= 0 && ((v >> 32) & 3ull) == 2);
+            const int stop = pmask ? (__ffs(pmask) - 1) : 31;            // nearest inclusive prefix
+            long long val = (j >= 0 && lane <= stop) ? (long long)(v & 0xFFFFFFFFull) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+            excl += val;
+            if (pmask) break;
+            base -= 32;
         }
-        excl_sh[e] = (int)excl;
-        if (tile == ntiles - 1) ws[8 + e] = (int)(excl + (long long)agg);   // total slots of expert e
+        if (lane == 0) {
+            if (tile > 0)
+                st_release_u64(status + (size_t)tile * EP + e, tag | (2ull << 32) | (unsigned long long)(excl + agg));
+            excl_sh[e] = (int)excl;
+            if (tile == ntiles - 1) ws[8 + e] = (int)(excl + (long long)agg);   // total slots of expert e
+        }
     }
     __syncthreads();
+    // a token row whose gates are all zero is a GateError row (the router found
+    // no finite kept logit, tensor.py:283-284): every valid row has a positive
+    // top-1 gate.  OR-ed into ws[3], reported in stats[2] by the last CTA.
+    {
+        bool zero_row = (t < T);
+#pragma unroll
+        for (int e = 0; e < EP; ++e) zero_row &= !(g[e] > 0.f);
+        if (__syncthreads_or(zero_row) && threadIdx.x == 0) atomicOr(&ws[3], 1);
+    }
     // ---- ranks, kept flags, per-thread sums
     float imp_e[EP], mass_e[EP];
 #pragma unroll
@@ -729,9 +763,11 @@ dispatch_scan_kernel(const float* __restrict__ gates, int T, int E, int capacity
         }
         stats[0] = dropped;
         stats[1] = total;
+        stats[2] = ((volatile int32_t*)ws)[3];
         if (imp_loss) importance_cv2(importance, E, imp_loss, imp_err);
         ws[0] = 0;          // ticket
         ws[1] = 0;          // tile counter
+        ws[3] = 0;          // error flag
         ws[2] = (int)((epoch + 1) & 0x3FFFFFFFu);
     }
 }

@@ -152,19 +152,19 @@ class _EPFunction(torch.autograd.Function):
         gates = torch.empty(T, E, **f32)
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
-        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        err = None          # gate errors reach the host through the dispatch stats (stats[2])
         ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
         ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
                   cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),
-                  ws.data_ptr(), err.data_ptr(), s)
+                  ws.data_ptr(), None, s)
         slot_rank = torch.empty(T, E, dtype=torch.int32, device=dev)
         counts = torch.empty(E, dtype=torch.int32, device=dev)
         seg_base = torch.empty(E, dtype=torch.int32, device=dev)
         gate_mass = torch.empty(E, **f32)
         imp = torch.empty(E, **f32)
         imp_loss = torch.empty(1, **f32)
-        stats = torch.empty(2, dtype=torch.int64, device=dev)
+        stats = torch.empty(3, dtype=torch.int64, device=dev)
         _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if plan.capacity is None else plan.capacity,
                   _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_COMPACT, 0, slot_rank.data_ptr(),
                   counts.data_ptr(), seg_base.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),
@@ -358,19 +358,19 @@ class _EPPeerFunction(torch.autograd.Function):
         gates = torch.empty(T, E, **f32)
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
-        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        err = None          # gate errors reach the host through the dispatch stats (stats[2])
         ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
         ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
                   cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),
-                  ws.data_ptr(), err.data_ptr(), s)
+                  ws.data_ptr(), None, s)
         slot_rank = torch.empty(T, E, dtype=torch.int32, device=dev)
         counts = torch.empty(E, dtype=torch.int32, device=dev)
         seg_local = torch.empty(E, dtype=torch.int32, device=dev)
         gate_mass = torch.empty(E, **f32)
         imp = torch.empty(E, **f32)
         imp_loss = torch.empty(1, **f32)
-        stats = torch.empty(2, dtype=torch.int64, device=dev)
+        stats = torch.empty(3, dtype=torch.int64, device=dev)
         _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if plan.capacity is None else plan.capacity,
                   _lib.POLICY[cfg.drop_policy], _lib.LAYOUT_FIXED, plan.cap_pad, slot_rank.data_ptr(),
                   counts.data_ptr(), seg_local.data_ptr(), gate_mass.data_ptr(), imp.data_ptr(), stats.data_ptr(),

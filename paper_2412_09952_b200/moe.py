@@ -207,9 +207,9 @@ class DeviceRoutingStats(RoutingStats):
     def _materialize(self):
         if self._host is None:
             counts, stats, mass, err = self._dev
-            if err is not None and int(err.item()) != 0:
-                raise GateError("softmax row with all entries masked")
             st = stats.cpu().numpy()
+            if (err is not None and int(err.item()) != 0) or (st.size > 2 and st[2] != 0):
+                raise GateError("softmax row with all entries masked")
             self._host = (counts.cpu().numpy().astype(np.int64), int(st[0]), int(st[1]), mass.cpu().numpy())
         return self._host
 
@@ -493,7 +493,7 @@ def _run_dispatch(gates: torch.Tensor, capacity: int | None, drop_policy: str, l
     seg_base = torch.empty(E, dtype=torch.int32, device=dev)
     gate_mass = torch.empty(E, dtype=torch.float32, device=dev)
     imp = torch.empty(E, dtype=torch.float32, device=dev)
-    stats = torch.empty(2, dtype=torch.int64, device=dev)
+    stats = torch.empty(3, dtype=torch.int64, device=dev)      # dropped, total slots, gate-error flag
     loss = torch.empty(1, dtype=torch.float32, device=dev)     # importance penalty of these gates
     _lib.call("b200moe_dispatch", gates.data_ptr(), T, E, -1 if capacity is None else int(capacity),
               _lib.POLICY[drop_policy], layout, seg_stride, slot_rank.data_ptr(), counts.data_ptr(),
@@ -595,12 +595,12 @@ class _MoEFunction(torch.autograd.Function):
         gates = torch.empty(T, E, **f32)
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
-        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        err = None          # gate errors reach the host through the dispatch stats (stats[2])
         ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
         ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E, k,
                   rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act), ws.data_ptr(),
-                  err.data_ptr(), s)
+                  None, s)
         cap = expert_capacity(T, E, cfg.capacity_factor)
         slot_rank, counts, seg_base, gate_mass, (imp, imp_loss), stats = _run_dispatch(gates, cap, cfg.drop_policy)
         R = _rows_bound(T, E, k, cap)
@@ -764,8 +764,7 @@ class _ImportanceFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, gates):
         T, E = gates.shape
-        loss = torch.empty(1, dtype=torch.float32, device=gates.device)
-        err = torch.zeros(1, dtype=torch.int32, device=gates.device)
+        loss = None
         cached = getattr(gates, "_b200_importance", None)
         if cached is not None and cached[1] == gates._version:
             # gates straight from moe_forward: the dispatch kernel already reduced
@@ -774,9 +773,11 @@ class _ImportanceFunction(torch.autograd.Function):
             if len(cached) > 2 and cached[2] is not None:
                 loss = cached[2]
             else:
-                _lib.call("b200moe_importance_loss", imp.data_ptr(), E, loss.data_ptr(), err.data_ptr(),
-                          _lib.stream_ptr())
+                loss = torch.empty(1, dtype=torch.float32, device=gates.device)
+                _lib.call("b200moe_importance_loss", imp.data_ptr(), E, loss.data_ptr(), None, _lib.stream_ptr())
         else:
+            loss = torch.empty(1, dtype=torch.float32, device=gates.device)
+            err = torch.zeros(1, dtype=torch.int32, device=gates.device)
             g = gates.detach().to(torch.float32).contiguous()
             imp = torch.empty(E, dtype=torch.float32, device=g.device)
             _lib.call("b200moe_importance_fwd", g.data_ptr(), T, E, imp.data_ptr(), loss.data_ptr(), err.data_ptr(),
@@ -789,7 +790,6 @@ class _ImportanceFunction(torch.autograd.Function):
                 raise GateError("importance penalty needs positive total gate mass")
         ctx.save_for_backward(imp)
         ctx.shape = (T, E)
-        ctx.err = err
         return loss[0]
 
     @staticmethod

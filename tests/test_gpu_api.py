@@ -132,3 +132,25 @@ def test_expert_list_layer_caches_stack_and_trains():
         ws[0][0].add_(0.01)
     B.moe_forward(x, layer, cfg)
     assert layer._stack_cache[1] is not stacks
+
+
+def test_layer_gate_error_row_surfaces_through_routing_stats():
+    """A token row with no finite logit (NaN input) makes the reference's
+    softmax raise GateError (tensor.py:283-284).  The layer reports it through
+    the dispatch statistics when they are read (no host sync in the forward),
+    for the scan dispatch (position) and the per-expert select (score)."""
+    T, H, F, E = 300, 256, 256, 8
+    for pol in ("position", "score"):
+        g = torch.Generator(device="cuda").manual_seed(1)
+        W = [(torch.randn(s, generator=g, device="cuda") * 0.05).to(torch.bfloat16) for s in ((E, F, H), (E, H, F),
+                                                                                            (E, F, H))]
+        wg = torch.randn(H, E, generator=g, device="cuda") * 0.1
+        layer = B.MoELayer.from_stacked(B.RouterParams(wg, torch.zeros_like(wg)), *W)
+        cfg = B.GateConfig(n_experts=E, top_k=2, capacity_factor=1.0, drop_policy=pol)
+        x = torch.randn(T, H, generator=g, device="cuda")
+        ok = B.moe_forward(x, layer, cfg)
+        assert ok.stats.assigned.sum() > 0                          # healthy batch: no error
+        x[17] = float("nan")
+        bad = B.moe_forward(x, layer, cfg)
+        with pytest.raises(B.GateError):
+            _ = bad.stats.assigned
