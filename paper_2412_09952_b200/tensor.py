@@ -301,6 +301,19 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, n_heads: int, n
 # dense SwiGLU FFN on the grouped-GEMM kernels (one segment)
 # --------------------------------------------------------------------------
 
+_SEG_CACHE: dict = {}
+
+
+def _one_segment(T: int, dev):
+    """Device segment table (base [0], count [T]) of a one-segment GEMM, cached."""
+    key = (T, dev)
+    t = _SEG_CACHE.get(key)
+    if t is None:
+        t = (torch.zeros(1, dtype=torch.int32, device=dev), torch.full((1,), T, dtype=torch.int32, device=dev))
+        _SEG_CACHE[key] = t
+    return t
+
+
 class _FFN(torch.autograd.Function):
     """o = (silu(x W1^T) * (x W3^T)) W2^T with kernel-layout weights
     W1, W3 [1, F, H], W2 [1, H, F] (bf16); x bf16 [T, H], H and F multiples
@@ -313,10 +326,12 @@ class _FFN(torch.autograd.Function):
         dev = x.device
         R = _pad_to(max(T, 1), SEG_PAD)
         bf = dict(dtype=torch.bfloat16, device=dev)
-        xp = torch.zeros(R, H, **bf)
-        xp[:T] = x
-        base = _arange_i32(1, dev) * 0
-        cnt = torch.full((1,), T, dtype=torch.int32, device=dev)
+        if R == T and x.dtype == torch.bfloat16 and x.is_contiguous():
+            xp = x                      # no padding rows needed: the GEMMs read x in place
+        else:
+            xp = torch.zeros(R, H, **bf)
+            xp[:T] = x
+        base, cnt = _one_segment(T, dev)
         seg_e = _arange_i32(1, dev)
         s = _lib.stream_ptr()
         A, B, Hh = (torch.empty(R, Fd, **bf) for _ in range(3))
@@ -339,8 +354,12 @@ class _FFN(torch.autograd.Function):
         bf = dict(dtype=torch.bfloat16, device=dev)
         seg_e = _arange_i32(1, dev)
         s = _lib.stream_ptr()
-        dO = torch.zeros(R, H, **bf)
-        dO[:T] = dy
+        dy = dy.to(torch.bfloat16)
+        if R == T and dy.is_contiguous():
+            dO = dy
+        else:
+            dO = torch.zeros(R, H, **bf)
+            dO[:T] = dy
         dA = torch.empty(R, Fd, **bf)
         dB = torch.empty(R, Fd, **bf)
         _lib.call("b200moe_expert_bwd2", dO.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(), base.data_ptr(),

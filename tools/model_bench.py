@@ -70,6 +70,9 @@ def main():
                     help="accumulate expert gradients with autograd adds instead of inside the WGRAD GEMM")
     ap.add_argument("--serial-opt", action="store_true",
                     help="optimizer after the backward in one launch (default: overlapped with the backward)")
+    ap.add_argument("--experts", type=int, default=8, help="experts per MoE layer (E8T2 = 8)")
+    ap.add_argument("--zero", action="store_true",
+                    help="ZeRO-1: shard the replicated tensors' optimizer state over the ranks")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = 0
@@ -89,12 +92,16 @@ def main():
                             seq_len=a.seq)
     dense = random_dense(cfg, dev)
     if world > 1:   # online upcycling of this rank's experts only (upcycle.py:187-227)
-        moe = P.upcycle_shard(P.shard_dense(dense, 1, world)[rank], 8, 2, router_seed=1, capacity_factor=a.cf)
+        moe = P.upcycle_shard(P.shard_dense(dense, 1, world)[rank], a.experts, 2, router_seed=1,
+                              capacity_factor=a.cf)
     else:
-        moe = P.upcycle_full(dense, 8, 2, router_seed=1, capacity_factor=a.cf)
+        moe = P.upcycle_full(dense, a.experts, 2, router_seed=1, capacity_factor=a.cf)
     del dense
+    torch.cuda.empty_cache()
     state = TrainState(moe, shadows=not a.no_shadows)
-    opt = state.optimizer("adam")
+    if a.zero and (world == 1 or a.serial_opt):
+        raise SystemExit("--zero needs N > 1 ranks and the overlapped optimizer")
+    opt = state.optimizer("adam", zero_group=group if a.zero else None)
     ov = None if a.serial_opt else OverlappedStep(opt, group)
     dp = DataParallelGrads(state.leaves, group) if (world > 1 and ov is None) else None
     rng = np.random.default_rng(rank)
@@ -149,11 +156,14 @@ def main():
     if world > 1:
         dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
-    t0 = time.perf_counter()
-    for i in range(a.steps):
-        loss, _ = step(evs[i])
-    torch.cuda.synchronize()
-    wall = (time.perf_counter() - t0) / a.steps
+    from bench import ClockSampler
+    with ClockSampler(dev.index) as clk:
+        t0 = time.perf_counter()
+        for i in range(a.steps):
+            loss, _ = step(evs[i])
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / a.steps
+    clocks = clk.summary()
     ms = float(np.median([e[0].elapsed_time(e[3]) for e in evs]))
     if world > 1:   # the step takes as long as the slowest rank
         t = torch.tensor([ms, float(kept)], device=dev, dtype=torch.float64)
@@ -170,7 +180,7 @@ def main():
         dist.destroy_process_group()
         return
     out = {
-        "metric": f"Llama-3-8B-shape E8T2 {cfg.layers}-layer training step tokens/s",
+        "metric": f"Llama-3-8B-shape E{a.experts}T2 {cfg.layers}-layer training step tokens/s",
         "value": round(world * T / (ms * 1e-3), 1), "unit": "tokens/s", "ms_per_step": round(ms, 3),
         "n_gpus": world, "parallelism": f"ep{world} (MoE) + dp{world} (rest)" if world > 1 else "single GPU",
         "wall_ms_per_step": round(wall * 1e3, 3), "phases_ms": split,
@@ -180,8 +190,10 @@ def main():
         "loss": float(loss.detach()) * world * M, "micro_batches": M,
         "expert_grad_accumulation": "fused into WGRAD" if (M > 1 and not a.no_fused_acc) else "autograd", "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
+        "optimizer_state_gb_rank0": round(opt.state_bytes() / 2**30, 2), "zero1": bool(a.zero),
+        "clocks": clocks,
         "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
-                   "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": 8,
+                   "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": a.experts,
                    "top_k": 2, "capacity_factor": a.cf,
                    "optimizer": "adam (fp32 masters), " + ("after the backward" if a.serial_opt else
                                                            "per tensor on a side stream during the backward")},

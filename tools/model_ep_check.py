@@ -17,7 +17,7 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2412_09952_b200 as P  # noqa: E402
-from paper_2412_09952_b200.train import DataParallelGrads, TrainState  # noqa: E402
+from paper_2412_09952_b200.train import DataParallelGrads, OverlappedStep, TrainState  # noqa: E402
 
 CFG = dict(vocab=512, hidden=256, layers=2, heads=4, kv_heads=2, ffn_hidden=512, seq_len=64)
 E, K, CF, AUX = 4, 2, 1.0, 0.01
@@ -45,6 +45,53 @@ def loss_of(fwd, targets, world):
     for g in fwd.gates:
         loss = loss + (AUX / len(fwd.gates)) * P.importance_penalty(g)
     return loss / world
+
+
+def zero_check(rank, world, cfg):
+    """ZeRO-1 (train.TrainState.optimizer(zero_group=...)): two Adam steps of the
+    EP+DP model with the replicated tensors' moments sharded over the ranks
+    (reduce-scatter / slice update / all-gather) against the replicated
+    overlapped update: every parameter delta and the full fp32 masters agree
+    (reduction order of the gradient sum aside), and the replicated tensors hold
+    1/world of their moments."""
+    res = {}
+    for zero in (False, True):
+        dense = P.init_dense(cfg, seed=11)
+        ms = P.upcycle_shard(P.shard_dense(dense, 1, world)[rank], E, K, moe_layers=MOE_LAYERS, router_seed=3,
+                             capacity_factor=CF)
+        state = TrainState(ms)
+        before = {n: t.detach().float().clone() for n, t in state.leaves.items()}
+        opt = state.optimizer("adam", zero_group=dist.group.WORLD if zero else None)
+        ov = OverlappedStep(opt, dist.group.WORLD)
+        for step in range(2):
+            for t in opt.params.values():
+                t.grad = None
+            inputs, targets = batch(rank + 10 * step, cfg)
+            fwd = P.forward_with_stats(ms, inputs, training=True, compute=state.compute, ep_group=dist.group.WORLD)
+            loss = loss_of(fwd, targets, world)
+            ov.begin(1e-3)
+            loss.backward()
+            ov.finish()
+        torch.cuda.synchronize()
+        ov.remove()
+        res[zero] = ({n: t.detach().float() - before[n] for n, t in state.leaves.items()},
+                     {n: m.detach().clone() for n, m in opt.master.items()}, opt.state_bytes(), len(opt.shards))
+    ok = True
+    worst = ("", 0.0)
+    for n, d in res[False][0].items():
+        e = rel(res[True][0][n], d) if float(d.norm()) > 0 else float((res[True][0][n] - d).abs().max())
+        if e > worst[1]:
+            worst = (n, e)
+        if e > 2e-2:
+            ok = False
+    for n, m in res[False][1].items():
+        if rel(res[True][1][n], m) > 1e-4:
+            ok = False
+            print(f"rank {rank}: zero master mismatch {n}", flush=True)
+    ok &= res[True][3] > 0 and res[True][2] < res[False][2]
+    print(f"rank {rank}: [zero1] sharded={res[True][3]} state_bytes {res[False][2]} -> {res[True][2]} "
+          f"worst_delta={worst[0]} {worst[1]:.2e} {'PASS' if ok else 'FAIL'}", flush=True)
+    return ok
 
 
 def main():
@@ -106,6 +153,7 @@ def main():
                   f"loss_rel={errs['loss']:.2e} worst_grad={worst[0]} {worst[1]:.2e} "
                   f"{'PASS' if ok else 'FAIL'}", flush=True)
         dist.barrier()
+    ok &= zero_check(rank, world, cfg)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     dist.destroy_process_group()
