@@ -267,15 +267,19 @@ class _EPFunction(torch.autograd.Function):
 
 
 class _PeerBuffers:
-    """One symmetric-memory allocation per (buffer slot, receive rows, hidden,
-    group) holding this rank's receive-side buffers -- xr (tokens in), O (expert
-    outputs), dO, dxp, each [R*E_local*cap_pad, H] bf16 -- plus the int32
-    receive-count table.  Peers address them through device arrays of per-rank
-    base pointers.  xr and O are saved for the backward, so every layer that is
-    alive in one autograd graph needs its own slot (the model forward uses the
-    layer index)."""
+    """Symmetric-memory receive buffers of the p2p transport.  A *forward*
+    set per (buffer slot, receive rows, hidden, group) holds xr (tokens in) and
+    O (expert outputs), each [R*E_local*cap_pad, H] bf16, plus the int32
+    receive-count table; xr and O are saved for the layer's backward, so every
+    layer alive in one autograd graph needs its own slot (the model forward
+    uses the layer index).  The *backward* planes dO and dxp live only inside
+    one layer's backward, and backward passes run one layer at a time, so one
+    set (slot -1) serves every layer.  Peers address the planes through device
+    arrays of per-rank base pointers; canary bands surround every plane."""
 
     _cache: dict = {}
+    GUARD = 4096          # canary bytes before, between and after the planes
+    CANARY = 0xA5
 
     @classmethod
     def get(cls, rows: int, H: int, n_counts: int, group, device, slot: int = 0):
@@ -287,16 +291,17 @@ class _PeerBuffers:
             cls._cache[key] = b
         return b
 
-    GUARD = 4096          # canary bytes before, between and after the planes
-    CANARY = 0xA5
+    @classmethod
+    def backward_set(cls, rows: int, H: int, group, device):
+        return cls.get(rows, H, 0, group, device, slot=-1)
 
     def __init__(self, rows, H, n_counts, grp, device):
         import torch.distributed._symmetric_memory as symm
         self.generation = 0   # bumped by every forward that (re)fills xr / O
         G = self.GUARD
         plane = rows * H * 2
-        offs = [G + i * (plane + G) for i in range(4)]
-        cnt_off = offs[3] + plane + G
+        offs = [G + i * (plane + G) for i in range(2)]
+        cnt_off = offs[1] + plane + G
         cnt_bytes = ((n_counts * 4 + 255) // 256) * 256
         total = cnt_off + cnt_bytes + G
         self.raw = symm.empty(total, dtype=torch.uint8, device=device)
@@ -307,7 +312,7 @@ class _PeerBuffers:
         self._guards = [(0, G)] + [(o + plane, G) for o in offs] + [(cnt_off + cnt_bytes, G)]
         ptrs = list(self.handle.buffer_ptrs)
         mk = lambda off: torch.tensor([p + off for p in ptrs], dtype=torch.int64, device=device)  # noqa: E731
-        self.peer = [mk(o) for o in offs]   # xr, O, dO, dxp base pointers on every rank
+        self.peer = [mk(o) for o in offs]   # the two planes' base pointers on every rank
         self.peer_counts = mk(cnt_off)
 
     def guards_intact(self) -> bool:
@@ -318,6 +323,7 @@ class _PeerBuffers:
     def barrier(self):
         self.handle.barrier(channel=0)
 
+    # forward set: plane 0 = xr, plane 1 = O;  backward set: plane 0 = dO, plane 1 = dxp
     @property
     def xr(self):
         return self.views[0]
@@ -328,11 +334,11 @@ class _PeerBuffers:
 
     @property
     def do(self):
-        return self.views[2]
+        return self.views[0]
 
     @property
     def dxp(self):
-        return self.views[3]
+        return self.views[1]
 
 
 class _EPPeerFunction(torch.autograd.Function):
@@ -391,6 +397,11 @@ class _EPPeerFunction(torch.autograd.Function):
                   rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, A.data_ptr(), B.data_ptr(), Hh.data_ptr(), s)
         _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
                   rexp.data_ptr(), nseg, Rs, H, F, El, pb.o.data_ptr(), s)
+        if st.get("recompute"):
+            # selective recompute: a, b, h ([rows, F] x 3, the layer's largest
+            # activations) are dropped here and rebuilt by one FWD1 launch at the
+            # start of the backward from xr (kept in the forward set anyway)
+            A = B = Hh = None
         pb.barrier()                            # all expert outputs are ready
         y = torch.empty(T, H, **bf)
         _lib.call("b200moe_combine_peer", pb.peer[1].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
@@ -402,6 +413,7 @@ class _EPPeerFunction(torch.autograd.Function):
         ctx.acc_targets = _acc_targets(W1, W2, W3)
         ctx.pb = pb
         ctx.generation = pb.generation
+        ctx.recompute = A is None
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer,
                               A, B, Hh)
         return y, gates
@@ -429,27 +441,34 @@ class _EPPeerFunction(torch.autograd.Function):
         nseg = plan.world * El
         rbase, rexp = plan.recv_segments(dev)
         rcounts = pb.counts
+        pbb = _PeerBuffers.backward_set(Rs, H, group, dev)   # dO, dxp: shared by every layer's backward
+        if ctx.recompute:
+            A, B, Hh = (torch.empty(Rs, F, **bf) for _ in range(3))
+            _lib.call("b200moe_expert_fwd1", pb.xr.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
+                      rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, A.data_ptr(), B.data_ptr(),
+                      Hh.data_ptr(), s)
 
         dy = (torch.zeros(T, H, **bf) if dy is None else dy).to(torch.bfloat16).contiguous()
         dg = torch.empty(T, E, **f32)
+        pbb.barrier()                           # every rank is done with the previous layer's dO / dxp
         _lib.call("b200moe_combine_bwd_peer", dy.data_ptr(), pb.peer[1].data_ptr(), gates.data_ptr(),
-                  slot_rank.data_ptr(), seg_peer.data_ptr(), counts.data_ptr(), T, H, E, El, pb.peer[2].data_ptr(),
+                  slot_rank.data_ptr(), seg_peer.data_ptr(), counts.data_ptr(), T, H, E, El, pbb.peer[0].data_ptr(),
                   dg.data_ptr(), s)
-        pb.barrier()                            # all output gradients have landed
+        pbb.barrier()                           # all output gradients have landed
         dA = torch.empty(Rs, F, **bf)
         dB = torch.empty(Rs, F, **bf)
-        _lib.call("b200moe_expert_bwd2", pb.do.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
+        _lib.call("b200moe_expert_bwd2", pbb.do.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
                   rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(),
                   dB.data_ptr(), s)
         dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
-        _wgrad_call(acc, pb.xr.data_ptr(), Hh.data_ptr(), pb.do.data_ptr(), dA.data_ptr(),
+        _wgrad_call(acc, pb.xr.data_ptr(), Hh.data_ptr(), pbb.do.data_ptr(), dA.data_ptr(),
                   dB.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El,
                   dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
         if acc:
             dW1 = dW2 = dW3 = None
         _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
-                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, pb.dxp.data_ptr(), s)
-        pb.barrier()                            # all input gradients are ready
+                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, pbb.dxp.data_ptr(), s)
+        pbb.barrier()                           # all input gradients are ready
         dx = torch.empty(T, H, **bf)
         dh = torch.empty(T, E, **f32)
         dn = torch.empty(T, E, **f32) if z is not None else None
@@ -458,7 +477,7 @@ class _EPPeerFunction(torch.autograd.Function):
             dgx = dgates.to(torch.float32)
             sx_t, sx_e = dgx.stride()
         ws = torch.empty(2 * H * _ep(E) + T * _ep(E), **f32)
-        _lib.call("b200moe_router_bwd_peer", pb.peer[3].data_ptr(), El, slot_rank.data_ptr(), seg_peer.data_ptr(),
+        _lib.call("b200moe_router_bwd_peer", pbb.peer[1].data_ptr(), El, slot_rank.data_ptr(), seg_peer.data_ptr(),
                   dg.data_ptr(), _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(),
                   w_noise.data_ptr(), _lib.ptr(z), _lib.ptr(noise_act), *_swizzled(ctx, H, E, z), T, H, E,
                   cfg.top_k, _lib.ROUTER[cfg.router_type], dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
@@ -482,7 +501,7 @@ class ExpertParallelMoE:
     TRANSPORTS = ("p2p", "nccl")
 
     def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None, transport: str = "p2p",
-                 buffer_slot: int = 0):
+                 buffer_slot: int = 0, recompute: bool = False):
         """transport: "p2p" (default) fuses the dispatch/combine exchange into the
         permute/combine kernels over NVLink symmetric memory; "nccl" uses
         all_to_all_single between separate kernels (the comparison baseline).
@@ -503,6 +522,7 @@ class ExpertParallelMoE:
             raise ConfigError("the B200 router supports up to 32 experts")
         self.w_g, self.w_noise, self.W1, self.W2, self.W3, self.cfg = w_g, w_noise, W1, W2, W3, cfg
         self.buffer_slot = buffer_slot
+        self.recompute = recompute   # p2p: rebuild a, b, h in the backward instead of keeping them
         self._tokens_checked = set()
 
     def _check_tokens(self, T: int, device) -> None:
@@ -527,7 +547,8 @@ class ExpertParallelMoE:
             self._check_tokens(T, x.device)
         plan = EPPlan.make(self.world, self.rank, self.cfg.n_experts, T, self.cfg.capacity_factor)
         z = _noise(T, self.cfg.n_experts, x.device, self.cfg.noise_enabled and training, rng, noise)
-        st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router, buffer_slot=self.buffer_slot)
+        st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router, buffer_slot=self.buffer_slot,
+                  recompute=self.recompute)
         fn = _EPPeerFunction if self.transport == "p2p" else _EPFunction
         y, gates = fn.apply(x.to(torch.bfloat16).contiguous(), self.w_g.to(torch.float32).contiguous(),
                             self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)

@@ -82,6 +82,33 @@ def case(rank, world, dev, T, H, F, router, policy, cf, noise, transport, E=8, k
     return ok
 
 
+def recompute_case(rank, world, dev, T=768, H=512, F=512, E=8, k=2):
+    """p2p EP layer with selective recompute (a, b, h rebuilt by FWD1 in the
+    backward) against the same layer keeping them: outputs and every gradient
+    bit-identical (same kernels on the same inputs)."""
+    El = E // world
+    g = torch.Generator(device=dev).manual_seed(7)
+    W = [(torch.randn(s_, generator=g, device=dev) * 0.05).to(torch.bfloat16) for s_ in ((El, F, H), (El, H, F),
+                                                                                          (El, F, H))]
+    wg = torch.randn(H, E, generator=g, device=dev) * 0.05
+    gx = torch.Generator(device=dev).manual_seed(300 + rank)
+    x = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
+    dy = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
+    cfg = P.GateConfig(n_experts=E, top_k=k, capacity_factor=2.0)
+    res = []
+    for rc in (False, True):
+        lw = [t.clone().requires_grad_() for t in [wg, torch.zeros_like(wg)] + W]
+        ep = ExpertParallelMoE(*lw, cfg, transport="p2p", buffer_slot=40 + int(rc), recompute=rc)
+        xe = x.clone().requires_grad_()
+        out = ep(xe)
+        ((out.output.float() * dy.float()).sum() + 0.1 * P.importance_penalty(out.gates)).backward()
+        torch.cuda.synchronize()
+        res.append([out.output, xe.grad] + [t.grad for t in lw if t.grad is not None])
+    ok = len(res[0]) == len(res[1]) and all(torch.equal(a, b) for a, b in zip(*res))
+    print(f"rank {rank}: {'PASS' if ok else 'FAIL'} [p2p recompute] bit-identical to keeping a, b, h", flush=True)
+    return ok
+
+
 def oracle_case(rank, world, dev, T, H, F, router, policy, cf, noise, transport, E=8, k=2, lam=0.1):
     """EP layer against the CPU ORACLE (oracle/moe_oracle.py, the reference's
     closed form, moefold/moe.py:250-283) on each rank's own batch: routing
@@ -172,6 +199,7 @@ def main():
         # against the CPU oracle directly (not the single-GPU CUDA layer)
         ok &= oracle_case(rank, world, dev, 512, 256, 512, "mixtral", "position", 1.0, True, transport)
         ok &= oracle_case(rank, world, dev, 384, 256, 256, "st", "score", None, False, transport)
+    ok &= recompute_case(rank, world, dev)
     # canary bands around every symmetric receive plane (written by peers over NVLink) untouched
     from paper_2412_09952_b200.ep import _PeerBuffers
     torch.cuda.synchronize()

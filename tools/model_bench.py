@@ -71,6 +71,8 @@ def main():
     ap.add_argument("--serial-opt", action="store_true",
                     help="optimizer after the backward in one launch (default: overlapped with the backward)")
     ap.add_argument("--experts", type=int, default=8, help="experts per MoE layer (E8T2 = 8)")
+    ap.add_argument("--recompute", type=int, default=0,
+                    help="MoE layers (the first N, p2p EP) that rebuild a, b, h in the backward instead of keeping them")
     ap.add_argument("--zero", action="store_true",
                     help="ZeRO-1: shard the replicated tensors' optimizer state over the ranks")
     a = ap.parse_args()
@@ -123,7 +125,7 @@ def main():
         for mb, (inputs, targets) in enumerate(batches):
             last = mb == M - 1
             fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute, ep_group=group,
-                                       transport=a.transport)
+                                       transport=a.transport, recompute_layers=range(a.recompute))
             loss = P.cross_entropy(fwd.logits, targets)
             for g in fwd.gates:
                 loss = loss + (aux / len(fwd.gates)) * P.importance_penalty(g)
@@ -191,6 +193,7 @@ def main():
         "expert_grad_accumulation": "fused into WGRAD" if (M > 1 and not a.no_fused_acc) else "autograd", "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
         "optimizer_state_gb_rank0": round(opt.state_bytes() / 2**30, 2), "zero1": bool(a.zero),
+        "recompute_moe_layers": a.recompute,
         "clocks": clocks,
         "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
                    "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": a.experts,
