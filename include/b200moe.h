@@ -216,6 +216,22 @@ int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, co
                              const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
                              int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate,
                              cudaStream_t stream);
+/* Per-call variants.  grid_ctas > 0 caps the persistent grid at that many
+ * CTAs (rounded down to the CTA-pair size) so that two GEMMs of the backward
+ * can run concurrently on disjoint parts of the chip; 0 = one CTA per SM.
+ * subs (WGRAD): bit 0 dW1, bit 1 dW3, bit 2 dW2 -- the sub-problems to compute
+ * (dW2 needs only dout and h, so it can start before BWD2 has produced da/db). */
+int b200moe_expert_bwd2_ex(const void* dout, const void* w2, const void* a_pre, const void* b_pre,
+                           const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                           int H, int F, int E_local, void* da_out, void* db_out, int grid_ctas, cudaStream_t stream);
+int b200moe_expert_bwd1_ex(const void* da, const void* db, const void* w1, const void* w3, const int* seg_base,
+                           const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
+                           void* dxp_out, int grid_ctas, cudaStream_t stream);
+int b200moe_expert_wgrad_ex(const void* xp, const void* h, const void* dout, const void* da, const void* db,
+                            const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                            int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate, int subs,
+                            int grid_ctas, cudaStream_t stream);
+
 /* Diagnostics knobs for tests and A/B tools, NOT part of the product path:
  * thread-local (they affect only GEMM launches issued by the calling thread;
  * other threads always run the defaults), so the entry points above stay

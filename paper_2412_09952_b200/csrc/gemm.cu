@@ -83,7 +83,10 @@ struct GemmArgs {
     const __nv_bfloat16* in0;
     const __nv_bfloat16* in1;
     int debug;  // bit 0: skip wgrad epilogue stores (diagnostics only)
+    int wgrad_subs;  // WGRAD sub-problems to compute: bit 0 dW1, bit 1 dW3, bit 2 dW2 (0 = all)
 };
+
+__host__ __device__ __forceinline__ int wgrad_mask(const GemmArgs& a) { return a.wgrad_subs ? a.wgrad_subs : 7; }
 
 template <int kCG>
 struct Cfg {
@@ -167,19 +170,20 @@ struct Sched {
             }
         } else if constexpr (is_wgrad1<kMode>()) {
             const int tiles_w13 = (a.F / Cfg<kCG>::kTileM) * (a.H / kBN);
-            if (r < 2 * tiles_w13) {
-                ti.sub = r / tiles_w13;
-                r -= ti.sub * tiles_w13;
-                const int nt = a.H / kBN;
-                ti.m_tile = r / nt;
-                ti.n_tile = r % nt;
-            } else {
-                ti.sub = 2;
-                r -= 2 * tiles_w13;
-                const int nt = a.F / kBN;
-                ti.m_tile = r / nt;
-                ti.n_tile = r % nt;
+            const int tiles_w2 = (a.H / Cfg<kCG>::kTileM) * (a.F / kBN);
+            const int mask = wgrad_mask(a);
+            ti.sub = 0;
+#pragma unroll
+            for (int sb = 0; sb < 3; ++sb) {          // enabled sub-problems in order dW1, dW3, dW2
+                if (!((mask >> sb) & 1)) continue;
+                const int n = sb < 2 ? tiles_w13 : tiles_w2;
+                ti.sub = sb;
+                if (r < n) break;
+                r -= n;
             }
+            const int nt = (ti.sub == 2 ? a.F : a.H) / kBN;
+            ti.m_tile = r / nt;
+            ti.n_tile = r % nt;
         } else {
             const int mt = (prefix[s + 1] - prefix[s]) / n_tiles;
             ti.sub = 0;
@@ -885,7 +889,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
                 prefix[e + 1] = acc;
             }
         } else if constexpr (is_wgrad1<kMode>()) {
-            const int per_e = 2 * (a.F / C::kTileM) * (a.H / kBN) + (a.H / C::kTileM) * (a.F / kBN);
+            const int mask = wgrad_mask(a);
+            const int per_e = (((mask & 1) != 0) + ((mask & 2) != 0)) * (a.F / C::kTileM) * (a.H / kBN) +
+                              ((mask & 4) != 0) * (a.H / C::kTileM) * (a.F / kBN);
             for (int e = 0; e < a.E_local; ++e) {
                 acc += per_e;
                 prefix[e + 1] = acc;
@@ -1097,7 +1103,7 @@ static thread_local int g_max_ctas = kNumSMs;
 static thread_local int g_debug = 0;
 
 template <int kMode, int kCG>
-static int launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s) {
+static int launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s, int grid_ctas = 0) {
     using G = Geo<kMode, kCG>;
     static_assert(G::kSmemBytes <= 227 * 1024, "shared memory plan exceeds 227 KB");
     auto kern = moe_gemm_kernel<kMode, kCG>;
@@ -1107,7 +1113,11 @@ static int launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s) {
         return B200MOE_ERR_CUDA;
     }
     cudaLaunchConfig_t cfg = {};
-    int grid = g_max_ctas - (g_max_ctas % kCG);
+    // persistent grid: one CTA per SM, or `grid_ctas` (a per-call request, e.g.
+    // to co-run two GEMMs on disjoint halves of the chip), or the diagnostics knob
+    const int want = grid_ctas > 0 ? (grid_ctas < g_max_ctas ? grid_ctas : g_max_ctas) : g_max_ctas;
+    int grid = want - (want % kCG);
+    if (grid < kCG) grid = kCG;
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kNumThreads);
     cfg.dynamicSmemBytes = G::kSmemBytes;
@@ -1130,8 +1140,8 @@ static int launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s) {
 }
 
 template <int kMode>
-static int dispatch_launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s) {
-    return g_cta_group == 2 ? launch<kMode, 2>(tm, a, s) : launch<kMode, 1>(tm, a, s);
+static int dispatch_launch(const TmaSet& tm, const GemmArgs& a, cudaStream_t s, int grid_ctas = 0) {
+    return g_cta_group == 2 ? launch<kMode, 2>(tm, a, s, grid_ctas) : launch<kMode, 1>(tm, a, s, grid_ctas);
 }
 
 static int check_common(int nseg, int H, int F, int E_local) {
@@ -1208,6 +1218,14 @@ int b200moe_expert_fwd2(const void* h, const void* w2, const int* seg_base, cons
 int b200moe_expert_bwd2(const void* dout, const void* w2, const void* a_pre, const void* b_pre, const int* seg_base,
                         const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
                         void* da_out, void* db_out, cudaStream_t stream) {
+    return b200moe_expert_bwd2_ex(dout, w2, a_pre, b_pre, seg_base, seg_count, seg_expert, nseg, rows, H, F, E_local,
+                                  da_out, db_out, 0, stream);
+}
+
+int b200moe_expert_bwd2_ex(const void* dout, const void* w2, const void* a_pre, const void* b_pre,
+                           const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                           int H, int F, int E_local, void* da_out, void* db_out, int grid_ctas,
+                           cudaStream_t stream) {
     B200_TRY(check_common(nseg, H, F, E_local));
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], dout, H, rows, H, false));
@@ -1221,12 +1239,19 @@ int b200moe_expert_bwd2(const void* dout, const void* w2, const void* a_pre, con
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)da_out, (__nv_bfloat16*)db_out, nullptr,
                   (const __nv_bfloat16*)a_pre, (const __nv_bfloat16*)b_pre};
-    return dispatch_launch<kBwd2>(tm, a, stream);
+    return dispatch_launch<kBwd2>(tm, a, stream, grid_ctas);
 }
 
 int b200moe_expert_bwd1(const void* da, const void* db, const void* w1, const void* w3, const int* seg_base,
                         const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
                         void* dxp_out, cudaStream_t stream) {
+    return b200moe_expert_bwd1_ex(da, db, w1, w3, seg_base, seg_count, seg_expert, nseg, rows, H, F, E_local, dxp_out,
+                                  0, stream);
+}
+
+int b200moe_expert_bwd1_ex(const void* da, const void* db, const void* w1, const void* w3, const int* seg_base,
+                           const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
+                           void* dxp_out, int grid_ctas, cudaStream_t stream) {
     B200_TRY(check_common(nseg, H, F, E_local));
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], da, F, rows, F, false));
@@ -1238,7 +1263,7 @@ int b200moe_expert_bwd1(const void* da, const void* db, const void* w1, const vo
     tm.st[1] = tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dxp_out, nullptr, nullptr, nullptr, nullptr};
-    return dispatch_launch<kBwd1>(tm, a, stream);
+    return dispatch_launch<kBwd1>(tm, a, stream, grid_ctas);
 }
 
 int b200moe_expert_wgrad(const void* xp, const void* h, const void* dout, const void* da, const void* db,
@@ -1252,6 +1277,15 @@ int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, co
                              const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
                              int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate,
                              cudaStream_t stream) {
+    return b200moe_expert_wgrad_ex(xp, h, dout, da, db, seg_base, seg_count, seg_expert, nseg, rows, H, F, E_local,
+                                   dw1, dw2, dw3, accumulate, 7, 0, stream);
+}
+
+int b200moe_expert_wgrad_ex(const void* xp, const void* h, const void* dout, const void* da, const void* db,
+                            const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                            int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate, int subs,
+                            int grid_ctas, cudaStream_t stream) {
+    B200_CHECK_ARG(subs >= 1 && subs <= 7, B200MOE_ERR_CONFIG, "wgrad sub-problem mask %d outside [1, 7]", subs);
     B200_TRY(check_common(nseg, H, F, E_local));
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], dout, H, rows, H, true));
@@ -1265,14 +1299,15 @@ int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, co
     B200_TRY(make_map(&tm.st[2], dw3, H, (uint64_t)E_local * F, H, false, true, wide));
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)dw1, (__nv_bfloat16*)dw2, (__nv_bfloat16*)dw3, nullptr, nullptr};
-    if (accumulate) return dispatch_launch<kWgradAcc>(tm, a, stream);   // adds into the existing gradients
+    a.wgrad_subs = subs;
+    if (accumulate) return dispatch_launch<kWgradAcc>(tm, a, stream, grid_ctas);   // adds into the existing gradients
     // Wide tiles (shared-operand accumulator pairs) are opt-in (GemmArgs.debug
     // bit 8 = 256, CTA pairs, F % 512 == 0): bit-identical and 25% less operand
     // traffic, but measured inside the layer step WGRAD takes 2.36-2.41 ms vs
     // 2.27-2.32 ms with the double-buffered one-accumulator tiles (standalone:
     // 2.10 ms both; 1.77 vs 1.82 ms without the weight-gradient stores).
-    if (g_cta_group == 2 && F % 512 == 0 && (g_debug & 256)) return launch<kWgradW, 2>(tm, a, stream);
-    return dispatch_launch<kWgrad>(tm, a, stream);
+    if (g_cta_group == 2 && F % 512 == 0 && (g_debug & 256) && subs == 7) return launch<kWgradW, 2>(tm, a, stream);
+    return dispatch_launch<kWgrad>(tm, a, stream, grid_ctas);
 }
 
 }  // extern "C"

@@ -655,18 +655,20 @@ class _MoEFunction(torch.autograd.Function):
                   seg_base.data_ptr(), counts.data_ptr(), T, H, E, dO.data_ptr(), dg.data_ptr(), s)
         dA = torch.empty(R, F, **bf)
         dB = torch.empty(R, F, **bf)
-        _lib.call("b200moe_expert_bwd2", dO.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
-                  seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E, dA.data_ptr(),
-                  dB.data_ptr(), s)
         dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
-        _wgrad_call(acc, xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(),
-                  dB.data_ptr(), seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E,
-                  dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
+        dxp = torch.empty(R, H, **bf)
+        seg = (seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E)
+        wg_args = (xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(), dB.data_ptr()) + seg + \
+            (dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), int(acc))
+        # serial BWD2 -> WGRAD -> BWD1, each on the whole chip (co-running WGRAD
+        # beside BWD1 / dW2 beside BWD2 on split CTA budgets measured slower)
+        _lib.call("b200moe_expert_bwd2", dO.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(), *seg,
+                  dA.data_ptr(), dB.data_ptr(), s)
+        _wgrad_call(acc, *wg_args[:-1], s)
+        _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(), *seg,
+                  dxp.data_ptr(), s)
         if acc:
             dW1 = dW2 = dW3 = None
-        dxp = torch.empty(R, H, **bf)
-        _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
-                  seg_base.data_ptr(), counts.data_ptr(), seg_e.data_ptr(), E, R, H, F, E, dxp.data_ptr(), s)
         dx = torch.empty(T, H, **bf)
         dh = torch.empty(T, E, **f32)
         dn = torch.empty(T, E, **f32) if z is not None else None
