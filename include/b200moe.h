@@ -232,6 +232,24 @@ int b200moe_expert_wgrad_ex(const void* xp, const void* h, const void* dout, con
                             int H, int F, int E_local, void* dw1, void* dw2, void* dw3, int accumulate, int subs,
                             int grid_ctas, cudaStream_t stream);
 
+/* Dense GEMMs of the transformer step around the layer (qkv / wo / lm-head,
+ * reference model.py:135-169 via tensor.py:192-207 matmul) on the same
+ * tcgen05 kernel, weights in the reference [in, out] layout w [K, N]:
+ *   fwd   y[M,N]  = x[M,K] . w        (ld* = row pitches in elements)
+ *   dgrad dx[M,K] = dy[M,N] . w^T
+ *   wgrad dw[K,N] = x^T . dy          (lddw must equal N)
+ * bf16 in / out, fp32 accumulation; K and N multiples of 256, any M >= 1.
+ * seg_base / seg_count / seg_expert: a device segment table of one segment
+ * {0, M, 0} (int32). */
+int b200moe_dense_fwd(const void* x, const void* w, const int* seg_base, const int* seg_count, const int* seg_expert,
+                      int M, int K, int N, int ldx, int ldw, int ldy, void* y, cudaStream_t stream);
+int b200moe_dense_dgrad(const void* dy, const void* w, const int* seg_base, const int* seg_count,
+                        const int* seg_expert, int M, int K, int N, int lddy, int ldw, int lddx, void* dx,
+                        cudaStream_t stream);
+int b200moe_dense_wgrad(const void* x, const void* dy, const int* seg_base, const int* seg_count,
+                        const int* seg_expert, int M, int K, int N, int ldx, int lddy, int lddw, void* dw,
+                        cudaStream_t stream);
+
 /* Diagnostics knobs for tests and A/B tools, NOT part of the product path:
  * thread-local (they affect only GEMM launches issued by the calling thread;
  * other threads always run the defaults), so the entry points above stay

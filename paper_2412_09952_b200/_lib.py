@@ -58,6 +58,9 @@ SIGNATURES = {
     "b200moe_expert_bwd2_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P],
     "b200moe_expert_bwd1_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P],
     "b200moe_expert_wgrad_ex": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P],
+    "b200moe_dense_fwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
+    "b200moe_dense_dgrad": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
+    "b200moe_dense_wgrad": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
     "b200moe_gemm_set_cta_group": [_I],
     "b200moe_gemm_set_max_ctas": [_I],
     "b200moe_gemm_set_debug": [_I],
@@ -119,6 +122,7 @@ KERNELS_PER_CALL = {
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_expert_wgrad_acc": 1,
     "b200moe_expert_bwd1_ex": 1, "b200moe_expert_wgrad_ex": 1, "b200moe_expert_bwd2_ex": 1,
+    "b200moe_dense_fwd": 1, "b200moe_dense_dgrad": 1, "b200moe_dense_wgrad": 1,
     "b200moe_upcycle_copy": 3,
     "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 2,
     "b200moe_rmsnorm_fwd": 1, "b200moe_rmsnorm_bwd": 2, "b200moe_embedding_fwd": 1, "b200moe_embedding_bwd": 1,

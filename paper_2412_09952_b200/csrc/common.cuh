@@ -18,6 +18,10 @@ namespace b200moe {
 // Thread-local error message behind b200moe_last_error().
 void set_error(const char* fmt, ...);
 
+// Make the current device's primary context current on this thread (for
+// driver-API calls on a thread that has made no runtime call yet).
+bool bind_current_context();
+
 // 2-D bf16 TMA map over a row-major [outer, inner] tensor (row pitch ld
 // elements), box {box_inner, box_outer}, no swizzle (rows land contiguous in
 // shared memory), out-of-bounds rows zero-filled.  Returns a B200MOE_* code.

@@ -84,6 +84,7 @@ struct GemmArgs {
     const __nv_bfloat16* in1;
     int debug;  // bit 0: skip wgrad epilogue stores (diagnostics only)
     int wgrad_subs;  // WGRAD sub-problems to compute: bit 0 dW1, bit 1 dW3, bit 2 dW2 (0 = all)
+    int dense;       // BWD1 as a plain dense GEMM: one (A, B) pair, K = F (0 = the two-pair expert BWD1)
 };
 
 __host__ __device__ __forceinline__ int wgrad_mask(const GemmArgs& a) { return a.wgrad_subs ? a.wgrad_subs : 7; }
@@ -212,7 +213,7 @@ template <int kMode>
 __device__ __forceinline__ int mode_k_blocks(const GemmArgs& a) {
     if constexpr (kMode == kFwd1 || kMode == kBwd2) return a.H / kBK;
     if constexpr (kMode == kFwd2) return a.F / kBK;
-    if constexpr (kMode == kBwd1) return 2 * a.F / kBK;
+    if constexpr (kMode == kBwd1) return (a.dense ? 1 : 2) * a.F / kBK;
     return 0;
 }
 
@@ -1084,9 +1085,13 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ou
         box[1] = 32;
         sw = wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     }
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    auto encode = [&] {
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUresult r = encode();
+    if (r == CUDA_ERROR_INVALID_CONTEXT && bind_current_context()) r = encode();
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d) inner=%llu outer=%llu ld=%llu", (int)r,
                   (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)ld);
@@ -1308,6 +1313,70 @@ int b200moe_expert_wgrad_ex(const void* xp, const void* h, const void* dout, con
     // 2.10 ms both; 1.77 vs 1.82 ms without the weight-gradient stores).
     if (g_cta_group == 2 && F % 512 == 0 && (g_debug & 256) && subs == 7) return launch<kWgradW, 2>(tm, a, stream);
     return dispatch_launch<kWgrad>(tm, a, stream, grid_ctas);
+}
+
+// ------------------------------------------------------------------ dense
+// Plain GEMMs of the transformer step around the MoE layer (qkv / wo / lm-head
+// projections, reference model.py:135-169 through tensor.py:192-207 matmul),
+// on the same kernel template with one segment: weights in the reference
+// [in, out] layout, w [K, N] row-major.
+//   fwd    y[M,N]  = x[M,K] . w          BWD1 mainloop, one pair (A K-major, B MN-major)
+//   dgrad  dx[M,K] = dy[M,N] . w^T       FWD2 mainloop (B = w rows, K-major)
+//   wgrad  dw[K,N] = x^T . dy            WGRAD, dW1 sub-problem only (A, B MN-major)
+// seg_* : device segment table of one segment {base 0, count M, expert 0}.
+static int check_dense(int M, int K, int N) {
+    B200_CHECK_ARG(M >= 1 && K % 256 == 0 && N % 256 == 0 && K > 0 && N > 0, B200MOE_ERR_SHAPE,
+                   "dense GEMM needs K and N multiples of 256 (M=%d K=%d N=%d)", M, K, N);
+    return B200MOE_OK;
+}
+
+int b200moe_dense_fwd(const void* x, const void* w, const int* seg_base, const int* seg_count, const int* seg_expert,
+                      int M, int K, int N, int ldx, int ldw, int ldy, void* y, cudaStream_t stream) {
+    B200_TRY(check_dense(M, K, N));
+    TmaSet tm = {};
+    B200_TRY(make_map(&tm.m[0], x, K, M, ldx, false));
+    B200_TRY(make_map(&tm.m[2], w, N, K, ldw, true));
+    tm.m[1] = tm.m[0];
+    tm.m[3] = tm.m[2];
+    tm.m[4] = tm.m[0];
+    B200_TRY(make_map(&tm.st[0], y, N, M, ldy, false, true));
+    tm.st[1] = tm.st[2] = tm.st[0];
+    GemmArgs a = {seg_base, seg_count, seg_expert, 1, N, K, 1, (__nv_bfloat16*)y, nullptr, nullptr, nullptr, nullptr};
+    a.dense = 1;
+    return dispatch_launch<kBwd1>(tm, a, stream);
+}
+
+int b200moe_dense_dgrad(const void* dy, const void* w, const int* seg_base, const int* seg_count,
+                        const int* seg_expert, int M, int K, int N, int lddy, int ldw, int lddx, void* dx,
+                        cudaStream_t stream) {
+    B200_TRY(check_dense(M, K, N));
+    TmaSet tm = {};
+    B200_TRY(make_map(&tm.m[0], dy, N, M, lddy, false));
+    B200_TRY(make_map(&tm.m[1], w, N, K, ldw, false));
+    tm.m[2] = tm.m[3] = tm.m[4] = tm.m[0];
+    B200_TRY(make_map(&tm.st[0], dx, K, M, lddx, false, true));
+    tm.st[1] = tm.st[2] = tm.st[0];
+    GemmArgs a = {seg_base, seg_count, seg_expert, 1, K, N, 1, (__nv_bfloat16*)dx, nullptr, nullptr, nullptr,
+                  nullptr};
+    return dispatch_launch<kFwd2>(tm, a, stream);
+}
+
+int b200moe_dense_wgrad(const void* x, const void* dy, const int* seg_base, const int* seg_count,
+                        const int* seg_expert, int M, int K, int N, int ldx, int lddy, int lddw, void* dw,
+                        cudaStream_t stream) {
+    B200_TRY(check_dense(M, K, N));
+    B200_CHECK_ARG(lddw == N, B200MOE_ERR_SHAPE, "dense wgrad writes a contiguous [K, N] gradient (ld %d != N %d)",
+                   lddw, N);
+    TmaSet tm = {};
+    B200_TRY(make_map(&tm.m[2], x, K, M, ldx, true));      // "da": output rows = K
+    B200_TRY(make_map(&tm.m[3], dy, N, M, lddy, true));    // "xp": output columns = N
+    tm.m[0] = tm.m[1] = tm.m[4] = tm.m[2];
+    B200_TRY(make_map(&tm.st[0], dw, N, K, lddw, false, true));
+    tm.st[1] = tm.st[2] = tm.st[0];
+    GemmArgs a = {seg_base, seg_count, seg_expert, 1, N, K, 1, (__nv_bfloat16*)dw, nullptr, nullptr, nullptr,
+                  nullptr};
+    a.wgrad_subs = 1;
+    return dispatch_launch<kWgrad>(tm, a, stream);
 }
 
 }  // extern "C"

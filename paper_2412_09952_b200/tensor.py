@@ -390,3 +390,64 @@ def ffn(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, w3: torch.Tensor) -
     W2 = F.pad(w2.t().to(torch.bfloat16), (0, Fp - Fd, 0, Hp - H))[None]
     out = _FFN.apply(xb.contiguous(), W1.contiguous(), W2.contiguous(), W3.contiguous())
     return out[:, :H]
+
+
+# --------------------------------------------------------------------------
+# dense projections (qkv, wo, lm-head) on the tcgen05 kernel
+# --------------------------------------------------------------------------
+
+class _Linear(torch.autograd.Function):
+    """y = x . w with the reference [in, out] weight layout (tensor.py:192-207
+    matmul), bf16 in / out, fp32 accumulation, on the repo's own tcgen05 GEMM
+    (b200moe_dense_fwd / _dgrad / _wgrad).  x [M, K], w [K, N] contiguous bf16,
+    K and N multiples of 256."""
+
+    @staticmethod
+    def forward(ctx, x, w):
+        M, K = x.shape
+        N = w.shape[1]
+        y = torch.empty(M, N, dtype=torch.bfloat16, device=x.device)
+        base, cnt = _one_segment(M, x.device)
+        e0 = _arange_i32(1, x.device)
+        _lib.call("b200moe_dense_fwd", x.data_ptr(), w.data_ptr(), base.data_ptr(), cnt.data_ptr(), e0.data_ptr(),
+                  M, K, N, K, N, N, y.data_ptr(), _lib.stream_ptr())
+        ctx.save_for_backward(x, w)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w = ctx.saved_tensors
+        M, K = x.shape
+        N = w.shape[1]
+        dy = dy.to(torch.bfloat16).contiguous()
+        base, cnt = _one_segment(M, x.device)
+        e0 = _arange_i32(1, x.device)
+        s = _lib.stream_ptr()
+        dx = dw = None
+        if ctx.needs_input_grad[0]:
+            dx = torch.empty(M, K, dtype=torch.bfloat16, device=x.device)
+            _lib.call("b200moe_dense_dgrad", dy.data_ptr(), w.data_ptr(), base.data_ptr(), cnt.data_ptr(),
+                      e0.data_ptr(), M, K, N, N, N, K, dx.data_ptr(), s)
+        if ctx.needs_input_grad[1]:
+            dw = torch.empty(K, N, dtype=torch.bfloat16, device=x.device)
+            _lib.call("b200moe_dense_wgrad", x.data_ptr(), dy.data_ptr(), base.data_ptr(), cnt.data_ptr(),
+                      e0.data_ptr(), M, K, N, K, N, N, dw.data_ptr(), s)
+        return dx, dw
+
+
+def linear(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """Differentiable x @ w (reference [in, out] weight layout) on the tcgen05
+    dense GEMM; bf16 result.  K / N that are not multiples of 256 are padded
+    with zeros (exact)."""
+    _require_cuda(x, "x")
+    if x.dim() != 2 or w.dim() != 2 or x.shape[1] != w.shape[0]:
+        raise ShapeError(f"linear shapes disagree: x {tuple(x.shape)}, w {tuple(w.shape)}")
+    K, N = w.shape
+    Kp, Np = _pad_to(K, GEMM_ALIGN), _pad_to(N, GEMM_ALIGN)
+    xb = x.to(torch.bfloat16)
+    wb = w.to(torch.bfloat16)
+    if Kp != K or Np != N:
+        xb = F.pad(xb, (0, Kp - K))
+        wb = F.pad(wb, (0, Np - N, 0, Kp - K))
+    y = _Linear.apply(xb.contiguous(), wb.contiguous())
+    return y[:, :N] if Np != N else y
