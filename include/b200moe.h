@@ -178,9 +178,11 @@ int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int3
 
 /* Router weight gradients: dW_g = x^T.dh, dW_noise = x^T.dn (fp32, [H,E]),
  * deterministic (fixed-order partial sums).  workspace: >= ceil(T/64)*H*E
- * floats. */
+ * floats.  tickets (nullable): ceil(H/256) int32, zeroed once and left zeroed
+ * -- with it (E <= 8) the last block of each hidden block finishes the
+ * reduction in the same launch; without it a second kernel does. */
 int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T, int H, int E, float* dw_g,
-                         float* dw_noise, float* workspace, cudaStream_t stream);
+                         float* dw_noise, float* workspace, int32_t* tickets, cudaStream_t stream);
 
 /* Importance (CV^2) penalty, tensor.py:503-521: loss = var(imp)/mean(imp)^2
  * with imp = sum_t gates[t,:].  Forward writes imp [E] and loss [1] (fp32);

@@ -40,7 +40,7 @@ SIGNATURES = {
     "b200moe_combine_bwd": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P],
     "b200moe_router_bwd": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I,
                            _P, _P, _P, _P, _P],
-    "b200moe_router_wgrad": [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P],
+    "b200moe_router_wgrad": [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P],
     "b200moe_permute_peer": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P],
     "b200moe_combine_peer": [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P],
     "b200moe_combine_bwd_peer": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P],
@@ -118,13 +118,13 @@ def exported_symbols() -> list[str]:
 # Kernel launches issued by each entry point (for the bench's gpu_launches).
 KERNELS_PER_CALL = {
     "b200moe_router_fwd": 1, "b200moe_gate_from_logits": 1, "b200moe_gate_bwd": 1, "b200moe_router_logits_bwd": 6, "b200moe_dispatch": 1, "b200moe_permute": 1,
-    "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 2, "b200moe_router_wgrad": 2,
+    "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 1, "b200moe_router_wgrad": 1,
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_expert_wgrad_acc": 1,
     "b200moe_expert_bwd1_ex": 1, "b200moe_expert_wgrad_ex": 1, "b200moe_expert_bwd2_ex": 1,
     "b200moe_dense_fwd": 1, "b200moe_dense_dgrad": 1, "b200moe_dense_wgrad": 1,
     "b200moe_upcycle_copy": 3,
-    "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 2,
+    "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 1,
     "b200moe_rmsnorm_fwd": 1, "b200moe_rmsnorm_bwd": 2, "b200moe_embedding_fwd": 1, "b200moe_embedding_bwd": 1,
     "b200moe_embedding_bwd_sorted": 1,
     "b200moe_cross_entropy_fwd": 2, "b200moe_cross_entropy_bwd": 1, "b200moe_optimizer_step": 1,

@@ -735,18 +735,26 @@ dispatch_scan_kernel(const float* __restrict__ gates, int T, int E, int capacity
     __syncthreads();
     if (!last_sh) return;
     __threadfence();
-    if (threadIdx.x < E) {
-        const int e = threadIdx.x;
+    // warp w reduces experts w, w + 8, ...: lane l sums tiles l, l + 32, ...
+    // (L2 loads, all in flight together), then a butterfly -- a fixed order
+    for (int e = warp; e < E; e += kWarps) {
         float a = 0.f, b = 0.f;
-        const volatile float2* vp = part;
-        for (int j = 0; j < ntiles; ++j) {
-            a += vp[(size_t)j * EP + e].x;
-            b += vp[(size_t)j * EP + e].y;
+        for (int j = lane; j < ntiles; j += 32) {
+            const float2 v = __ldcg(part + (size_t)j * EP + e);
+            a += v.x;
+            b += v.y;
         }
-        importance[e] = a;
-        gate_mass[e] = b;
-        const int tot_e = ((volatile int32_t*)ws)[8 + e];
-        counts[e] = dropless ? tot_e : min(tot_e, capacity);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (lane == 0) {
+            importance[e] = a;
+            gate_mass[e] = b;
+            const int tot_e = __ldcg(ws + 8 + e);
+            counts[e] = dropless ? tot_e : min(tot_e, capacity);
+        }
     }
     __syncthreads();
     __threadfence();

@@ -128,36 +128,106 @@ constexpr int kDxThreads = 256;
 // ring evicts the 128 KB W_g table from L1.
 __host__ __device__ constexpr int dx_tokens_per_warp(int ep) { return 32 / ep; }
 
-template <int EP, int KM, bool kNoise>
+// Inputs of the softmax' step when it is fused into the dx kernel (the
+// per-token pass of router_dh_kernel done by the warp that owns the token).
+struct DhIn {
+    const int32_t* slot_rank;
+    const int32_t* seg_base;
+    const float* dg;
+    const float* dgx;
+    int64_t sx_t, sx_e;
+    const float* gates;
+    const float* probs;
+    const float* z;
+    const float* noise_act;
+    int router_type;
+    int e_per_rank;
+};
+
+template <int EP, int KM, bool kNoise, bool kFused = false>
 __global__ void __launch_bounds__(kDxThreads)
 router_dx_kernel(const __nv_bfloat16* __restrict__ dxp_local, const uint64_t* __restrict__ dxp_bufs,
                  const int32_t* __restrict__ rows_in,
-                 const float* __restrict__ dh, const float* __restrict__ dn, const float4* __restrict__ wsw,
-                 const float4* __restrict__ wnsw, int T, int H, int E, __nv_bfloat16* __restrict__ dx) {
+                 float* __restrict__ dh, float* __restrict__ dn, const float4* __restrict__ wsw,
+                 const float4* __restrict__ wnsw, int T, int H, int E, __nv_bfloat16* __restrict__ dx,
+                 const DhIn din) {
     constexpr int TT = dx_tokens_per_warp(EP);
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (kDxThreads / 32) + (threadIdx.x >> 5);
     const int t0 = gw * TT;
     if (t0 >= T) return;
     const int HB = H / 8;
+    const int t_l = t0 + lane / EP, e_l = lane % EP;              // this lane's (token, expert)
+    const bool live = lane < TT * EP && t_l < T && e_l < E;
+    int rr[TT][KM];
+    float v = 0.f, w = 0.f;
+    if constexpr (kFused) {
+        // softmax' of this lane's entry, bit-identical to router_dh_kernel: the
+        // row dot product is the same sequential fmaf chain over e, evaluated by
+        // every lane of the token's EP-lane group from shuffled values
+        const size_t i = (size_t)t_l * E + e_l;
+        float gt = 0.f, pv = 0.f, geff = 0.f;
+        int rk = -1;
+        if (live) {
+            gt = din.dg[i];
+            if (din.dgx) gt += din.dgx[(int64_t)t_l * din.sx_t + (int64_t)e_l * din.sx_e];
+            const float gv = din.gates[i];
+            pv = (din.router_type == B200MOE_ROUTER_MIXTRAL) ? gv : din.probs[i];
+            const bool topk = gv > 0.f;
+            geff = (din.router_type == B200MOE_ROUTER_MIXTRAL) ? (pv > 0.f ? gt : 0.f) : (topk ? gt : 0.f);
+            rk = din.slot_rank[i];
+        }
+        const int gbase = (lane / EP) * EP;
+        float dot = 0.f;
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+            const float pe = __shfl_sync(0xffffffffu, pv, gbase + e);
+            const float ge = __shfl_sync(0xffffffffu, geff, gbase + e);
+            if (e < E) dot = fmaf(pe, ge, dot);
+        }
+        float dhv = pv * (geff - dot);
+        if (din.router_type == B200MOE_ROUTER_MIXTRAL && !(pv > 0.f)) dhv = 0.f;
+        v = live ? dhv : 0.f;
+        if (live) dh[i] = dhv;
+        if constexpr (kNoise) {
+            if (live) {
+                w = dhv * din.z[i] * (1.0f / (1.0f + expf(-din.noise_act[i])));
+                dn[i] = w;
+            }
+        }
+        // the token's kept rows in ascending expert order (row handles as in router_dh_kernel)
+        const int handle = rk >= 0 ? (((e_l / din.e_per_rank) << kRowBits) | (din.seg_base[e_l] + rk)) : -1;
+        const unsigned kept = __ballot_sync(0xffffffffu, rk >= 0);
+        const unsigned gmask = (EP == 32) ? 0xffffffffu : (((1u << EP) - 1u) << gbase);
+        const int pos = __popc(kept & gmask & ((1u << lane) - 1u));   // rank among the group's kept lanes
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const unsigned m = __ballot_sync(0xffffffffu, rk >= 0 && pos == j);
+#pragma unroll
+            for (int tt = 0; tt < TT; ++tt) {
+                const unsigned gm = (EP == 32) ? 0xffffffffu : (((1u << EP) - 1u) << (tt * EP));
+                const unsigned mm = m & gm;
+                const int src = mm ? (__ffs(mm) - 1) : 0;
+                const int hv = __shfl_sync(0xffffffffu, handle, src);
+                rr[tt][j] = mm ? hv : -1;
+            }
+        }
+    } else {
+        v = live ? dh[(size_t)t_l * E + e_l] : 0.f;
+        w = (kNoise && live) ? dn[(size_t)t_l * E + e_l] : 0.f;
+#pragma unroll
+        for (int tt = 0; tt < TT; ++tt)
+#pragma unroll
+            for (int j = 0; j < KM; ++j)
+                rr[tt][j] = (rows_in && t0 + tt < T) ? rows_in[(size_t)(t0 + tt) * KM + j] : -1;
+    }
     // (token, expert) values broadcast to every lane
     float dhall[TT * EP], dnall[TT * EP];
-    {
-        const int t = t0 + lane / EP, e = lane % EP;
-        const bool live = lane < TT * EP && t < T && e < E;
-        const float v = live ? dh[(size_t)t * E + e] : 0.f;
-        const float w = (kNoise && live) ? dn[(size_t)t * E + e] : 0.f;
 #pragma unroll
-        for (int i = 0; i < TT * EP; ++i) {
-            dhall[i] = __shfl_sync(0xffffffffu, v, i);
-            if constexpr (kNoise) dnall[i] = __shfl_sync(0xffffffffu, w, i);
-        }
+    for (int i = 0; i < TT * EP; ++i) {
+        dhall[i] = __shfl_sync(0xffffffffu, v, i);
+        if constexpr (kNoise) dnall[i] = __shfl_sync(0xffffffffu, w, i);
     }
-    int rr[TT][KM];
-#pragma unroll
-    for (int tt = 0; tt < TT; ++tt)
-#pragma unroll
-        for (int j = 0; j < KM; ++j) rr[tt][j] = (rows_in && t0 + tt < T) ? rows_in[(size_t)(t0 + tt) * KM + j] : -1;
 
     for (int hb = lane; hb < HB; hb += 32) {
         float acc[TT][8];
@@ -307,7 +377,7 @@ constexpr int kRgConsumers = 8;
 template <int EP>
 __global__ void __launch_bounds__((kRgConsumers + 1) * 32, 2)
 router_wgrad_ring(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ d, int T, int H, int E,
-                  float* __restrict__ part) {
+                  float* __restrict__ part, float* __restrict__ out, int32_t* __restrict__ tickets) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
     __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(sm_raw);
     float* ds = reinterpret_cast<float*>(sm_raw + kRgStages * kRgStageBytes);       // [kRgTok][EP]
@@ -421,6 +491,32 @@ router_wgrad_ring(const __grid_constant__ CUtensorMap xmap, const float* __restr
         for (int w = 0; w < kRgConsumers; ++w) sum += red[(size_t)w * 256 * EP + i];
         if (e < E && hh < hw) p[(size_t)(h0 + hh) * E + e] = sum;
     }
+    if (tickets == nullptr) return;        // reduce_partials follows
+    // the last chunk block of this hidden block sums the chunks' partials in
+    // chunk order (same order as reduce_partials) and resets its ticket
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1) == (int)gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int nch = gridDim.y;
+    for (int i = threadIdx.x; i < hw * E; i += blockDim.x) {
+        const size_t o = (size_t)h0 * E + i;
+        float sum = 0.f;
+        int c = 0;
+        for (; c + 8 <= nch; c += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = __ldcg(part + (size_t)(c + j) * H * E + o);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sum += v[j];
+        }
+        for (; c < nch; ++c) sum += __ldcg(part + (size_t)c * H * E + o);
+        out[o] = sum;
+    }
+    if (threadIdx.x == 0) tickets[blockIdx.x] = 0;
 }
 
 __global__ void reduce_partials(const float* __restrict__ part, int nchunks, size_t n, float* __restrict__ out) {
@@ -538,19 +634,18 @@ int router_bwd_impl(const void* dxp, const uint64_t* dxp_bufs, int e_per_rank, c
         if (wn_swz) wnsw = reinterpret_cast<float4*>(const_cast<float*>(wn_swz));
         else swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
     }
-    router_dh_kernel<EP, KM><<<ceil_div(T, 256), 256, 0, stream>>>(slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates,
-                                                                    probs, z, noise_act, T, E, router_type, dh,
-                                                                    noise ? dn : nullptr, rows, e_per_rank);
+    (void)rows;
+    // softmax' + kept-row lists fused into the dx pass (one launch: each warp
+    // derives its tokens' dh / dn rows before streaming their dxp rows)
+    const DhIn din{slot_rank, seg_base, dg, dgx, sx_t, sx_e, gates, probs, z, noise_act, router_type, e_per_rank};
     constexpr int TT = dx_tokens_per_warp(EP);
     const int grid = ceil_div(ceil_div(T, TT), kDxThreads / 32);
     if (noise)
-        router_dx_kernel<EP, KM, true><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, dxp_bufs, rows,
-                                                                         dh, dn, wsw, wnsw, T, H, E,
-                                                                         (__nv_bfloat16*)dx);
+        router_dx_kernel<EP, KM, true, true><<<grid, kDxThreads, 0, stream>>>(
+            (const __nv_bfloat16*)dxp, dxp_bufs, nullptr, dh, dn, wsw, wnsw, T, H, E, (__nv_bfloat16*)dx, din);
     else
-        router_dx_kernel<EP, KM, false><<<grid, kDxThreads, 0, stream>>>((const __nv_bfloat16*)dxp, dxp_bufs, rows,
-                                                                          dh, dn, wsw, wnsw, T, H, E,
-                                                                          (__nv_bfloat16*)dx);
+        router_dx_kernel<EP, KM, false, true><<<grid, kDxThreads, 0, stream>>>(
+            (const __nv_bfloat16*)dxp, dxp_bufs, nullptr, dh, nullptr, wsw, wnsw, T, H, E, (__nv_bfloat16*)dx, din);
     B200_CHECK_LAUNCH("router_bwd");
     return B200MOE_OK;
 }
@@ -572,7 +667,8 @@ int router_bwd_k(int k, const void* dxp, const uint64_t* dxp_bufs, int e_per_ran
 }
 
 template <int EP>
-int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, float* part, cudaStream_t stream) {
+int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, float* part, cudaStream_t stream,
+               int32_t* tickets = nullptr) {
     int nch = ceil_div(T, kWgTok);
     if constexpr (EP <= 8) {
         nch = ceil_div(T, kRgTok);
@@ -586,7 +682,11 @@ int wgrad_impl(const void* x, const float* d, int T, int H, int E, float* out, f
         auto kern = router_wgrad_ring<EP>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
         dim3 grid(ceil_div(H, 256), nch);
-        kern<<<grid, (kRgConsumers + 1) * 32, sh, stream>>>(xmap, d, T, H, E, part);
+        kern<<<grid, (kRgConsumers + 1) * 32, sh, stream>>>(xmap, d, T, H, E, part, out, tickets);
+        if (tickets) {
+            B200_CHECK_LAUNCH("router_wgrad");
+            return B200MOE_OK;
+        }
     } else {
         dim3 grid(ceil_div(H, 1024), nch);
         router_wgrad_partial<EP><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, d, T, H, E, part);
@@ -617,12 +717,15 @@ int router_logits_bwd_impl(const void* x, const float* dh, const float* w_g, con
         if (noise) swizzle_w_j<EP, 8><<<64, 256, 0, stream>>>(w_noise, H, E, wnsw);
         constexpr int TT = dx_tokens_per_warp(EP);
         const int grid = ceil_div(ceil_div(T, TT), kDxThreads / 32);
+        const DhIn none{};
         if (noise)
-            router_dx_kernel<EP, 1, true><<<grid, kDxThreads, 0, stream>>>(nullptr, nullptr, nullptr, dh, dn, wsw,
-                                                                            wnsw, T, H, E, (__nv_bfloat16*)dx);
+            router_dx_kernel<EP, 1, true><<<grid, kDxThreads, 0, stream>>>(nullptr, nullptr, nullptr,
+                                                                            const_cast<float*>(dh), dn, wsw, wnsw, T,
+                                                                            H, E, (__nv_bfloat16*)dx, none);
         else
-            router_dx_kernel<EP, 1, false><<<grid, kDxThreads, 0, stream>>>(nullptr, nullptr, nullptr, dh, dn, wsw,
-                                                                             wnsw, T, H, E, (__nv_bfloat16*)dx);
+            router_dx_kernel<EP, 1, false><<<grid, kDxThreads, 0, stream>>>(nullptr, nullptr, nullptr,
+                                                                             const_cast<float*>(dh), dn, wsw, wnsw, T,
+                                                                             H, E, (__nv_bfloat16*)dx, none);
     }
     if (dw_g) {
         int rc = wgrad_impl<EP>(x, dh, T, H, E, dw_g, part, stream);
@@ -683,10 +786,10 @@ int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int3
 }
 
 int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T, int H, int E, float* dw_g,
-                         float* dw_noise, float* workspace, cudaStream_t stream) {
+                         float* dw_noise, float* workspace, int32_t* tickets, cudaStream_t stream) {
     B200_CHECK_ARG(T >= 1 && E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "bad T/E (%d, %d)", T, E);
     B200_CHECK_ARG(H % 4 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 4");
-#define CALL(EP, D, O) wgrad_impl<EP>(x, D, T, H, E, O, workspace, stream)
+#define CALL(EP, D, O) wgrad_impl<EP>(x, D, T, H, E, O, workspace, stream, tickets)
     int rc;
     if (E <= 4) rc = CALL(4, dh, dw_g);
     else if (E <= 8) rc = CALL(8, dh, dw_g);

@@ -34,7 +34,7 @@ import torch.distributed as dist
 from . import _lib
 from .errors import ConfigError, ShapeError
 from .moe import (DeviceRoutingStats, GateConfig, SEG_PAD, _acc_targets, _arange_i32, _dispatch_ws, _ep, _noise,
-                  _swizzled, _wgrad_call, _wgrad_outputs, expert_capacity)
+                  _swizzled, _wgrad_call, _wgrad_outputs, _wgrad_tickets, expert_capacity)
 
 
 @dataclass
@@ -258,7 +258,7 @@ class _EPFunction(torch.autograd.Function):
         dwn = torch.empty(H, E, **f32) if z is not None else None
         wsw = torch.empty((T + 63) // 64 * H * E, **f32)
         _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), _lib.ptr(dn), T, H, E, dwg.data_ptr(),
-                  _lib.ptr(dwn), wsw.data_ptr(), s)
+                  _lib.ptr(dwn), wsw.data_ptr(), _wgrad_tickets(dev, H).data_ptr(), s)
         if st.get("reduce_router", True):
             dist.all_reduce(dwg, group=group)
             if dwn is not None:
@@ -485,7 +485,7 @@ class _EPPeerFunction(torch.autograd.Function):
         dwn = torch.empty(H, E, **f32) if z is not None else None
         wsw = torch.empty((T + 63) // 64 * H * E, **f32)
         _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), _lib.ptr(dn), T, H, E, dwg.data_ptr(),
-                  _lib.ptr(dwn), wsw.data_ptr(), s)
+                  _lib.ptr(dwn), wsw.data_ptr(), _wgrad_tickets(dev, H).data_ptr(), s)
         if st.get("reduce_router", True):
             dist.all_reduce(dwg, group=group)
             if dwn is not None:

@@ -293,6 +293,18 @@ def _dispatch_ws(device, T: int) -> torch.Tensor:
     return ws
 
 
+def _wgrad_tickets(device, H: int) -> torch.Tensor:
+    """Per-hidden-block tickets of the router weight-gradient kernel (zeroed
+    once; each launch leaves them zeroed), one buffer per (device, stream)."""
+    key = ("wg_tickets", device, torch.cuda.current_stream(device).cuda_stream)
+    t = _CACHE.get(key)
+    n = (H + 255) // 256
+    if t is None or t.numel() < n:
+        t = torch.zeros(n, dtype=torch.int32, device=device)
+        _CACHE[key] = t
+    return t
+
+
 def _arange_i32(n: int, device) -> torch.Tensor:
     key = ("arange", n, device)
     t = _CACHE.get(key)
@@ -686,7 +698,7 @@ class _MoEFunction(torch.autograd.Function):
         dwn = torch.empty(H, E, **f32) if z is not None else None
         wsw = torch.empty((T + 63) // 64 * H * E, **f32)
         _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), _lib.ptr(dn), T, H, E, dwg.data_ptr(),
-                  _lib.ptr(dwn), wsw.data_ptr(), s)
+                  _lib.ptr(dwn), wsw.data_ptr(), _wgrad_tickets(dev, H).data_ptr(), s)
         if st.routing is not None:   # router-logit gradients, for inspection (out.routing["dh"])
             st.routing["dh"], st.routing["dn"] = dh, dn
         return dx, dwg, dwn, dW1, dW2, dW3, None, None

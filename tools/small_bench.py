@@ -68,7 +68,7 @@ cases = {
                                                      E, k, 0,
                                                      dx.data_ptr(), dh.data_ptr(), None, ws.data_ptr(), s)),
     "router_wgrad": (MB, lambda: _lib.call("b200moe_router_wgrad", x.data_ptr(), dh.data_ptr(), None, T, H, E,
-                                           dwg.data_ptr(), None, wsw.data_ptr(), s)),
+                                           dwg.data_ptr(), None, wsw.data_ptr(), None, s)),
 }
 res = {}
 for name, (nbytes, fn) in cases.items():
