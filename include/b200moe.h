@@ -67,11 +67,16 @@ int b200moe_version(void);
  * softmax s; may be NULL for mixtral.  noise_act = x.W_noise (needed by the
  * backward; NULL when z == NULL).  err_flag (nullable): set to 1 on a GateError
  * row (callers of the layer read it from the dispatch stats instead).
- * workspace: >= 2*H*E_pad floats; on return
+ * E <= 16 and H % 64 == 0 run on the tensor cores (x . W with W split into
+ * three bf16 parts, fp32 accumulation); otherwise on the CUDA cores.
+ * workspace: b200moe_router_workspace_floats(H, E) floats; on return
  * it holds the swizzled W_g (and W_noise) tables b200moe_router_bwd can reuse. */
 int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E,
                        int k, int router_type, float* logits, float* gates, float* probs, float* noise_act,
                        float* workspace, int32_t* err_flag, cudaStream_t stream);
+
+size_t b200moe_router_workspace_floats(int H, int E);
+int b200moe_router_set_fma(int on);   /* diagnostics (thread-local): 1 = CUDA-core K1 even where tcgen05 applies */
 
 /* Gating only, from given fp32 logits (moe.py:152-186).  Used to check the
  * device gate arithmetic against the reference's own gates bit-for-bit.

@@ -35,6 +35,8 @@ SIGNATURES = {
     "b200moe_router_logits_bwd": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P],
     "b200moe_dispatch": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "b200moe_dispatch_workspace_words": [_I],
+    "b200moe_router_workspace_floats": [_I, _I],
+    "b200moe_router_set_fma": [_I],
     "b200moe_permute": [_P, _P, _P, _P, _I, _I, _I, _P, _P],
     "b200moe_combine": [_P, _P, _P, _P, _I, _I, _I, _P, _P],
     "b200moe_combine_bwd": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P],
@@ -105,6 +107,7 @@ def load() -> ctypes.CDLL:
                 fn.restype = ctypes.c_int
             lib.b200moe_crc32c_workspace_bytes.restype = ctypes.c_longlong
             lib.b200moe_dispatch_workspace_words.restype = ctypes.c_size_t
+            lib.b200moe_router_workspace_floats.restype = ctypes.c_size_t
             lib.b200moe_last_error.argtypes = []
             lib.b200moe_last_error.restype = ctypes.c_char_p
             _lib = lib
@@ -117,7 +120,7 @@ def exported_symbols() -> list[str]:
 
 # Kernel launches issued by each entry point (for the bench's gpu_launches).
 KERNELS_PER_CALL = {
-    "b200moe_router_fwd": 1, "b200moe_gate_from_logits": 1, "b200moe_gate_bwd": 1, "b200moe_router_logits_bwd": 6, "b200moe_dispatch": 1, "b200moe_permute": 1,
+    "b200moe_router_fwd": 2, "b200moe_gate_from_logits": 1, "b200moe_gate_bwd": 1, "b200moe_router_logits_bwd": 6, "b200moe_dispatch": 1, "b200moe_permute": 1,
     "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 1, "b200moe_router_wgrad": 1,
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_expert_wgrad_acc": 1,

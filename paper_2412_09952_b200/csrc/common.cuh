@@ -24,9 +24,10 @@ bool bind_current_context();
 
 // 2-D bf16 TMA map over a row-major [outer, inner] tensor (row pitch ld
 // elements), box {box_inner, box_outer}, no swizzle (rows land contiguous in
-// shared memory), out-of-bounds rows zero-filled.  Returns a B200MOE_* code.
+// shared memory) or the 128-byte swizzle of K-major tcgen05 operands,
+// out-of-bounds rows zero-filled.  Returns a B200MOE_* code.
 int make_tmap_bf16_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
-                      uint32_t box_inner, uint32_t box_outer);
+                      uint32_t box_inner, uint32_t box_outer, bool sw128 = false);
 
 #define B200_CHECK_ARG(cond, code, ...)          \
     do {                                         \

@@ -9,6 +9,7 @@
 //                             by gate (stable, position breaks ties)
 // The gate arithmetic reproduces numpy float32 bit-for-bit: numpy's exp
 // (npexp.cuh), its pairwise row sum, IEEE division, no FTZ.
+#include <atomic>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <math.h>
@@ -292,6 +293,203 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__
             if (probs) probs[(size_t)t_mine * E + e_mine] = pe;
             if (!ok && e_mine == 0 && err_flag) atomicExch(err_flag, 1);
         }
+    }
+}
+
+// ---------------------------------------------------------------- K1 on tcgen05
+// The router GEMV h = x . W_g (+ x . W_noise) on the tensor cores.  W (fp32)
+// is split into three bf16 parts, W = W_hi + W_mid + W_lo, each the bf16
+// rounding of what the previous parts leave (together within 2^-24 of W); x
+// is bf16, so every product x * W_s is exact and the MMA accumulates in fp32.
+// B = [W_hi | W_mid | W_lo (| noise parts)]^T is stacked along N, so a CTA's
+// accumulator row t holds x_t . W_s[:, e] in column s*EP + e; the epilogue adds
+// the parts smallest first and runs the gating of K1 on its token.  A CTA owns
+// 128 tokens: x streams through an 8-deep TMA ring (SWIZZLE_128B, 64 hidden per
+// stage), one thread issues 4 MMAs (K = 16) per stage, and the 128 threads of
+// the epilogue each own one token (TMEM lane).  The CUDA-core K1 above stays
+// for E > 16 (N would exceed the TMEM budget of this layout).
+template <int EP, bool kNoise>
+struct RtcCfg {
+    static constexpr int NB = ((3 * EP + 15) / 16) * 16;   // B rows per matrix (3 splits, padded)
+    static constexpr int N = kNoise ? 2 * NB : NB;
+    static constexpr int kStages = 8;
+    static constexpr int kABytes = 128 * 64 * 2;         // 16 KB of x per stage
+    static constexpr int kBBytes = N * 64 * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kTmemCols = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// W_g / W_noise [H, E] fp32 -> the bf16 split table B [N, H] (row s*EP + e of
+// matrix block m: part s of column e; unused rows zero) and the swizzled fp32
+// tables the router backward reads (same layout as swizzle_w_kernel).
+template <int EP, bool kNoise>
+__global__ void router_wsplit_kernel(const float* __restrict__ w_g, const float* __restrict__ w_n, int H, int E,
+                                     __nv_bfloat16* __restrict__ bsplit, float4* __restrict__ wsw,
+                                     float4* __restrict__ wnsw) {
+    using C = RtcCfg<EP, kNoise>;
+    const int HB = H / 8;
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int m = 0; m < (kNoise ? 2 : 1); ++m) {
+            const float* w = m == 0 ? w_g : w_n;
+            float v[EP];
+#pragma unroll
+            for (int e = 0; e < EP; ++e) v[e] = (e < E) ? w[(size_t)h * E + e] : 0.f;
+            __nv_bfloat16* b = bsplit + (size_t)m * C::NB * H;
+#pragma unroll
+            for (int e = 0; e < EP; ++e) {
+                const __nv_bfloat16 hi = __float2bfloat16_rn(v[e]);
+                const float r1 = v[e] - __bfloat162float(hi);
+                const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+                const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+                b[(size_t)e * H + h] = hi;
+                b[(size_t)(EP + e) * H + h] = mid;
+                b[(size_t)(2 * EP + e) * H + h] = lo;
+            }
+            for (int r = 3 * EP; r < C::NB; ++r) b[(size_t)r * H + h] = __float2bfloat16_rn(0.f);
+            float4* sw = m == 0 ? wsw : wnsw;
+            const int hb = h / 8, j = h % 8;
+#pragma unroll
+            for (int e4 = 0; e4 < EP / 4; ++e4)
+                sw[(j * (EP / 4) + e4) * HB + hb] = make_float4(v[4 * e4], v[4 * e4 + 1], v[4 * e4 + 2], v[4 * e4 + 3]);
+        }
+    }
+}
+
+template <int EP, bool kNoise>
+__global__ void __launch_bounds__(128, 1)
+router_fwd_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
+                     const float* __restrict__ z, int T, int H, int E, int k, int router_type,
+                     float* __restrict__ logits, float* __restrict__ gates, float* __restrict__ probs,
+                     float* __restrict__ noise_act, int32_t* __restrict__ err_flag) {
+    using C = RtcCfg<EP, kNoise>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* done = empty + C::kStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // a cluster of two CTAs shares one 128-token tile: CTA r accumulates the
+    // hidden half r (twice the SMs streaming x), then CTA 1 hands its partial
+    // sums to CTA 0 through distributed shared memory
+    const uint32_t crank = ptx::cluster_ctarank();
+    const int t0 = (int)ptx::cluster_id_x() * 128;
+    const int nkb_all = H / 64;
+    const int kb0 = (int)crank * (nkb_all / 2);
+    const int nkb = crank ? nkb_all - nkb_all / 2 : nkb_all / 2;
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&xmap);
+        ptx::prefetch_tmap(&bmap);
+        for (int s = 0; s < C::kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<1>(tslot, C::kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0 && lane == 0) {            // TMA producer: x tile + split-B tile per stage
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % C::kStages;
+            if (kb >= C::kStages) ptx::mbar_wait(&empty[st], ((kb / C::kStages) - 1) & 1);
+            uint8_t* a = smem + st * C::kStageBytes;
+            ptx::mbar_arrive_expect_tx(&full[st], C::kStageBytes);   // rows beyond T arrive as zeros
+            ptx::tma_load_2d(&xmap, &full[st], a, (kb0 + kb) * 64, t0);
+            ptx::tma_load_2d(&bmap, &full[st], a + C::kABytes, (kb0 + kb) * 64, 0);
+        }
+    } else if (warp == 1 && lane == 0) {     // MMA issuer
+        constexpr uint32_t idesc = ptx::make_idesc_bf16(128, C::N, false, false);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % C::kStages;
+            ptx::mbar_wait(&full[st], (kb / C::kStages) & 1);
+            ptx::tc_fence_after();
+            const uint32_t a = ptx::smem_u32(smem + st * C::kStageBytes);
+            const uint32_t b = a + C::kABytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                ptx::mma_bf16<1>(tmem, ptx::make_sdesc(a + kk * 32, 16, 1024), ptx::make_sdesc(b + kk * 32, 16, 1024),
+                                 idesc, (kb | kk) != 0);
+            ptx::mma_commit<1>(&empty[st], 1);
+        }
+        ptx::mma_commit<1>(done, 1);
+    }
+    // ---- epilogue: thread i owns token t0 + i (TMEM lane i)
+    ptx::mbar_wait(done, 0);
+    ptx::tc_fence_after();
+    constexpr int kLoads = (C::N + 31) / 32;
+    uint32_t d[kLoads * 32];
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+    for (int c = 0; c < kLoads; ++c) ptx::tmem_ld_32x32b_x32(lane_addr + c * 32, d + c * 32);
+    ptx::tmem_ld_wait();
+    // cross-CTA reduction over the two hidden halves: both rings are drained
+    // (barrier 1), CTA 1 stores its partials into CTA 0's ring memory
+    // ([column][row] floats, conflict-free), barrier 2, CTA 0 adds them
+    float* red = reinterpret_cast<float*>(smem);
+    ptx::cluster_sync();
+    if (crank == 1) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(ptx::smem_u32(red)));
+#pragma unroll
+        for (int c = 0; c < C::N; ++c)
+            asm volatile("st.shared::cluster.f32 [%0], %1;" :: "r"(remote + (uint32_t)(c * 128 + threadIdx.x) * 4u),
+                         "f"(__uint_as_float(d[c])) : "memory");
+    }
+    ptx::cluster_sync();
+    if (crank == 1) {
+        ptx::tc_fence_before();
+        __syncthreads();
+        if (warp == 1) {
+            ptx::tc_fence_after();
+            ptx::tmem_dealloc<1>(tmem, C::kTmemCols);
+        }
+        return;
+    }
+#pragma unroll
+    for (int c = 0; c < C::N; ++c) d[c] = __float_as_uint(__uint_as_float(d[c]) + red[c * 128 + threadIdx.x]);
+    const int t = t0 + threadIdx.x;
+    float row[EP];
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+        float hv = (__uint_as_float(d[2 * EP + e]) + __uint_as_float(d[EP + e])) + __uint_as_float(d[e]);
+        if constexpr (kNoise) {
+            const int o = C::NB;
+            const float an = (__uint_as_float(d[o + 2 * EP + e]) + __uint_as_float(d[o + EP + e])) +
+                             __uint_as_float(d[o + e]);
+            if (t < T && e < E) {
+                const float zz = z[(size_t)t * E + e];
+                const float sp = fmaxf(an, 0.f) + log1pf(expf(-fabsf(an)));
+                hv = hv + zz * sp;
+                noise_act[(size_t)t * E + e] = an;
+            }
+        }
+        row[e] = hv;
+        if (t < T && e < E) logits[(size_t)t * E + e] = hv;
+    }
+    if (t < T) {
+        float g[EP], p[EP];
+        const bool ok = gate_row<EP>(row, E, k, router_type, g, p);
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+            if (e < E) {
+                gates[(size_t)t * E + e] = g[e];
+                if (probs) probs[(size_t)t * E + e] = p[e];
+            }
+        }
+        if (!ok && err_flag) atomicExch(err_flag, 1);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<1>(tmem, C::kTmemCols);
     }
 }
 
@@ -785,10 +983,63 @@ dispatch_scan_kernel(const float* __restrict__ gates, int T, int E, int capacity
 using namespace b200moe;
 
 namespace {
+// Diagnostics (A/B against the CUDA-core K1): thread-local, product default off.
+thread_local int g_router_fma = 0;
+
+template <int EP, bool kNoise>
+int router_fwd_tc(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E, int k,
+                  int router_type, float* logits, float* gates, float* probs, float* noise_act, float* workspace,
+                  int32_t* err_flag, cudaStream_t stream) {
+    using C = RtcCfg<EP, kNoise>;
+    float4* wsw = reinterpret_cast<float4*>(workspace);
+    float4* wnsw = reinterpret_cast<float4*>(workspace + (size_t)H * EP);
+    __nv_bfloat16* bsplit = reinterpret_cast<__nv_bfloat16*>(workspace + (size_t)2 * H * EP);
+    router_wsplit_kernel<EP, kNoise><<<ceil_div(H, 256), 256, 0, stream>>>(w_g, w_noise, H, E, bsplit, wsw, wnsw);
+    CUtensorMap xmap, bmap;
+    int rc = make_tmap_bf16_2d(&xmap, x, (uint64_t)H, (uint64_t)T, (uint64_t)H, 64, 128, true);
+    if (rc) return rc;
+    rc = make_tmap_bf16_2d(&bmap, bsplit, (uint64_t)H, (uint64_t)C::N, (uint64_t)H, 64, C::N, true);
+    if (rc) return rc;
+    auto kern = router_fwd_tc_kernel<EP, kNoise>;
+    static std::atomic<uint64_t> attr{0};
+    if (cudaError_t ae = ensure_smem_attr(kern, C::kSmem, attr); ae != cudaSuccess) {
+        set_error("router_fwd_tc smem attribute: %s", cudaGetErrorString(ae));
+        return B200MOE_ERR_CUDA;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ceil_div(T, 128));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = 2;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, xmap, bmap, z, T, H, E, k, router_type, logits, gates, probs,
+                                        noise_act, err_flag);
+    if (le != cudaSuccess) {
+        set_error("router_fwd_tc launch: %s", cudaGetErrorString(le));
+        return B200MOE_ERR_CUDA;
+    }
+    return B200MOE_OK;
+}
+
 template <int EP>
 int router_fwd_impl(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E,
                     int k, int router_type, float* logits, float* gates, float* probs, float* noise_act,
                     float* workspace, int32_t* err_flag, cudaStream_t stream) {
+    if constexpr (EP <= 16) {   // tensor-core path (H a multiple of 128: two full-width hidden halves)
+        if (H % 128 == 0 && !g_router_fma) {
+            if (z != nullptr)
+                return router_fwd_tc<EP, true>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs,
+                                               noise_act, workspace, err_flag, stream);
+            return router_fwd_tc<EP, false>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs,
+                                            noise_act, workspace, err_flag, stream);
+        }
+    }
     float4* wsw = reinterpret_cast<float4*>(workspace);
     float4* wnsw = reinterpret_cast<float4*>(workspace + (size_t)H * EP);
     const size_t wbytes = (size_t)H * EP * sizeof(float);
@@ -855,6 +1106,17 @@ int b200moe_router_fwd(const void* x, const float* w_g, const float* w_noise, co
     if (E <= 8) return router_fwd_impl<8>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs, noise_act, workspace, err_flag, stream);
     if (E <= 16) return router_fwd_impl<16>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs, noise_act, workspace, err_flag, stream);
     return router_fwd_impl<32>(x, w_g, w_noise, z, T, H, E, k, router_type, logits, gates, probs, noise_act, workspace, err_flag, stream);
+}
+
+size_t b200moe_router_workspace_floats(int H, int E) {
+    const int EP = E <= 4 ? 4 : E <= 8 ? 8 : E <= 16 ? 16 : 32;
+    const int NB = ((3 * EP + 15) / 16) * 16;
+    return (size_t)2 * H * EP + (size_t)NB * H;   // swizzled W_g, W_noise (fp32) + split table (2 x NB x H bf16)
+}
+
+int b200moe_router_set_fma(int on) {
+    g_router_fma = on;
+    return B200MOE_OK;
 }
 
 int b200moe_gate_from_logits(const float* logits, int T, int E, int k, int router_type, float* gates, float* probs,

@@ -34,7 +34,7 @@ import torch.distributed as dist
 from . import _lib
 from .errors import ConfigError, ShapeError
 from .moe import (DeviceRoutingStats, GateConfig, SEG_PAD, _acc_targets, _arange_i32, _dispatch_ws, _ep, _noise,
-                  _swizzled, _wgrad_call, _wgrad_outputs, _wgrad_tickets, expert_capacity)
+                  _router_ws, _swizzled, _wgrad_call, _wgrad_outputs, _wgrad_tickets, expert_capacity)
 
 
 @dataclass
@@ -153,7 +153,7 @@ class _EPFunction(torch.autograd.Function):
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
         err = None          # gate errors reach the host through the dispatch stats (stats[2])
-        ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
+        ws = _router_ws(H, E, dev)      # left holding the swizzled W_g / W_noise (reused below)
         ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
                   cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),
@@ -365,7 +365,7 @@ class _EPPeerFunction(torch.autograd.Function):
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
         err = None          # gate errors reach the host through the dispatch stats (stats[2])
-        ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
+        ws = _router_ws(H, E, dev)      # left holding the swizzled W_g / W_noise (reused below)
         ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E,
                   cfg.top_k, rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act),

@@ -293,6 +293,13 @@ def _dispatch_ws(device, T: int) -> torch.Tensor:
     return ws
 
 
+def _router_ws(H: int, E: int, device) -> torch.Tensor:
+    """Workspace of b200moe_router_fwd (swizzled W tables for the backward +
+    the bf16 split table of the tensor-core router)."""
+    n = int(_lib.load().b200moe_router_workspace_floats(int(H), int(E)))
+    return torch.empty(n, dtype=torch.float32, device=device)
+
+
 def _wgrad_tickets(device, H: int) -> torch.Tensor:
     """Per-hidden-block tickets of the router weight-gradient kernel (zeroed
     once; each launch leaves them zeroed), one buffer per (device, stream)."""
@@ -432,7 +439,7 @@ class _RouterLogitsFunction(torch.autograd.Function):
         logits = torch.empty(T, E, dtype=torch.float32, device=dev)
         gates = torch.empty_like(logits)
         na = torch.empty_like(logits) if z is not None else None
-        ws = torch.empty(2 * H * _ep(E), dtype=torch.float32, device=dev)
+        ws = _router_ws(H, E, dev)
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.call("b200moe_router_fwd", xb.data_ptr(), wg.data_ptr(), wn.data_ptr(), _lib.ptr(z), T, H, E, 1, 0,
                   logits.data_ptr(), gates.data_ptr(), None, _lib.ptr(na), ws.data_ptr(), err.data_ptr(),
@@ -608,7 +615,7 @@ class _MoEFunction(torch.autograd.Function):
         probs = torch.empty(T, E, **f32) if cfg.router_type == "st" else None
         noise_act = torch.empty(T, E, **f32) if z is not None else None
         err = None          # gate errors reach the host through the dispatch stats (stats[2])
-        ws = torch.empty(2 * H * _ep(E), **f32)      # left holding the swizzled W_g / W_noise (reused below)
+        ws = _router_ws(H, E, dev)      # left holding the swizzled W_g / W_noise (reused below)
         ctx.router_ws = ws
         _lib.call("b200moe_router_fwd", x.data_ptr(), w_g.data_ptr(), w_noise.data_ptr(), _lib.ptr(z), T, H, E, k,
                   rt, logits.data_ptr(), gates.data_ptr(), _lib.ptr(probs), _lib.ptr(noise_act), ws.data_ptr(),

@@ -369,3 +369,45 @@ def test_upcycle_copy_bitwise():
         assert torch.equal(W3[e].t(), w3.to(torch.bfloat16))
     W1b, _, _ = upcycle_experts(w1.to(torch.bfloat16), w2.to(torch.bfloat16), w3.to(torch.bfloat16), 3)
     assert torch.equal(W1b[2].t(), w1.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("E,noise", [(4, False), (8, False), (8, True), (16, True), (6, True)])
+def test_router_fwd_tensor_core_matches_fp64_and_cuda_core_path(E, noise):
+    """K1 on tcgen05 (x . W with W split into three bf16 parts, fp32
+    accumulation) against an fp64 reference of x . W (+ z softplus(x . W_n))
+    and against the CUDA-core K1: logits agree to fp32 accumulation slack
+    (|dh| <= 2e-6 * sum |x w| + 1e-7), and the gates each path produces from its
+    own logits are the oracle's gates for those logits (bit-exact)."""
+    T, H = 1000, 1024
+    g = O.rng(60, E)
+    x = torch.from_numpy(g.standard_normal((T, H)).astype(np.float32)).cuda().to(torch.bfloat16)
+    wg = torch.from_numpy((g.standard_normal((H, E)) * 0.05).astype(np.float32)).cuda()
+    wn = torch.from_numpy((g.standard_normal((H, E)) * 0.05).astype(np.float32)).cuda()
+    z = torch.from_numpy(g.standard_normal((T, E)).astype(np.float32)).cuda() if noise else None
+    out = {}
+    for fma in (0, 1):
+        _lib.call("b200moe_router_set_fma", fma)
+        try:
+            logits = torch.empty(T, E, device="cuda")
+            gates = torch.empty(T, E, device="cuda")
+            na = torch.empty(T, E, device="cuda") if noise else None
+            ws = B.moe._router_ws(H, E, torch.device("cuda"))
+            _lib.call("b200moe_router_fwd", x.data_ptr(), wg.data_ptr(), wn.data_ptr(), _lib.ptr(z), T, H, E, 2, 0,
+                      logits.data_ptr(), gates.data_ptr(), None, _lib.ptr(na), ws.data_ptr(), None, _lib.stream_ptr())
+            torch.cuda.synchronize()
+        finally:
+            _lib.call("b200moe_router_set_fma", 0)
+        out[fma] = (logits.cpu().numpy(), gates.cpu().numpy())
+    xd = x.double().cpu().numpy()
+    wgd, wnd = wg.double().cpu().numpy(), wn.double().cpu().numpy()
+    ref = xd @ wgd
+    slack = np.abs(xd) @ np.abs(wgd)
+    if noise:
+        an = xd @ wnd
+        zd = z.double().cpu().numpy()
+        ref = ref + zd * (np.maximum(an, 0) + np.log1p(np.exp(-np.abs(an))))
+        slack = slack + np.abs(zd) * (np.abs(xd) @ np.abs(wnd) + 1.0)
+    for fma in (0, 1):
+        h, gts = out[fma]
+        assert np.all(np.abs(h - ref) <= 2e-6 * slack + 1e-7), (fma, np.abs(h - ref).max())
+        assert gts.tobytes() == O.gate(h, 2, "mixtral").gates.tobytes()
