@@ -85,6 +85,8 @@ struct GemmArgs {
     int debug;  // bit 0: skip wgrad epilogue stores (diagnostics only)
     int wgrad_subs;  // WGRAD sub-problems to compute: bit 0 dW1, bit 1 dW3, bit 2 dW2 (0 = all)
     int dense;       // BWD1 as a plain dense GEMM: one (A, B) pair, K = F (0 = the two-pair expert BWD1)
+    int wgrad_mfast; // WGRAD raster: output-row tiles fastest (dense wgrad with many more column tiles than row
+                     // tiles and a long K: concurrent tiles then share the column block of dy in L2)
 };
 
 __host__ __device__ __forceinline__ int wgrad_mask(const GemmArgs& a) { return a.wgrad_subs ? a.wgrad_subs : 7; }
@@ -183,8 +185,14 @@ struct Sched {
                 r -= n;
             }
             const int nt = (ti.sub == 2 ? a.F : a.H) / kBN;
-            ti.m_tile = r / nt;
-            ti.n_tile = r % nt;
+            if (a.wgrad_mfast) {
+                const int mt = (ti.sub == 2 ? a.H : a.F) / Cfg<kCG>::kTileM;
+                ti.n_tile = r / mt;
+                ti.m_tile = r % mt;
+            } else {
+                ti.m_tile = r / nt;
+                ti.n_tile = r % nt;
+            }
         } else {
             const int mt = (prefix[s + 1] - prefix[s]) / n_tiles;
             ti.sub = 0;
@@ -1376,6 +1384,7 @@ int b200moe_dense_wgrad(const void* x, const void* dy, const int* seg_base, cons
     GemmArgs a = {seg_base, seg_count, seg_expert, 1, N, K, 1, (__nv_bfloat16*)dw, nullptr, nullptr, nullptr,
                   nullptr};
     a.wgrad_subs = 1;
+    a.wgrad_mfast = (N / 256) > (K / 256);   // e.g. the lm-head: 16 row tiles x 501 column tiles, K = tokens
     return dispatch_launch<kWgrad>(tm, a, stream);
 }
 

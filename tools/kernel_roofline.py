@@ -23,11 +23,14 @@ T, H, E, K, S = 8192, 4096, 8, 2, 8192          # bench shape, CF=1: S kept slot
 BF = 2
 ALG = {  # algorithmic bytes per launch (bf16 activations, fp32 [T, E] routing tensors)
     "router_fwd_kernel": T * H * BF + H * E * 4 + 3 * T * E * 4,
+    "router_fwd_tc_kernel": T * H * BF + 3 * 32 * H * BF + 3 * T * E * 4,   # x, split-W table, outputs
+    "router_wsplit_kernel": H * E * 4 + 32 * H * BF + H * E * 4,
     "dispatch_kernel": T * E * 4 + T * E * 4,
+    "dispatch_scan_kernel": T * E * 4 + T * E * 4,
     "permute_kernel": T * H * BF + S * H * BF,
     "combine_kernel": S * H * BF + T * H * BF + T * E * 4,
     "combine_bwd_kernel": T * H * BF + 2 * S * H * BF + T * E * 4,
-    "router_dx_kernel": S * H * BF + T * H * BF,
+    "router_dx_kernel": S * H * BF + T * H * BF + 5 * T * E * 4,   # dxp rows, dx; dg, gates, slots in, dh out
     "router_wgrad_ring": T * H * BF + T * E * 4,
     "router_dh_kernel": 4 * T * E * 4,
 }

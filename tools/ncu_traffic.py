@@ -16,7 +16,10 @@ WANT = {
     "gpu__time_duration.sum": "duration",
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
-    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_active_pct",
+    # tcgen05 MMA activity of the tensor pipe per SM cycle (the realtime per-TPC
+    # counter used in round 1 does not track UTCHMMA work; this one does: FWD2
+    # reads ~92% at ~0.92 of the clock-scaled peak)
+    "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_active_pct",
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
     "lts__t_bytes.sum": "l2_bytes",
     "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum": "tma_load_bytes",
@@ -45,6 +48,15 @@ def main(rep, out):
                     rec[key] = float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
                     break
         launches.append(rec)
+    H, F, S = 4096, 14336, 8192
+    flops = {"fwd1": 4.0 * H * F * S, "fwd2": 2.0 * H * F * S, "bwd2": 2.0 * H * F * S, "bwd1": 4.0 * H * F * S,
+             "wgrad": 6.0 * H * F * S}
+    for x in launches:
+        if x["mode"] in flops and x.get("duration"):
+            tf = flops[x["mode"]] / x["duration"] / 1e12
+            x["tflops"] = tf
+            if x.get("sm_clock"):   # dense bf16: 8192 FLOP / clock / SM on 148 SMs
+                x["frac_of_clock_peak"] = tf * 1e12 / (148 * 8192 * x["sm_clock"])
     total = sum(x.get("dram_read", 0) + x.get("dram_write", 0) for x in launches)
     res = {"source": rep, "launches": launches, "dram_bytes_per_step": total,
            "note": "ncu --set full --clock-control none, one bench step (5 grouped-GEMM launches); cold, serialised"}
