@@ -247,15 +247,17 @@ int b200moe_expert_wgrad_ex(const void* xp, const void* h, const void* dout, con
  *   wgrad dw[K,N] = x^T . dy          (lddw must equal N)
  * bf16 in / out, fp32 accumulation; K and N multiples of 256, any M >= 1.
  * seg_base / seg_count / seg_expert: a device segment table of one segment
- * {0, M, 0} (int32). */
+ * {0, M, 0} (int32).  grid_ctas: persistent grid cap (0 = one CTA per SM);
+ * the model step leaves a few SMs to the overlapped NCCL reductions and
+ * optimizer updates running on other streams. */
 int b200moe_dense_fwd(const void* x, const void* w, const int* seg_base, const int* seg_count, const int* seg_expert,
-                      int M, int K, int N, int ldx, int ldw, int ldy, void* y, cudaStream_t stream);
+                      int M, int K, int N, int ldx, int ldw, int ldy, void* y, int grid_ctas, cudaStream_t stream);
 int b200moe_dense_dgrad(const void* dy, const void* w, const int* seg_base, const int* seg_count,
                         const int* seg_expert, int M, int K, int N, int lddy, int ldw, int lddx, void* dx,
-                        cudaStream_t stream);
+                        int grid_ctas, cudaStream_t stream);
 int b200moe_dense_wgrad(const void* x, const void* dy, const int* seg_base, const int* seg_count,
                         const int* seg_expert, int M, int K, int N, int ldx, int lddy, int lddw, void* dw,
-                        cudaStream_t stream);
+                        int grid_ctas, cudaStream_t stream);
 
 /* Diagnostics knobs for tests and A/B tools, NOT part of the product path:
  * thread-local (they affect only GEMM launches issued by the calling thread;

@@ -60,9 +60,9 @@ SIGNATURES = {
     "b200moe_expert_bwd2_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P],
     "b200moe_expert_bwd1_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P],
     "b200moe_expert_wgrad_ex": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P],
-    "b200moe_dense_fwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
-    "b200moe_dense_dgrad": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
-    "b200moe_dense_wgrad": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
+    "b200moe_dense_fwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P],
+    "b200moe_dense_dgrad": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P],
+    "b200moe_dense_wgrad": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P],
     "b200moe_gemm_set_cta_group": [_I],
     "b200moe_gemm_set_max_ctas": [_I],
     "b200moe_gemm_set_debug": [_I],

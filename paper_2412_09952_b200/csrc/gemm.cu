@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -1339,7 +1340,7 @@ static int check_dense(int M, int K, int N) {
 }
 
 int b200moe_dense_fwd(const void* x, const void* w, const int* seg_base, const int* seg_count, const int* seg_expert,
-                      int M, int K, int N, int ldx, int ldw, int ldy, void* y, cudaStream_t stream) {
+                      int M, int K, int N, int ldx, int ldw, int ldy, void* y, int grid_ctas, cudaStream_t stream) {
     B200_TRY(check_dense(M, K, N));
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], x, K, M, ldx, false));
@@ -1351,12 +1352,12 @@ int b200moe_dense_fwd(const void* x, const void* w, const int* seg_base, const i
     tm.st[1] = tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, 1, N, K, 1, (__nv_bfloat16*)y, nullptr, nullptr, nullptr, nullptr};
     a.dense = 1;
-    return dispatch_launch<kBwd1>(tm, a, stream);
+    return dispatch_launch<kBwd1>(tm, a, stream, grid_ctas);
 }
 
 int b200moe_dense_dgrad(const void* dy, const void* w, const int* seg_base, const int* seg_count,
                         const int* seg_expert, int M, int K, int N, int lddy, int ldw, int lddx, void* dx,
-                        cudaStream_t stream) {
+                        int grid_ctas, cudaStream_t stream) {
     B200_TRY(check_dense(M, K, N));
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], dy, N, M, lddy, false));
@@ -1366,12 +1367,12 @@ int b200moe_dense_dgrad(const void* dy, const void* w, const int* seg_base, cons
     tm.st[1] = tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, 1, K, N, 1, (__nv_bfloat16*)dx, nullptr, nullptr, nullptr,
                   nullptr};
-    return dispatch_launch<kFwd2>(tm, a, stream);
+    return dispatch_launch<kFwd2>(tm, a, stream, grid_ctas);
 }
 
 int b200moe_dense_wgrad(const void* x, const void* dy, const int* seg_base, const int* seg_count,
                         const int* seg_expert, int M, int K, int N, int ldx, int lddy, int lddw, void* dw,
-                        cudaStream_t stream) {
+                        int grid_ctas, cudaStream_t stream) {
     B200_TRY(check_dense(M, K, N));
     B200_CHECK_ARG(lddw == N, B200MOE_ERR_SHAPE, "dense wgrad writes a contiguous [K, N] gradient (ld %d != N %d)",
                    lddw, N);
@@ -1385,7 +1386,7 @@ int b200moe_dense_wgrad(const void* x, const void* dy, const int* seg_base, cons
                   nullptr};
     a.wgrad_subs = 1;
     a.wgrad_mfast = (N / 256) > (K / 256);   // e.g. the lm-head: 16 row tiles x 501 column tiles, K = tokens
-    return dispatch_launch<kWgrad>(tm, a, stream);
+    return dispatch_launch<kWgrad>(tm, a, stream, grid_ctas);
 }
 
 }  // extern "C"

@@ -396,6 +396,18 @@ def ffn(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, w3: torch.Tensor) -
 # dense projections (qkv, wo, lm-head) on the tcgen05 kernel
 # --------------------------------------------------------------------------
 
+# Persistent-grid cap of the dense projections (0 = one CTA per SM).  A
+# multi-GPU training step sets it a little below the SM count
+# (set_dense_grid) so the NCCL reductions and the overlapped optimizer updates
+# on other streams find free SMs while a projection GEMM runs.
+_DENSE_GRID = 0
+
+
+def set_dense_grid(ctas: int) -> None:
+    global _DENSE_GRID
+    _DENSE_GRID = int(ctas)
+
+
 class _Linear(torch.autograd.Function):
     """y = x . w with the reference [in, out] weight layout (tensor.py:192-207
     matmul), bf16 in / out, fp32 accumulation, on the repo's own tcgen05 GEMM
@@ -410,7 +422,7 @@ class _Linear(torch.autograd.Function):
         base, cnt = _one_segment(M, x.device)
         e0 = _arange_i32(1, x.device)
         _lib.call("b200moe_dense_fwd", x.data_ptr(), w.data_ptr(), base.data_ptr(), cnt.data_ptr(), e0.data_ptr(),
-                  M, K, N, K, N, N, y.data_ptr(), _lib.stream_ptr())
+                  M, K, N, K, N, N, y.data_ptr(), _DENSE_GRID, _lib.stream_ptr())
         ctx.save_for_backward(x, w)
         return y
 
@@ -427,11 +439,11 @@ class _Linear(torch.autograd.Function):
         if ctx.needs_input_grad[0]:
             dx = torch.empty(M, K, dtype=torch.bfloat16, device=x.device)
             _lib.call("b200moe_dense_dgrad", dy.data_ptr(), w.data_ptr(), base.data_ptr(), cnt.data_ptr(),
-                      e0.data_ptr(), M, K, N, N, N, K, dx.data_ptr(), s)
+                      e0.data_ptr(), M, K, N, N, N, K, dx.data_ptr(), _DENSE_GRID, s)
         if ctx.needs_input_grad[1]:
             dw = torch.empty(K, N, dtype=torch.bfloat16, device=x.device)
             _lib.call("b200moe_dense_wgrad", x.data_ptr(), dy.data_ptr(), base.data_ptr(), cnt.data_ptr(),
-                      e0.data_ptr(), M, K, N, K, N, N, dw.data_ptr(), s)
+                      e0.data_ptr(), M, K, N, K, N, N, dw.data_ptr(), _DENSE_GRID, s)
         return dx, dw
 
 

@@ -57,13 +57,13 @@ def main():
         s = lambda: _lib.stream_ptr()  # noqa: E731
         phases = {
             "fwd": (lambda: _lib.call("b200moe_dense_fwd", xb.data_ptr(), wb.data_ptr(), base.data_ptr(),
-                                      cnt.data_ptr(), e0.data_ptr(), M, K, N, K, N, N, y.data_ptr(), s()),
+                                      cnt.data_ptr(), e0.data_ptr(), M, K, N, K, N, N, y.data_ptr(), 0, s()),
                     lambda: torch.matmul(xb, wb, out=y)),
             "dgrad": (lambda: _lib.call("b200moe_dense_dgrad", dy.data_ptr(), wb.data_ptr(), base.data_ptr(),
-                                        cnt.data_ptr(), e0.data_ptr(), M, K, N, N, N, K, dx.data_ptr(), s()),
+                                        cnt.data_ptr(), e0.data_ptr(), M, K, N, N, N, K, dx.data_ptr(), 0, s()),
                       lambda: torch.matmul(dy, wb.t(), out=dx)),
             "wgrad": (lambda: _lib.call("b200moe_dense_wgrad", xb.data_ptr(), dy.data_ptr(), base.data_ptr(),
-                                        cnt.data_ptr(), e0.data_ptr(), M, K, N, K, N, N, dw.data_ptr(), s()),
+                                        cnt.data_ptr(), e0.data_ptr(), M, K, N, K, N, N, dw.data_ptr(), 0, s()),
                       lambda: torch.matmul(xb.t(), dy, out=dw)),
             "fwd+bwd": (ours, cublas),
         }

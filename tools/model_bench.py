@@ -75,6 +75,8 @@ def main():
                     help="MoE layers (the first N, p2p EP) that rebuild a, b, h in the backward instead of keeping them")
     ap.add_argument("--cublas-proj", action="store_true",
                     help="A/B only: qkv / wo / lm-head through torch.matmul (cuBLAS) instead of the repo's tcgen05 GEMM")
+    ap.add_argument("--dense-grid", type=int, default=0,
+                    help="persistent-grid cap of the projection GEMMs (0 = all SMs; caps measured no faster)")
     ap.add_argument("--zero", action="store_true",
                     help="ZeRO-1: shard the replicated tensors' optimizer state over the ranks")
     a = ap.parse_args()
@@ -88,6 +90,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         rank, group = dist.get_rank(), dist.group.WORLD
     dev = torch.device("cuda", torch.cuda.current_device())
+    import paper_2412_09952_b200.tensor as PT0
+    PT0.set_dense_grid(a.dense_grid)
     if a.cublas_proj:
         import paper_2412_09952_b200.tensor as PT
         PT.linear = lambda x, w: x.to(torch.bfloat16) @ w.to(torch.bfloat16)   # noqa: E731
@@ -199,7 +203,8 @@ def main():
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
         "optimizer_state_gb_rank0": round(opt.state_bytes() / 2**30, 2), "zero1": bool(a.zero),
         "recompute_moe_layers": a.recompute,
-        "projections": "torch.matmul (cuBLAS), A/B run" if a.cublas_proj else "tcgen05 dense GEMM (tensor.linear)",
+        "projections": "torch.matmul (cuBLAS), A/B run" if a.cublas_proj else
+        f"tcgen05 dense GEMM (tensor.linear), grid cap {PT0._DENSE_GRID or 148}",
         "clocks": clocks,
         "config": {"vocab": cfg.vocab, "hidden": cfg.hidden, "layers": cfg.layers, "heads": cfg.heads,
                    "kv_heads": cfg.kv_heads, "ffn": cfg.ffn_hidden, "seq": a.seq, "batch": a.batch, "experts": a.experts,
