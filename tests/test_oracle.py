@@ -254,3 +254,50 @@ def test_identical_experts_mixtral_dropless_equals_dense():
     dense = ((a * O.sigmoid(a)) * (x @ w3)) @ w2
     assert np.max(np.abs(y - dense) / np.maximum(np.abs(dense), 1e-30)) <= 1e-12
     assert cache.disp.n_dropped == 0
+
+
+@pytest.mark.parametrize("rt,pol,cf,noise", [("mixtral", "position", 1.0, True), ("st", "score", 2.0, False),
+                                             ("mixtral", "score", None, True)])
+def test_sampled_oracle_pieces_equal_full_oracle(rt, pol, cf, noise):
+    """The row / column pieces the bench-shape GPU test uses (expert_rows,
+    expert_wgrad_columns, router_bwd_rows) reproduce the pinned full oracle
+    (moe_forward / moe_backward) on the rows and columns they cover."""
+    T, H, F, E, k = 96, 16, 24, 8, 2
+    g = O.rng(77, 1)
+    wg = (g.standard_normal((H, E)) * 0.5).astype(np.float64)
+    wn = (g.standard_normal((H, E)) * 0.2).astype(np.float64)
+    w1 = [g.standard_normal((H, F)) * 0.3 for _ in range(E)]
+    w2 = [g.standard_normal((F, H)) * 0.3 for _ in range(E)]
+    w3 = [g.standard_normal((H, F)) * 0.3 for _ in range(E)]
+    x = g.standard_normal((T, H))
+    dy = g.standard_normal((T, H))
+    z = g.standard_normal((T, E))
+    cfg = O.LayerCfg(n_experts=E, top_k=k, router_type=rt, noise=noise, capacity_factor=cf, drop_policy=pol)
+    y, gates, cache = O.moe_forward(x, wg, wn, w1, w2, w3, cfg, z=z if noise else None)
+    _, dimp = O.importance_penalty(gates)
+    gr = O.moe_backward(cache, dy, dgates=0.3 * dimp)
+    kept = cache.disp.kept
+    idx = np.arange(0, T, 3)
+    y_s = np.zeros((idx.size, H))
+    dx_s = np.zeros((idx.size, H))
+    dg = np.zeros((idx.size, E))
+    cols = np.array([0, 5, 11, 23])
+    for e in range(E):
+        rows = np.flatnonzero(kept[idx, e])
+        if rows.size:
+            yc, dgc, dxc = O.expert_rows(x[idx[rows]], dy[idx[rows]], gates[idx[rows], e], w1[e], w2[e], w3[e])
+            y_s[rows] += yc
+            dg[rows, e] = dgc
+            dx_s[rows] += dxc
+        allr = np.flatnonzero(kept[:, e])
+        if allr.size:
+            d1, d3, d2 = O.expert_wgrad_columns(x[allr], dy[allr], gates[allr, e], w1[e][:, cols], w3[e][:, cols],
+                                                w2[e][cols, :])
+            np.testing.assert_allclose(d1, gr["dw1"][e][:, cols], rtol=1e-10, atol=1e-12)
+            np.testing.assert_allclose(d3, gr["dw3"][e][:, cols], rtol=1e-10, atol=1e-12)
+            np.testing.assert_allclose(d2, gr["dw2"][e][cols, :], rtol=1e-10, atol=1e-12)
+    dh, dxr, dn = O.router_bwd_rows(cache.logits[idx], k, rt, dg + 0.3 * dimp[None, :], x[idx], wg, wn,
+                                    z[idx] if noise else None, cache.an[idx] if noise else None)
+    np.testing.assert_allclose(y_s, y[idx], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dh, gr["dh"][idx], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dx_s + dxr, gr["dx"][idx], rtol=1e-10, atol=1e-12)
