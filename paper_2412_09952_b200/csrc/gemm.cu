@@ -137,7 +137,8 @@ struct Geo {
     static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? kEpiLoadBufs * 2 * 2048 : 0) + (kAccLoads ? 2 * 2048 : 0) +
                                          kRing * kStoreBytes;
     static constexpr int kSmemBytes = kStages * kStageBytes + kNumEpiWarps * kEpiWarpBytes +
-                                      1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2);
+                                      1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2) +
+                                      3 * 4 * kMaxSeg /*segment table*/;
 };
 
 // ------------------------------------------------------------------ tile map
@@ -867,7 +868,7 @@ __device__ __forceinline__ void mma_wide(const GemmArgs& a, const S& sched, uint
 
 // ------------------------------------------------------------------ kernel
 template <int kMode, int kCG>
-__global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_constant__ TmaSet tm, GemmArgs a) {
+__global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_constant__ TmaSet tm, GemmArgs a_in) {
     using C = Cfg<kCG>;
     using G = Geo<kMode, kCG>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -881,6 +882,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
     uint64_t* ldbar = tempty + 2;  // 2 per epilogue warp (BWD2 TMA load ring)
     uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(ldbar + 2 * kNumEpiWarps);
     int* prefix = reinterpret_cast<int*>(tmem_base_slot + 1);
+    // The segment table (base, count, expert; nseg <= 64) is read by every
+    // role at every tile: keep a shared-memory copy so no tile start waits on a
+    // global load.
+    int* segtab = prefix + kMaxSeg + 2;
+    for (int i = threadIdx.x; i < a_in.nseg; i += blockDim.x) {
+        segtab[i] = a_in.seg_base[i];
+        segtab[kMaxSeg + i] = a_in.seg_count[i];
+        segtab[2 * kMaxSeg + i] = a_in.seg_expert[i];
+    }
+    __syncthreads();
+    GemmArgs a = a_in;
+    a.seg_base = segtab;
+    a.seg_count = segtab + kMaxSeg;
+    a.seg_expert = segtab + 2 * kMaxSeg;
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
