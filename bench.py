@@ -213,6 +213,35 @@ def gemm_min_bytes(S: int) -> int:
     return int(3 * w + 13 * act_f + 6 * act_h)
 
 
+WARMUP_SECONDS = 0.5
+
+
+def warmup(args, fn, agree=None) -> int:
+    """max(W, 3) untimed steps, then more until the warm-up has run for about
+    WARMUP_SECONDS (at most 200 steps), so the timed steps start from a settled
+    GPU (clock and power state) rather than from the first milliseconds of
+    load: measured 6.80 vs 6.59-6.67 ms/step with W=5 vs W=100 on one box.
+    The step count is decided from the first steps' time, so that all ranks of
+    a multi-GPU run can agree on it (`agree`: e.g. an all_reduce MAX).
+    Returns the number of warm-up steps run (reported as "warmup")."""
+    import torch
+    w = max(args.warmup, 3)
+    fn()                                  # first step: one-time setup (module load, allocations)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(w - 1):
+        fn()
+    torch.cuda.synchronize()
+    per = (time.perf_counter() - t0) / (w - 1)
+    n = min(200, max(w, int(WARMUP_SECONDS / max(per, 1e-6))))
+    if agree is not None:
+        n = agree(n)
+    for _ in range(n - w):
+        fn()
+    torch.cuda.synchronize()
+    return n
+
+
 def layer_flops(T: int, S: int) -> float:
     """Algorithmic FLOPs of one fwd+bwd: 18*H*F per kept slot + router 6*T*H*E."""
     return 18.0 * H * F * S + 6.0 * T * H * E
@@ -350,8 +379,9 @@ def run_single(args, dev):
         return out, aux
 
     # warmup
-    for _ in range(max(args.warmup, 3)):
-        out, _ = step(x, dy)
+    warm = warmup(args, lambda: step(x, dy))
+    out, _ = step(x, dy)
+    warm += 1
     torch.cuda.synchronize()
     S = int(out.stats.assigned.sum())
 
@@ -366,8 +396,10 @@ def run_single(args, dev):
     with ClockSampler(dev.index) as clk:
         torch.cuda.synchronize()
         s0.record()
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             step(x, dy)
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # host time to enqueue a step
         s1.record()
         torch.cuda.synchronize()
     _lib.PROFILER = None
@@ -434,7 +466,7 @@ def run_single(args, dev):
     clocks = clk.summary()
     line = {
         "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 1), "unit": "tokens/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "steps": args.steps, "warmup": warm, "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": "Llama-3-8B-shape E8T2 MoE layer fwd+bwd (configs[1])", "hidden": H, "ffn": F,
                    "experts": E, "top_k": K_TOP, "tokens": T, "capacity_factor": args.cf, "router": args.router,
@@ -463,6 +495,7 @@ def run_single(args, dev):
                               f"measured HBM)"},
         "kernels_ms_per_step": {n.replace("b200moe_", ""): round(t / args.steps, 4) for n, (t, c) in ktimes.items()},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+        "host_enqueue_ms_per_step": round(host_ms, 4),
     }
     print(json.dumps(line), flush=True)
 

@@ -616,8 +616,14 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
               file=sys.stderr, flush=True)
         args.transport = "nccl"   # reported in the JSON line's config
         layer = ExpertParallelMoE(wg, wn, W1, W2, W3, gate, transport="nccl")
-    for _ in range(max(args.warmup, 3)):
-        out, _ = step(x, dy)
+    def agree(n):   # the same number of warm-up steps on every rank (EP steps synchronise the ranks)
+        t = torch.tensor([n], device=dev, dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return int(t)
+
+    warm = B.warmup(args, lambda: step(x, dy), agree)
+    out, _ = step(x, dy)
+    warm += 1
     torch.cuda.synchronize()
     S = int(out.routing["recv_counts"].sum().item())
     # timed region: GEMM spans recorded inside the same steps (see bench.py)
@@ -698,7 +704,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
         roof_peak = peak if burst else peak_s
         line = {
             "metric": "E8T2 MoE-layer fwd+bwd tokens/s", "value": round(tps, 1), "unit": "tokens/s",
-            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4),
+            "n_gpus": world, "steps": args.steps, "warmup": warm, "ms_per_step": round(ms_max, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "Llama-3-8B-shape E8T2 MoE layer fwd+bwd, expert parallel (configs[2])",
                        "hidden": H, "ffn": F, "experts": E, "top_k": K, "tokens_per_gpu": T,
