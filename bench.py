@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--cpu-tokens", type=int, default=512, help="bounded CPU sample (tokens per oracle step)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--eager", action="store_true",
+                   help="launch every step from Python instead of replaying a captured CUDA graph")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                    help="EP exchange: fused NVLink peer-memory kernels (default) or NCCL all-to-all")
     p.add_argument("--gemm-debug", type=int, default=0, help=argparse.SUPPRESS)  # A/B experiment switches
@@ -80,6 +82,18 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def _smi_id(index: int) -> str:
+    """nvidia-smi's id for torch device `index`: its UUID, so that the sampler
+    reads the GPU the process runs on even when CUDA_VISIBLE_DEVICES remaps
+    the ordinals (a box that hands out one GPU of eight)."""
+    try:
+        import torch
+        u = str(torch.cuda.get_device_properties(index).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        return str(index)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 20 ms in the
     background; only samples whose timestamp falls inside the timed region
@@ -88,12 +102,13 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
+        self.smi_id = _smi_id(index)
         self.proc = None
         self.t0 = self.t1 = None
         self.lines = []
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index),
+                ["nvidia-smi", "-i", self.smi_id,
                  "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
@@ -123,7 +138,7 @@ class ClockSampler:
         names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                  0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                  0x100: "display_clock_setting"}
-        all_sm = []
+        all_sm, idle = [], 0
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             try:
@@ -137,11 +152,12 @@ class ClockSampler:
                 continue
             sm.append(s)
             mx = max(mx, m)
+            idle += bool(r & 0x1)
             for bit, nm in names.items():
                 if r & bit and nm != "gpu_idle":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "idle_samples": idle, "gpu": self.smi_id}
 
 
 def reference_arm(args, rank: int):
@@ -247,7 +263,7 @@ def layer_flops(T: int, S: int) -> float:
     return 18.0 * H * F * S + 6.0 * T * H * E
 
 
-def run_e2e(steps, T, x, dy, step):
+def run_e2e(steps, T, x, dy, step, graphed=False):
     """End-to-end through the public API with HOST buffers: every step copies
     its inputs (x, dy) from pinned host memory and copies its results -- the
     layer output y, the input gradient dx and the aux loss -- back to pinned
@@ -256,7 +272,10 @@ def run_e2e(steps, T, x, dy, step):
     leaves on a second copy stream as soon as the forward is done (overlapping
     the backward), dx and the loss right after the backward (overlapping the
     next step).  Every copy is inside the timed region; the region ends when
-    the last D2H copy has landed."""
+    the last D2H copy has landed.  With `graphed`, each of the two input
+    buffers has its step captured as a CUDA graph (y's D2H copy is a node of
+    it) and the loop replays them; the H2D prefetch and the dx / loss copies
+    stay outside, so they overlap the neighbouring steps as in the eager loop."""
     import torch
     xh = x.detach().cpu().pin_memory()
     dyh = dy.cpu().pin_memory()
@@ -269,7 +288,8 @@ def run_e2e(steps, T, x, dy, step):
     main = torch.cuda.current_stream()
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
-    for ev in consumed:
+    landed = [torch.cuda.Event() for _ in range(2)]     # dx of the buffer's last step copied out
+    for ev in consumed + landed:
         ev.record(main)
 
     def prefetch(i):
@@ -280,6 +300,33 @@ def run_e2e(steps, T, x, dy, step):
             bufs[b][1].copy_(dyh, non_blocking=True)
             copied[b].record(cs)
 
+    def fwd_bwd(b):
+        cur = torch.cuda.current_stream()
+        xin = bufs[b][0].detach().requires_grad_()
+        out, aux = step(xin, bufs[b][1], lambda y: _d2h(ds, cur, y, yh[b]))
+        return xin, aux
+
+    def results(b, slot, xin, aux):
+        _d2h(ds, torch.cuda.current_stream(), xin.grad, dxh[b])
+        with torch.cuda.stream(ds):
+            res_h[slot:slot + 1].copy_(aux.detach().reshape(1), non_blocking=True)
+            landed[b].record(ds)
+
+    caps = None
+    if graphed:
+        from paper_2412_09952_b200.graphs import capture
+
+        def captured(b):
+            def fn():
+                r = fwd_bwd(b)
+                torch.cuda.current_stream().wait_stream(ds)     # join the y copy into the capture
+                return r
+            return capture(fn, warmup=1)
+        for b in range(2):
+            bufs[b][0].copy_(x.detach())
+            bufs[b][1].copy_(dy)
+        caps = [captured(0), captured(1)]
+
     def run(n):
         prefetch(0)
         for i in range(n):
@@ -287,12 +334,14 @@ def run_e2e(steps, T, x, dy, step):
                 prefetch(i + 1)
             b = i % 2
             main.wait_event(copied[b])
-            xin = bufs[b][0].detach().requires_grad_()
-            out, aux = step(xin, bufs[b][1], lambda y, b=b: _d2h(ds, main, y, yh[b]))
+            if caps is not None:
+                main.wait_event(landed[b])       # the graph rewrites this buffer's dx in place
+                caps[b].replay()                 # forward + backward, y copied out inside
+                r = caps[b].outputs
+            else:
+                r = fwd_bwd(b)
             consumed[b].record(main)
-            _d2h(ds, main, xin.grad, dxh[b])
-            with torch.cuda.stream(ds):
-                res_h[i:i + 1].copy_(aux.detach().reshape(1), non_blocking=True)
+            results(b, i, *r)                    # dx and the loss leave on the copy stream
         main.wait_stream(ds)
 
     run(2)
@@ -309,7 +358,9 @@ def run_e2e(steps, T, x, dy, step):
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb + 4,
             "ms_per_step": round(e2e_ms, 4),
             "h2d": "x, dy from pinned host, copy stream double-buffered one step ahead",
-            "d2h": "y (after the forward, overlapping the backward), dx and the aux loss to pinned host every step"}
+            "d2h": "y (after the forward, overlapping the backward), dx and the aux loss to pinned host every step",
+            "launch": ("CUDA graph per input buffer (y's copy to host is a node of it; dx and the loss are copied "
+                       "after the replay, overlapping the next step)") if graphed else "eager"}
 
 
 def _d2h(ds, main, t, host):
@@ -380,29 +431,49 @@ def run_single(args, dev):
 
     # warmup
     warm = warmup(args, lambda: step(x, dy))
-    out, _ = step(x, dy)
+    # (the step's outputs die with this statement: no autograd graph of an eager
+    # step may outlive it into a capture -- graphs.py)
+    S = int(step(x, dy)[0].stats.assigned.sum())
     warm += 1
     torch.cuda.synchronize()
-    S = int(out.stats.assigned.sum())
 
     # ---- timed region (device time, CUDA events on the launching stream).  The
     # grouped-GEMM time is measured INSIDE the same steps: one event before FWD1
     # and one after FWD2, one before BWD2 and one after BWD1 (the two contiguous
     # GEMM runs of a step; _lib.GEMM_SPANS), 4 events per step.
+    # Default launch path: the K timed steps are captured once into a CUDA
+    # graph (graphs.capture; the span events become event-record nodes of the
+    # graph), replayed once untimed and once timed -- one host call launches
+    # all K steps, so the GPU never waits on the Python enqueue.  --eager
+    # launches every step from Python.
     prof = _lib.Profiler(spans=_lib.GEMM_SPANS)
-    _lib.PROFILER = prof
+    cap = None
+    if not args.eager:
+        from paper_2412_09952_b200.graphs import capture
+        _lib.PROFILER = prof
+        cap = capture(lambda: step(x, dy), repeat=args.steps, warmup=0)
+        _lib.PROFILER = None
+        cap.replay()
+        torch.cuda.synchronize()
+        warm += args.steps
+    else:
+        _lib.PROFILER = prof
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         torch.cuda.synchronize()
         s0.record()
         h0 = time.perf_counter()
-        for _ in range(args.steps):
-            step(x, dy)
+        if cap is not None:
+            cap.replay()
+        else:
+            for _ in range(args.steps):
+                step(x, dy)
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # host time to enqueue a step
         s1.record()
         torch.cuda.synchronize()
     _lib.PROFILER = None
+    del cap
     ms = s0.elapsed_time(s1) / args.steps
     gemm_ms = prof.span_ms() / args.steps
     launches = prof.launches
@@ -411,7 +482,7 @@ def run_single(args, dev):
     # (right after the timed region, before the attribution pass: same thermal state)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args.steps, T, x, dy, step)
+        e2e = run_e2e(args.steps, T, x, dy, step, graphed=not args.eager)
 
     # ---- attribution pass: per-entry-point events around every call, to split
     # the step into kernels (its GEMM total is reported next to the timed one)
@@ -471,7 +542,10 @@ def run_single(args, dev):
         "config": {"workload": "Llama-3-8B-shape E8T2 MoE layer fwd+bwd (configs[1])", "hidden": H, "ffn": F,
                    "experts": E, "top_k": K_TOP, "tokens": T, "capacity_factor": args.cf, "router": args.router,
                    "drop_policy": args.policy, "kept_slots": S, "parallelism": "single GPU",
-                   "l2": "inputs > L2, no flush: 2.8 GB of expert weights + ~1.5 GB of activations stream each step"},
+                   "l2": "inputs > L2, no flush: 2.8 GB of expert weights + ~1.5 GB of activations stream each step",
+                   "launch": ("eager (one Python call chain per step)" if args.eager else
+                              f"CUDA graph of the {args.steps} timed steps, captured after the warm-up and replayed "
+                              f"once untimed before the timed replay")},
         "mfu": {"measured_peak": round(mfu_measured, 4), "spec_2250": round(mfu_spec, 4),
                 "flops_per_step": flops},
         "roofline": {"kernel": "moe_gemm (tcgen05 grouped GEMM, all 5 launches/step)", "bound": "tensor",

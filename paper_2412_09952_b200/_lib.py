@@ -157,12 +157,15 @@ class Profiler:
         self.calls[name] = self.calls.get(name, 0) + 1
         if self.spans is not None:
             import torch
+            # inside a CUDA-graph capture the events become event-record nodes
+            # of the graph (external), so every replay re-times the spans
+            ext = torch.cuda.is_current_stream_capturing()
             if name in self.spans[0] and self._open is None:
-                self._open = torch.cuda.Event(enable_timing=True)
+                self._open = torch.cuda.Event(enable_timing=True, external=ext)
                 self._open.record()
             rc = fn()
             if name in self.spans[1] and self._open is not None:
-                b = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True, external=ext)
                 b.record()
                 self.span_pairs.append((self._open, b))
                 self._open = None

@@ -117,7 +117,12 @@ class MoELayer:
 
     @classmethod
     def from_stacked(cls, router: RouterParams, W1: torch.Tensor, W2: torch.Tensor, W3: torch.Tensor) -> "MoELayer":
-        experts = [ExpertFFN(w1=W1[e].t(), w2=W2[e].t(), w3=W3[e].t()) for e in range(W1.shape[0])]
+        # detached views: reading an expert shares the stacked storage, its
+        # gradient is expert_grad(); an autograd view would keep the stacked
+        # parameters' grad accumulators alive (and bound to the stream the
+        # layer was built on, which a CUDA-graph capture cannot wait on)
+        experts = [ExpertFFN(w1=W1[e].detach().t(), w2=W2[e].detach().t(), w3=W3[e].detach().t())
+                   for e in range(W1.shape[0])]
         return cls(router=router, experts=experts, stacked=(W1, W2, W3))
 
     def stacked_weights(self):
@@ -148,7 +153,13 @@ class _StackExperts(torch.autograd.Function):
     def forward(ctx, layer, *ws):
         key = tuple((t.data_ptr(), t._version, t.dtype, tuple(t.shape), tuple(t.stride())) for t in ws)
         cache = layer.__dict__.get("_stack_cache")
-        if cache is None or cache[0] != key:
+        if torch.cuda.is_current_stream_capturing():
+            # inside a CUDA graph the stack is part of the recorded step, so a
+            # replay after an in-place weight update re-stacks (graphs.py)
+            n = len(ws) // 3
+            cache = (None, tuple(torch.stack([ws[3 * e + j].detach().t() for e in range(n)])
+                                 .to(torch.bfloat16).contiguous() for j in range(3)))
+        elif cache is None or cache[0] != key:
             n = len(ws) // 3
             stacks = tuple(torch.stack([ws[3 * e + j].detach().t() for e in range(n)]).to(torch.bfloat16).contiguous()
                            for j in range(3))
@@ -497,6 +508,9 @@ def _noise(T, E, device, enabled, rng, noise):
         return noise.detach().to(torch.float32).contiguous()
     if rng is None:
         raise ConfigError("router noise enabled but no rng supplied")
+    if torch.cuda.is_current_stream_capturing():
+        raise ConfigError("router noise from a host rng cannot be recorded in a CUDA graph: pass noise= "
+                          "(a device tensor refilled before each replay)")
     z = rng.standard_normal((T, E)).astype(np.float32)   # row-major, like moe.py:148
     return torch.from_numpy(z).to(device, non_blocking=False)
 
