@@ -606,7 +606,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
         return out, aux
 
     try:
-        out, _ = step(x, dy)
+        step(x, dy)
         torch.cuda.synchronize()
     except Exception as exc:   # noqa: BLE001 -- symmetric-memory setup failed on this box
         if args.transport != "p2p":
@@ -622,24 +622,45 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
         return int(t)
 
     warm = B.warmup(args, lambda: step(x, dy), agree)
-    out, _ = step(x, dy)
+    out = step(x, dy)[0]
     warm += 1
     torch.cuda.synchronize()
     S = int(out.routing["recv_counts"].sum().item())
-    # timed region: GEMM spans recorded inside the same steps (see bench.py)
+    s_send = int(out.routing["counts"].sum().item())
+    del out          # no autograd graph of an eager step may outlive it into a capture (graphs.py)
+    # timed region: GEMM spans recorded inside the same steps (see bench.py).
+    # Default: the K steps are captured into one CUDA graph per rank (device
+    # barriers, peer kernels and the dW_g all_reduce are all stream work) and
+    # replayed once untimed, once timed; --eager launches them from Python.
     prof = _lib.Profiler(spans=_lib.GEMM_SPANS)
-    _lib.PROFILER = prof
+    cap = None
+    eager = getattr(args, "eager", False)
+    if not eager:
+        from .graphs import capture
+        _lib.PROFILER = prof
+        cap = capture(lambda: step(x, dy), repeat=args.steps, warmup=0)
+        _lib.PROFILER = None
+        dist.barrier()
+        cap.replay()
+        torch.cuda.synchronize()
+        warm += args.steps
+    else:
+        _lib.PROFILER = prof
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with B.ClockSampler(dev.index) as clk:
         dist.barrier()
         torch.cuda.synchronize()
         e0.record()
-        for _ in range(args.steps):
-            step(x, dy)
+        if cap is not None:
+            cap.replay()
+        else:
+            for _ in range(args.steps):
+                step(x, dy)
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
     _lib.PROFILER = None
+    del cap
     ms = e0.elapsed_time(e1) / args.steps
     gemm_ms = prof.span_ms() / args.steps
     t = torch.tensor([ms, float(S)], device=dev, dtype=torch.float64)
@@ -649,10 +670,13 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     dist.all_reduce(ssum, op=dist.ReduceOp.SUM)
     ms_max = float(tmax[0])
     S_tot = float(ssum[0])
+    s_all = [torch.zeros(1, device=dev, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(s_all, t[1:].clone())
+    s_ranks = [int(v) for v in s_all]
 
     # e2e: host-resident x / dy copied in, y / dx / aux loss copied out, every step
     dist.barrier()
-    e2e_rank = B.run_e2e(args.steps, T, x, dy, step)
+    e2e_rank = B.run_e2e(args.steps, T, x, dy, step, graphed=not eager)
     e2e_t = torch.tensor([e2e_rank["ms_per_step"]], device=dev, dtype=torch.float64)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     clocks = clk.summary()
@@ -672,7 +696,6 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     # direction (B200_PROFILING.md).  Event times include the kernels' local work.
     exchange = None
     if args.transport == "p2p" and world > 1:
-        s_send = int(out.routing["counts"].sum().item())
         remote = s_send * H * 2 * (world - 1) / world
         per = {"b200moe_permute_peer": remote, "b200moe_combine_peer": remote,
                "b200moe_combine_bwd_peer": 2 * remote, "b200moe_router_bwd_peer": remote}
@@ -714,6 +737,9 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                                 "(device barriers) + NCCL all_reduce(dW_g)" if args.transport == "p2p" else
                                 "NCCL all_to_all_single (exact splits) + all_reduce(dW_g)"),
                        "transport": args.transport,
+                       "launch": ("eager (one Python call chain per step)" if eager else
+                                  f"CUDA graph of the {args.steps} timed steps per rank, replayed once untimed "
+                                  f"before the timed replay"),
                        "l2": "inputs > L2, no flush (expert weights + activations)"},
             "mfu": {"measured_peak": round(flops / (ms_max * 1e-3) / (world * peak * 1e12), 4),
                     "spec_2250": round(flops / (ms_max * 1e-3) / (world * 2.25e15), 4)},
@@ -733,5 +759,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                     "h2d": e2e_rank["h2d"], "d2h": e2e_rank["d2h"]},
             "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": prof.launches,
             "exchange": exchange,
+            "kernels_ms_per_step": {n.replace("b200moe_", ""): round(t_ / n_prof, 4) for n, (t_, c) in kt.items()},
+            "kept_slots_per_rank": s_ranks,
         }
         print(json.dumps(line), flush=True)
