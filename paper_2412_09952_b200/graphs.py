@@ -24,8 +24,11 @@ Rules for a captured step (the same as for any CUDA graph):
     the stream they were created on (the default stream), which a capture
     cannot wait on.
 
-Expert-parallel layers are not graph-capturable: their transport checks run
-on the host per call (`ep.ExpertParallelMoE`)."""
+Expert-parallel layers (`ep.ExpertParallelMoE`) capture the same way on every
+rank -- device barriers, peer kernels and the NCCL all_reduce are stream
+work -- once the token-count agreement (one host all_reduce per new T) has
+run eagerly; their buffer-generation check is evaluated at capture time, so
+a captured step must own its buffer slot (one layer, one slot)."""
 
 from __future__ import annotations
 
