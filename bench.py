@@ -271,7 +271,8 @@ def run_e2e(steps, T, x, dy, step, graphed=False):
     step i computes (double-buffered, as a training loop's data prefetch); y
     leaves on a second copy stream as soon as the forward is done (overlapping
     the backward), dx and the loss right after the backward (overlapping the
-    next step).  Every copy is inside the timed region; the region ends when
+    next step).  x is copied before dy and a step waits for dy only before its
+    backward, so the first step's forward overlaps its dy copy.  Every copy is inside the timed region; the region ends when
     the last D2H copy has landed.  With `graphed`, each of the two input
     buffers has its step captured as a CUDA graph (y's D2H copy is a node of
     it) and the loop replays them; the H2D prefetch and the dx / loss copies
@@ -286,10 +287,14 @@ def run_e2e(steps, T, x, dy, step, graphed=False):
     cs = torch.cuda.Stream()
     ds = torch.cuda.Stream()
     main = torch.cuda.current_stream()
-    copied = [torch.cuda.Event() for _ in range(2)]
+    copied = [torch.cuda.Event() for _ in range(2)]                  # x landed
+    # dy landed: waited on only before the backward (so a step's forward starts
+    # as soon as its x is in); external, so that inside a captured graph the
+    # wait is a node that honours the record made before each replay
+    dy_copied = [torch.cuda.Event(external=True) for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
     landed = [torch.cuda.Event() for _ in range(2)]     # dx of the buffer's last step copied out
-    for ev in consumed + landed:
+    for ev in consumed + landed + dy_copied:
         ev.record(main)
 
     def prefetch(i):
@@ -297,13 +302,18 @@ def run_e2e(steps, T, x, dy, step, graphed=False):
         with torch.cuda.stream(cs):
             cs.wait_event(consumed[b])
             bufs[b][0].copy_(xh, non_blocking=True)
-            bufs[b][1].copy_(dyh, non_blocking=True)
             copied[b].record(cs)
+            bufs[b][1].copy_(dyh, non_blocking=True)
+            dy_copied[b].record(cs)
 
     def fwd_bwd(b):
         cur = torch.cuda.current_stream()
         xin = bufs[b][0].detach().requires_grad_()
-        out, aux = step(xin, bufs[b][1], lambda y: _d2h(ds, cur, y, yh[b]))
+
+        def after_forward(y):
+            _d2h(ds, cur, y, yh[b])
+            cur.wait_event(dy_copied[b])
+        out, aux = step(xin, bufs[b][1], after_forward)
         return xin, aux
 
     def results(b, slot, xin, aux):
@@ -357,7 +367,7 @@ def run_e2e(steps, T, x, dy, step, graphed=False):
     return {"value": round(T / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb + 4,
             "ms_per_step": round(e2e_ms, 4),
-            "h2d": "x, dy from pinned host, copy stream double-buffered one step ahead",
+            "h2d": "x, dy from pinned host, copy stream double-buffered one step ahead (dy waited for before the backward)",
             "d2h": "y (after the forward, overlapping the backward), dx and the aux loss to pinned host every step",
             "launch": ("CUDA graph per input buffer (y's copy to host is a node of it; dx and the loss are copied "
                        "after the replay, overlapping the next step)") if graphed else "eager"}

@@ -11,7 +11,11 @@
  * Conventions
  *  - Every pointer is a DEVICE pointer unless named *_host.  No function
  *    allocates: outputs and workspaces are caller-owned (PyTorch's allocator).
- *  - All work is enqueued on `stream`; nothing synchronises the host.
+ *  - All work is enqueued on `stream`; nothing synchronises the host.  The
+ *    state a call leaves for the next one lives on the device (the dispatch
+ *    scan's epoch word, the router-wgrad tickets, segment counts read by the
+ *    GEMMs), so a sequence of calls can be recorded into a CUDA graph and
+ *    replayed (paper_2412_09952_b200/graphs.py does this for a layer step).
  *  - bf16 tensors are passed as `void*` (row-major, contiguous).
  *  - Return 0 on success or a negative B200MOE_ERR_* code; the message is in
  *    b200moe_last_error() (thread-local).  Codes map to the reference's

@@ -118,6 +118,14 @@ struct Geo {
 #define B200_BWD2_LOAD_BUFS 1
 #endif
     static constexpr int kEpiLoadBufs = B200_BWD2_LOAD_BUFS;
+    // In place: the a/b load buffers double as the da/db store staging (same
+    // 32 x 32 SWIZZLE_64B box), 4 KB per epilogue warp instead of 8, which buys
+    // a 6th operand stage; a chunk's loads are issued once the previous
+    // chunk's stores have read the buffers.
+#ifndef B200_BWD2_INPLACE
+#define B200_BWD2_INPLACE 1
+#endif
+    static constexpr bool kInPlace = kTmaEpiLoads && B200_BWD2_INPLACE;
     // Store-ring depth per epilogue warp (4 buffers + 5 stages measured no
     // better than 2 + 6 for WGRAD on B200).
     static constexpr int kRing = 2;
@@ -132,10 +140,11 @@ struct Geo {
     static constexpr bool kAccLoads = (kMode == kWgradAcc);  // old-gradient TMA load ring (2 x 2 KB per warp)
     static constexpr int kStageBytes = kPairAcc ? 3 * 16384 : Cfg<kCG>::kStageBytes;
     static constexpr int kStages = kPairAcc ? 4 : (kAccLoads ? (kCG == 2 ? 5 : 3)
-                                                             : (kTmaEpiLoads ? (kEpiLoadBufs == 1 ? 5 : 4)
+                                                             : (kTmaEpiLoads ? (kInPlace ? 6 : (kEpiLoadBufs == 1 ? 5 : 4))
                                                                              : (kWide ? 5 : Cfg<kCG>::kStages)));
-    static constexpr int kEpiWarpBytes = (kTmaEpiLoads ? kEpiLoadBufs * 2 * 2048 : 0) + (kAccLoads ? 2 * 2048 : 0) +
-                                         kRing * kStoreBytes;
+    static constexpr int kEpiWarpBytes = kInPlace ? 2 * 2048
+                                                  : (kTmaEpiLoads ? kEpiLoadBufs * 2 * 2048 : 0) +
+                                                        (kAccLoads ? 2 * 2048 : 0) + kRing * kStoreBytes;
     static constexpr int kSmemBytes = kStages * kStageBytes + kNumEpiWarps * kEpiWarpBytes +
                                       1024 /*align*/ + 512 /*barriers*/ + 4 * (kMaxSeg + 2) +
                                       3 * 4 * kMaxSeg /*segment table*/;
@@ -585,6 +594,53 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
             // experiment switches: debug & 32 skips the a/b loads, & 64 the stores
             const bool no_ld = a.debug & 32, no_st = a.debug & 64;
             const int col0 = ti.n_tile * kBN + half * 128;
+            if constexpr (Geo<kMode, kCG>::kInPlace) {
+                // buffers: a chunk at ld.base (then da), b chunk at +2 KB (then db)
+                uint8_t* const abuf = ld.base;
+                uint8_t* const bbuf = ld.base + kStageBufBytes;
+                auto issue = [&](int col) {
+                    if (lane == 0) ptx::bulk_wait_read<0>();   // the previous chunk's stores have read the buffers
+                    __syncwarp();
+                    ld.idx = 0;
+                    epi_load_issue(ld, &tm.m[2], &tm.m[3], col, row0, lane);
+                };
+                if (live) issue(col0);
+                ptx::mbar_wait(tfull, tphase);
+                ptx::tc_fence_after();
+                if (!live) return;
+#pragma unroll 1
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int c = cc * 32;
+                    ptx::tmem_ld_32x32b_x32(lane_addr + half * 128 + c, r0);
+                    epi_load_take(ld, 0, lane, v0, v1);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float dm = __uint_as_float(r0[i]);
+                        const float av = v0[i], bv = v1[i];
+                        const float sg = sigmoidf_(av);
+                        v0[i] = dm * bv * (sg * (1.0f + av * (1.0f - sg)));
+                        v1[i] = dm * (av * sg);
+                    }
+                    uint4* ra = reinterpret_cast<uint4*>(abuf + lane * 64);
+                    uint4* rb = reinterpret_cast<uint4*>(bbuf + lane * 64);
+                    const int sw = (lane >> 1) & 3;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        ra[j ^ sw] = pack8(v0 + 8 * j);
+                        rb[j ^ sw] = pack8(v1 + 8 * j);
+                    }
+                    ptx::fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&tm.st[0], abuf, col0 + c, row0);
+                        ptx::tma_store_2d(&tm.st[1], bbuf, col0 + c, row0);
+                        ptx::bulk_commit();
+                    }
+                    if (cc + 1 < 4) issue(col0 + c + 32);
+                }
+                return;
+            }
             if (live && !no_ld) {
                 if (Geo<kMode, kCG>::kEpiLoadBufs == 1) ld.idx = 0;
                 epi_load_issue(ld, &tm.m[2], &tm.m[3], col0, row0, lane);
@@ -1039,8 +1095,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) moe_gemm_kernel(const __grid_c
         int acc = 0;
         uint32_t acc_phase = 0;
         EpiRing ring{staging + (warp - 2) * G::kEpiWarpBytes, 0};
-        EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + G::kRing * G::kStoreBytes, ldbar + 2 * (warp - 2), 0,
-                    0};
+        EpiLoads ld{staging + (warp - 2) * G::kEpiWarpBytes + (G::kInPlace ? 0 : G::kRing * G::kStoreBytes),
+                    ldbar + 2 * (warp - 2), 0, 0};
         if constexpr (kMode == kWgradW) {
             uint32_t tphase = 0;
             for (int t = cid; t < sched.total; t += ncl) {
