@@ -37,6 +37,9 @@ from .moe import (DeviceRoutingStats, GateConfig, SEG_PAD, _acc_targets, _arange
                   _router_ws, _swizzled, _wgrad_call, _wgrad_outputs, _wgrad_tickets, expert_capacity)
 
 
+_INDEX_CACHE: dict = {}   # EPPlan key -> {(kind, device): index tensors}; read-only after creation
+
+
 @dataclass
 class EPPlan:
     """Static layout of one EP step (identical on every rank)."""
@@ -71,17 +74,28 @@ class EPPlan:
 
     def recv_segments(self, device):
         """(base, expert) of the R * E_local received segments: segment
-        (src, el) starts at (src * E_local + el) * cap_pad."""
-        n = self.world * self.e_local
-        base = torch.arange(n, dtype=torch.int32, device=device) * self.cap_pad
-        expert = torch.arange(n, dtype=torch.int32, device=device) % self.e_local
-        return base, expert
+        (src, el) starts at (src * E_local + el) * cap_pad.  Built once per
+        (plan, device) and cached (no per-step index kernels)."""
+        key = ("recv", device)
+        if key not in _INDEX_CACHE.setdefault(self._key(), {}):
+            n = self.world * self.e_local
+            base = torch.arange(n, dtype=torch.int32, device=device) * self.cap_pad
+            expert = torch.arange(n, dtype=torch.int32, device=device) % self.e_local
+            _INDEX_CACHE[self._key()][key] = (base, expert)
+        return _INDEX_CACHE[self._key()][key]
 
     def peer_seg_base(self, device) -> torch.Tensor:
         """[E] row of (this rank, expert e) inside expert e's owner receive buffer:
-        (rank * E_local + e % E_local) * cap_pad."""
-        e = torch.arange(self.n_experts, dtype=torch.int32, device=device)
-        return ((self.rank * self.e_local + e % self.e_local) * self.cap_pad).to(torch.int32)
+        (rank * E_local + e % E_local) * cap_pad (cached like recv_segments)."""
+        key = ("peer", device)
+        if key not in _INDEX_CACHE.setdefault(self._key(), {}):
+            e = torch.arange(self.n_experts, dtype=torch.int32, device=device)
+            _INDEX_CACHE[self._key()][key] = ((self.rank * self.e_local + e % self.e_local) *
+                                              self.cap_pad).to(torch.int32)
+        return _INDEX_CACHE[self._key()][key]
+
+    def _key(self):
+        return (self.world, self.rank, self.n_experts, self.cap_pad)
 
     def exchange_counts(self, counts: torch.Tensor, group=None) -> torch.Tensor:
         """counts[E] (tokens this rank sends to each expert) -> recv[R * E_local]
