@@ -172,11 +172,16 @@ int b200moe_router_bwd(const void* dxp, const int32_t* slot_rank, const int32_t*
 int b200moe_permute_peer(const void* x, const int32_t* slot_rank, const int32_t* seg_base, const int32_t* counts,
                          int T, int H, int E, int e_per_rank, int rank, const uint64_t* xp_bufs,
                          const uint64_t* count_bufs, cudaStream_t stream);
+/* og (optional, [T, og_k, H] bf16): combine_peer also writes every token's
+ * gathered expert rows there (row j = its j-th kept expert, ascending), and
+ * combine_bwd_peer then reads them locally instead of from the owners' buffers,
+ * so the backward's NVLink traffic is only the dO stores.  NULL: read remote. */
 int b200moe_combine_peer(const uint64_t* o_bufs, int e_per_rank, const float* gates, const int32_t* slot_rank,
-                         const int32_t* seg_base, int T, int H, int E, void* y, cudaStream_t stream);
+                         const int32_t* seg_base, int T, int H, int E, void* y, void* og, int og_k,
+                         cudaStream_t stream);
 int b200moe_combine_bwd_peer(const void* dy, const uint64_t* o_bufs, const float* gates, const int32_t* slot_rank,
                              const int32_t* seg_base, const int32_t* counts, int T, int H, int E, int e_per_rank,
-                             const uint64_t* dout_bufs, float* dg, cudaStream_t stream);
+                             const uint64_t* dout_bufs, float* dg, const void* og, int og_k, cudaStream_t stream);
 int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
                             const int32_t* seg_base, const float* dg, const float* dgates_ext,
                             int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates, const float* probs,

@@ -44,8 +44,8 @@ SIGNATURES = {
                            _P, _P, _P, _P, _P],
     "b200moe_router_wgrad": [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P],
     "b200moe_permute_peer": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P],
-    "b200moe_combine_peer": [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P],
-    "b200moe_combine_bwd_peer": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P],
+    "b200moe_combine_peer": [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _P],
+    "b200moe_combine_bwd_peer": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "b200moe_router_bwd_peer": [_P, _I, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I,
                                 _I, _P, _P, _P, _P, _P],
     "b200moe_importance_fwd": [_P, _I, _I, _P, _P, _P, _P],

@@ -110,10 +110,14 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
     }
 }
 
+// og (optional): the gathered expert rows, og[(t * og_k + j) * H] = token t's
+// j-th kept row (ascending expert), written while they pass through registers
+// so that the backward reads them locally instead of over NVLink again.
 template <bool kPeer>
 __global__ void __launch_bounds__(kPermThreads)
 combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restrict__ slot_rank,
-               const int32_t* __restrict__ seg_base, int T, int H, int E, __nv_bfloat16* __restrict__ y) {
+               const int32_t* __restrict__ seg_base, int T, int H, int E, __nv_bfloat16* __restrict__ y,
+               __nv_bfloat16* __restrict__ og, int og_k) {
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * (kPermThreads / 32) + (threadIdx.x >> 5);
     if (t >= T) return;
@@ -129,6 +133,8 @@ combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restric
         // latency-bound single-row loop reached only ~0.6 of the link
         const uint4* s0 = reinterpret_cast<const uint4*>(o.base<kPeer>(experts[0]) + (size_t)rows[0] * H);
         const uint4* s1 = reinterpret_cast<const uint4*>(o.base<kPeer>(experts[1]) + (size_t)rows[1] * H);
+        uint4* m0 = og ? reinterpret_cast<uint4*>(og + (size_t)t * og_k * H) : nullptr;
+        uint4* m1 = og ? m0 + nvec : nullptr;
         const float g0 = g[0], g1 = g[1];
         for (int base = 0; base < nvec; base += 32 * 4) {
             uint4 v0[4], v1[4];
@@ -138,6 +144,16 @@ combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restric
                 if (j < nvec) {
                     v0[i] = kPeer ? s0[j] : ld_nc_v4(s0 + j);
                     v1[i] = kPeer ? s1[j] : ld_nc_v4(s1 + j);
+                }
+            }
+            if (m0) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = base + i * 32 + lane;
+                    if (j < nvec) {
+                        m0[j] = v0[i];
+                        m1[j] = v1[i];
+                    }
                 }
             }
 #pragma unroll
@@ -169,6 +185,14 @@ combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restric
                 const int j = base + i * 32 + lane;
                 if (j < nvec) v[i] = kPeer ? src[j] : ld_nc_v4(src + j);
             }
+            if (og) {
+                uint4* m = reinterpret_cast<uint4*>(og + ((size_t)t * og_k + r) * H);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = base + i * 32 + lane;
+                    if (j < nvec) m[j] = v[i];
+                }
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 float f[8];
@@ -185,12 +209,14 @@ combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restric
     }
 }
 
+// og (optional): the forward's gathered rows (combine_kernel): read locally
+// instead of from the owners' buffers.
 template <bool kPeer>
 __global__ void __launch_bounds__(kPermThreads)
 combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __restrict__ gates,
                    const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
                    const int32_t* __restrict__ counts, int T, int H, int E, int token_blocks, Rows dout,
-                   float* __restrict__ dg) {
+                   float* __restrict__ dg, const __nv_bfloat16* __restrict__ og, int og_k) {
     if ((int)blockIdx.x >= token_blocks) {
         const int e = blockIdx.x - token_blocks;
         zero_pad_rows(dout.base<kPeer>(e), seg_base, counts, e, H);
@@ -211,8 +237,11 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __
     if (n == 2) {
         // top-2 tokens: dy and both expert rows' loads in flight together
         // (12 x 16 B per lane) before the dot products and the two stores
-        const uint4* os0 = reinterpret_cast<const uint4*>(o.base<kPeer>(experts[0]) + (size_t)rows[0] * H);
-        const uint4* os1 = reinterpret_cast<const uint4*>(o.base<kPeer>(experts[1]) + (size_t)rows[1] * H);
+        const bool mir = og != nullptr;
+        const uint4* os0 = mir ? reinterpret_cast<const uint4*>(og + (size_t)t * og_k * H)
+                               : reinterpret_cast<const uint4*>(o.base<kPeer>(experts[0]) + (size_t)rows[0] * H);
+        const uint4* os1 = mir ? os0 + nvec
+                               : reinterpret_cast<const uint4*>(o.base<kPeer>(experts[1]) + (size_t)rows[1] * H);
         uint4* ds0 = reinterpret_cast<uint4*>(dout.base<kPeer>(experts[0]) + (size_t)rows[0] * H);
         uint4* ds1 = reinterpret_cast<uint4*>(dout.base<kPeer>(experts[1]) + (size_t)rows[1] * H);
         const float g0 = g[0], g1 = g[1];
@@ -224,8 +253,8 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __
                 const int j = base + i * 32 + lane;
                 if (j < nvec) {
                     dv[i] = ld_nc_v4(src + j);
-                    v0[i] = kPeer ? os0[j] : ld_nc_v4(os0 + j);
-                    v1[i] = kPeer ? os1[j] : ld_nc_v4(os1 + j);
+                    v0[i] = (kPeer && !mir) ? os0[j] : ld_nc_v4(os0 + j);
+                    v1[i] = (kPeer && !mir) ? os1[j] : ld_nc_v4(os1 + j);
                 }
             }
             // per-chunk fma chains in the general path's order (bit-identical dg)
@@ -275,7 +304,8 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __
             unpack8(v, d[i]);
         }
         for (int r = 0; r < n; ++r) {
-            const uint4* os = reinterpret_cast<const uint4*>(o.base<kPeer>(experts[r]) + (size_t)rows[r] * H);
+            const uint4* os = og ? reinterpret_cast<const uint4*>(og + ((size_t)t * og_k + r) * H)
+                                 : reinterpret_cast<const uint4*>(o.base<kPeer>(experts[r]) + (size_t)rows[r] * H);
             uint4* ds = reinterpret_cast<uint4*>(dout.base<kPeer>(experts[r]) + (size_t)rows[r] * H);
             float s = 0.f;
 #pragma unroll
@@ -283,7 +313,7 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __
                 const int j = base + i * 32 + lane;
                 if (j < nvec) {
                     float f[8], w[8];
-                    unpack8(kPeer ? os[j] : ld_nc_v4(os + j), f);
+                    unpack8((kPeer && !og) ? os[j] : ld_nc_v4(os + j), f);
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                         s = fmaf(d[i][c], f[c], s);
@@ -357,19 +387,21 @@ int b200moe_combine(const void* o, const float* gates, const int32_t* slot_rank,
     if (rc) return rc;
     const int tb = ceil_div(T, kPermThreads / 32);
     combine_kernel<false><<<tb, kPermThreads, 0, stream>>>(local_rows((void*)o, E), gates, slot_rank, seg_base, T, H,
-                                                            E, (__nv_bfloat16*)y);
+                                                            E, (__nv_bfloat16*)y, nullptr, 0);
     B200_CHECK_LAUNCH("combine");
     return B200MOE_OK;
 }
 
 int b200moe_combine_peer(const uint64_t* o_bufs, int e_per_rank, const float* gates, const int32_t* slot_rank,
-                         const int32_t* seg_base, int T, int H, int E, void* y, cudaStream_t stream) {
+                         const int32_t* seg_base, int T, int H, int E, void* y, void* og, int og_k,
+                         cudaStream_t stream) {
     int rc = check_perm(T, H, E);
     if (rc) return rc;
     if ((rc = check_peer(E, e_per_rank))) return rc;
+    B200_CHECK_ARG(og == nullptr || (og_k >= 1 && og_k <= E), B200MOE_ERR_CONFIG, "og_k %d outside [1, %d]", og_k, E);
     const int tb = ceil_div(T, kPermThreads / 32);
     combine_kernel<true><<<tb, kPermThreads, 0, stream>>>(peer_rows(o_bufs, e_per_rank), gates, slot_rank, seg_base,
-                                                           T, H, E, (__nv_bfloat16*)y);
+                                                           T, H, E, (__nv_bfloat16*)y, (__nv_bfloat16*)og, og_k);
     B200_CHECK_LAUNCH("combine_peer");
     return B200MOE_OK;
 }
@@ -382,21 +414,22 @@ int b200moe_combine_bwd(const void* dy, const void* o, const float* gates, const
     const int tb = ceil_div(T, kPermThreads / 32);
     combine_bwd_kernel<false><<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)dy, local_rows((void*)o, E),
                                                                     gates, slot_rank, seg_base, counts, T, H, E, tb,
-                                                                    local_rows(dout, E), dg);
+                                                                    local_rows(dout, E), dg, nullptr, 0);
     B200_CHECK_LAUNCH("combine_bwd");
     return B200MOE_OK;
 }
 
 int b200moe_combine_bwd_peer(const void* dy, const uint64_t* o_bufs, const float* gates, const int32_t* slot_rank,
                              const int32_t* seg_base, const int32_t* counts, int T, int H, int E, int e_per_rank,
-                             const uint64_t* dout_bufs, float* dg, cudaStream_t stream) {
+                             const uint64_t* dout_bufs, float* dg, const void* og, int og_k, cudaStream_t stream) {
     int rc = check_perm(T, H, E);
     if (rc) return rc;
     if ((rc = check_peer(E, e_per_rank))) return rc;
+    B200_CHECK_ARG(og == nullptr || (og_k >= 1 && og_k <= E), B200MOE_ERR_CONFIG, "og_k %d outside [1, %d]", og_k, E);
     const int tb = ceil_div(T, kPermThreads / 32);
     combine_bwd_kernel<true><<<tb + E, kPermThreads, 0, stream>>>(
         (const __nv_bfloat16*)dy, peer_rows(o_bufs, e_per_rank), gates, slot_rank, seg_base, counts, T, H, E, tb,
-        peer_rows(dout_bufs, e_per_rank), dg);
+        peer_rows(dout_bufs, e_per_rank), dg, (const __nv_bfloat16*)og, og_k);
     B200_CHECK_LAUNCH("combine_bwd_peer");
     return B200MOE_OK;
 }

@@ -418,8 +418,12 @@ class _EPPeerFunction(torch.autograd.Function):
             A = B = Hh = None
         pb.barrier()                            # all expert outputs are ready
         y = torch.empty(T, H, **bf)
+        # the gathered expert rows are kept for the backward (read locally there
+        # instead of over NVLink again), except in recompute layers (memory)
+        og = None if st.get("recompute") else torch.empty(T * cfg.top_k, H, **bf)
         _lib.call("b200moe_combine_peer", pb.peer[1].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
-                  seg_peer.data_ptr(), T, H, E, y.data_ptr(), s)
+                  seg_peer.data_ptr(), T, H, E, y.data_ptr(), _lib.ptr(og), cfg.top_k, s)
+        ctx.og = og
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_peer,
                              gate_mass=gate_mass, importance=imp, importance_loss=imp_loss, stats=stats, err=err,
                              recv_counts=rcounts.clone())
@@ -467,7 +471,8 @@ class _EPPeerFunction(torch.autograd.Function):
         pbb.barrier()                           # every rank is done with the previous layer's dO / dxp
         _lib.call("b200moe_combine_bwd_peer", dy.data_ptr(), pb.peer[1].data_ptr(), gates.data_ptr(),
                   slot_rank.data_ptr(), seg_peer.data_ptr(), counts.data_ptr(), T, H, E, El, pbb.peer[0].data_ptr(),
-                  dg.data_ptr(), s)
+                  dg.data_ptr(), _lib.ptr(ctx.og), cfg.top_k, s)
+        ctx.og = None
         pbb.barrier()                           # all output gradients have landed
         dA = torch.empty(Rs, F, **bf)
         dB = torch.empty(Rs, F, **bf)
@@ -712,7 +717,8 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     if args.transport == "p2p" and world > 1:
         remote = s_send * H * 2 * (world - 1) / world
         per = {"b200moe_permute_peer": remote, "b200moe_combine_peer": remote,
-               "b200moe_combine_bwd_peer": 2 * remote, "b200moe_router_bwd_peer": remote}
+               # the backward reads the forward's gathered rows locally (og): only the dO stores cross
+               "b200moe_combine_bwd_peer": remote, "b200moe_router_bwd_peer": remote}
         exchange = {}
         for name, nbytes in per.items():
             if name in kt:
