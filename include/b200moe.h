@@ -240,6 +240,14 @@ int b200moe_expert_wgrad_acc(const void* xp, const void* h, const void* dout, co
 int b200moe_expert_bwd2_ex(const void* dout, const void* w2, const void* a_pre, const void* b_pre,
                            const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
                            int H, int F, int E_local, void* da_out, void* db_out, int grid_ctas, cudaStream_t stream);
+/* BWD2 that also writes h = silu(a) * b (bf16, [rows, F]) rebuilt from the
+ * stored a, b, for a caller that did not keep the forward's h (memory): WGRAD's
+ * dW2 operand.  h_out NULL = b200moe_expert_bwd2_ex.  The rebuilt h rounds
+ * silu(bf16 a) * bf16 b, where the forward's h rounds the fp32 accumulators. */
+int b200moe_expert_bwd2_h(const void* dout, const void* w2, const void* a_pre, const void* b_pre,
+                          const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                          int H, int F, int E_local, void* da_out, void* db_out, void* h_out, int grid_ctas,
+                          cudaStream_t stream);
 int b200moe_expert_bwd1_ex(const void* da, const void* db, const void* w1, const void* w3, const int* seg_base,
                            const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
                            void* dxp_out, int grid_ctas, cudaStream_t stream);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "b200moe_expert_wgrad": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
     "b200moe_expert_wgrad_acc": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "b200moe_expert_bwd2_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P],
+    "b200moe_expert_bwd2_h": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "b200moe_expert_bwd1_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P],
     "b200moe_expert_wgrad_ex": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P],
     "b200moe_dense_fwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P],
@@ -124,7 +125,7 @@ KERNELS_PER_CALL = {
     "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 1, "b200moe_router_wgrad": 1,
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_expert_wgrad_acc": 1,
-    "b200moe_expert_bwd1_ex": 1, "b200moe_expert_wgrad_ex": 1, "b200moe_expert_bwd2_ex": 1,
+    "b200moe_expert_bwd1_ex": 1, "b200moe_expert_wgrad_ex": 1, "b200moe_expert_bwd2_ex": 1, "b200moe_expert_bwd2_h": 1,
     "b200moe_dense_fwd": 1, "b200moe_dense_dgrad": 1, "b200moe_dense_wgrad": 1,
     "b200moe_upcycle_copy": 3,
     "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 1,
@@ -201,7 +202,8 @@ class Profiler:
 
 # The grouped-GEMM launches of one layer step form two contiguous runs on the
 # stream: FWD1 -> FWD2 and BWD2 -> WGRAD -> BWD1.
-GEMM_SPANS = (("b200moe_expert_fwd1", "b200moe_expert_bwd2", "b200moe_expert_bwd2_ex", "b200moe_expert_wgrad_ex"),
+GEMM_SPANS = (("b200moe_expert_fwd1", "b200moe_expert_bwd2", "b200moe_expert_bwd2_ex", "b200moe_expert_bwd2_h",
+               "b200moe_expert_wgrad_ex"),
               ("b200moe_expert_fwd2", "b200moe_expert_bwd1", "b200moe_expert_bwd1_ex"))
 
 

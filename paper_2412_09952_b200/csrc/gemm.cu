@@ -614,6 +614,16 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     ptx::tmem_ld_32x32b_x32(lane_addr + half * 128 + c, r0);
                     epi_load_take(ld, 0, lane, v0, v1);
                     ptx::tmem_ld_wait();
+                    if (a.out2) {
+                        // h = silu(a) * b rebuilt from the stored (bf16) a, b for a caller
+                        // that dropped the forward's h (WGRAD's dW2 operand): 64 contiguous
+                        // bytes of this lane's row, straight from registers
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v2[i] = v0[i] * sigmoidf_(v0[i]) * v1[i];
+                        uint4* hp = reinterpret_cast<uint4*>(a.out2 + (size_t)(row0 + lane) * a.F + col0 + c);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) hp[j] = pack8(v2 + 8 * j);
+                    }
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const float dm = __uint_as_float(r0[i]);
@@ -667,6 +677,13 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                     for (int i = 0; i < 32; ++i) { v0[i] = 0.5f; v1[i] = 0.25f; }
                 }
                 ptx::tmem_ld_wait();
+                if (a.out2) {   // h = silu(a) * b for a caller that dropped the forward's h
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v2[i] = v0[i] * sigmoidf_(v0[i]) * v1[i];
+                    uint4* hp = reinterpret_cast<uint4*>(a.out2 + (size_t)(row0 + lane) * a.F + col0 + c);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) hp[j] = pack8(v2 + 8 * j);
+                }
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const float dm = __uint_as_float(r0[i]);
@@ -714,6 +731,13 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
                 for (int i = 0; i < 4; ++i) {
                     unpack8(pa[cur][i], v0 + 8 * i);
                     unpack8(pb[cur][i], v1 + 8 * i);
+                }
+                if (a.out2) {   // h = silu(a) * b for a caller that dropped the forward's h
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v2[i] = v0[i] * sigmoidf_(v0[i]) * v1[i];
+                    uint4* hp = reinterpret_cast<uint4*>(a.out2 + (size_t)(row0 + lane) * a.F + col0 + c);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) hp[j] = pack8(v2 + 8 * j);
                 }
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
@@ -1311,6 +1335,14 @@ int b200moe_expert_bwd2_ex(const void* dout, const void* w2, const void* a_pre, 
                            const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
                            int H, int F, int E_local, void* da_out, void* db_out, int grid_ctas,
                            cudaStream_t stream) {
+    return b200moe_expert_bwd2_h(dout, w2, a_pre, b_pre, seg_base, seg_count, seg_expert, nseg, rows, H, F, E_local,
+                                 da_out, db_out, nullptr, grid_ctas, stream);
+}
+
+int b200moe_expert_bwd2_h(const void* dout, const void* w2, const void* a_pre, const void* b_pre,
+                          const int* seg_base, const int* seg_count, const int* seg_expert, int nseg, int rows,
+                          int H, int F, int E_local, void* da_out, void* db_out, void* h_out, int grid_ctas,
+                          cudaStream_t stream) {
     B200_TRY(check_common(nseg, H, F, E_local));
     TmaSet tm = {};
     B200_TRY(make_map(&tm.m[0], dout, H, rows, H, false));
@@ -1322,7 +1354,7 @@ int b200moe_expert_bwd2_ex(const void* dout, const void* w2, const void* a_pre, 
     B200_TRY(make_map(&tm.st[1], db_out, F, rows, F, false, true));
     tm.st[2] = tm.st[0];
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
-                  (__nv_bfloat16*)da_out, (__nv_bfloat16*)db_out, nullptr,
+                  (__nv_bfloat16*)da_out, (__nv_bfloat16*)db_out, (__nv_bfloat16*)h_out,
                   (const __nv_bfloat16*)a_pre, (const __nv_bfloat16*)b_pre};
     return dispatch_launch<kBwd2>(tm, a, stream, grid_ctas);
 }

@@ -37,6 +37,7 @@ from .moe import (DeviceRoutingStats, GateConfig, SEG_PAD, _acc_targets, _arange
                   _router_ws, _swizzled, _wgrad_call, _wgrad_outputs, _wgrad_tickets, expert_capacity)
 
 
+_TOKENS_CHECKED: set = set()   # (group id, T_local) pairs every rank agreed on (ExpertParallelMoE._check_tokens)
 _INDEX_CACHE: dict = {}   # EPPlan key -> {(kind, device): index tensors}; read-only after creation
 
 
@@ -416,6 +417,9 @@ class _EPPeerFunction(torch.autograd.Function):
             # activations) are dropped here and rebuilt by one FWD1 launch at the
             # start of the backward from xr (kept in the forward set anyway)
             A = B = Hh = None
+        elif st.get("drop_h"):
+            # keep a, b only: BWD2 rebuilds h = silu(a) * b for WGRAD (b200moe_expert_bwd2_h)
+            Hh = None
         pb.barrier()                            # all expert outputs are ready
         y = torch.empty(T, H, **bf)
         # the gathered expert rows are kept for the backward (read locally there
@@ -432,6 +436,7 @@ class _EPPeerFunction(torch.autograd.Function):
         ctx.pb = pb
         ctx.generation = pb.generation
         ctx.recompute = A is None
+        ctx.rebuild_h = A is not None and Hh is None
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer,
                               A, B, Hh)
         return y, gates
@@ -476,9 +481,15 @@ class _EPPeerFunction(torch.autograd.Function):
         pbb.barrier()                           # all output gradients have landed
         dA = torch.empty(Rs, F, **bf)
         dB = torch.empty(Rs, F, **bf)
-        _lib.call("b200moe_expert_bwd2", pbb.do.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
-                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(),
-                  dB.data_ptr(), s)
+        if ctx.rebuild_h:
+            Hh = torch.empty(Rs, F, **bf)
+            _lib.call("b200moe_expert_bwd2_h", pbb.do.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
+                      rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(),
+                      dB.data_ptr(), Hh.data_ptr(), 0, s)
+        else:
+            _lib.call("b200moe_expert_bwd2", pbb.do.data_ptr(), W2.data_ptr(), A.data_ptr(), B.data_ptr(),
+                      rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dA.data_ptr(),
+                      dB.data_ptr(), s)
         dW1, dW2, dW3, acc = _wgrad_outputs(ctx.acc_targets, W1, W2, W3)
         _wgrad_call(acc, pb.xr.data_ptr(), Hh.data_ptr(), pbb.do.data_ptr(), dA.data_ptr(),
                   dB.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El,
@@ -520,7 +531,7 @@ class ExpertParallelMoE:
     TRANSPORTS = ("p2p", "nccl")
 
     def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None, transport: str = "p2p",
-                 buffer_slot: int = 0, recompute: bool = False):
+                 buffer_slot: int = 0, recompute: bool = False, drop_h: bool = False):
         """transport: "p2p" (default) fuses the dispatch/combine exchange into the
         permute/combine kernels over NVLink symmetric memory; "nccl" uses
         all_to_all_single between separate kernels (the comparison baseline).
@@ -542,13 +553,20 @@ class ExpertParallelMoE:
         self.w_g, self.w_noise, self.W1, self.W2, self.W3, self.cfg = w_g, w_noise, W1, W2, W3, cfg
         self.buffer_slot = buffer_slot
         self.recompute = recompute   # p2p: rebuild a, b, h in the backward instead of keeping them
-        self._tokens_checked = set()
+        self.drop_h = drop_h         # p2p: keep a, b only; BWD2 rebuilds h (one third of the memory of a, b, h)
 
     def _check_tokens(self, T: int, device) -> None:
         """The p2p transport sizes every rank's receive segments from T_local
-        (EPPlan.cap_pad), so all ranks must agree on T.  Checked once per T with
-        one all_reduce (max of T and of -T) and a host read."""
-        if T in self._tokens_checked:
+        (EPPlan.cap_pad), so all ranks must agree on T.  Checked once per
+        (group, T) in the process -- with one all_reduce (max of T and of -T)
+        and a host read -- not per layer object: a model builds its layers'
+        ExpertParallelMoE views on every forward, and a per-layer check was a
+        host synchronisation per layer and micro-batch.  Like every collective
+        decision, this assumes SPMD ranks: each rank meets a new T_local in the
+        same call (a rank that alone switched to a T another rank already
+        checked would not join that rank's all_reduce)."""
+        key = (id(self.group) if self.group is not None else None, T)
+        if key in _TOKENS_CHECKED:
             return
         t = torch.tensor([T, -T], dtype=torch.int64, device=device if dist.get_backend(self.group) == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
@@ -556,7 +574,7 @@ class ExpertParallelMoE:
         if hi != T or lo != T:
             raise ShapeError(f"expert-parallel ranks disagree on tokens per rank (this rank {T}, range [{lo}, {hi}]); "
                              f"the p2p transport needs equal T_local on every rank")
-        self._tokens_checked.add(T)
+        _TOKENS_CHECKED.add(key)
 
     def forward(self, x: torch.Tensor, rng=None, training: bool = False, noise=None, reduce_router: bool = True):
         T, H = x.shape
@@ -567,7 +585,7 @@ class ExpertParallelMoE:
         plan = EPPlan.make(self.world, self.rank, self.cfg.n_experts, T, self.cfg.capacity_factor)
         z = _noise(T, self.cfg.n_experts, x.device, self.cfg.noise_enabled and training, rng, noise)
         st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router, buffer_slot=self.buffer_slot,
-                  recompute=self.recompute)
+                  recompute=self.recompute, drop_h=self.drop_h)
         fn = _EPPeerFunction if self.transport == "p2p" else _EPFunction
         y, gates = fn.apply(x.to(torch.bfloat16).contiguous(), self.w_g.to(torch.float32).contiguous(),
                             self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)

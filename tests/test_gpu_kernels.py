@@ -92,6 +92,10 @@ def test_grouped_gemm_all_modes(cg, H, F, counts):
     dA, dB = (torch.full((R, F), float("nan"), **bf) for _ in range(2))
     _lib.call("b200moe_expert_bwd2", dO.data_ptr(), W2.data_ptr(), A.data_ptr(), Bm.data_ptr(), base.data_ptr(),
               cnt.data_ptr(), sege.data_ptr(), E, R, H, F, E, dA.data_ptr(), dB.data_ptr(), s)
+    # BWD2 that also rebuilds h = silu(a) * b (callers that dropped the forward's h)
+    dA2, dB2, H2 = (torch.full((R, F), float("nan"), **bf) for _ in range(3))
+    _lib.call("b200moe_expert_bwd2_h", dO.data_ptr(), W2.data_ptr(), A.data_ptr(), Bm.data_ptr(), base.data_ptr(),
+              cnt.data_ptr(), sege.data_ptr(), E, R, H, F, E, dA2.data_ptr(), dB2.data_ptr(), H2.data_ptr(), 0, s)
     dW1, dW3 = (torch.full((E, F, H), float("nan"), **bf) for _ in range(2))
     dW2 = torch.full((E, H, F), float("nan"), **bf)
     _lib.call("b200moe_expert_wgrad", xp.data_ptr(), Hh.data_ptr(), dO.data_ptr(), dA.data_ptr(), dB.data_ptr(),
@@ -119,10 +123,13 @@ def test_grouped_gemm_all_modes(cg, H, F, counts):
             sg = torch.sigmoid(av)
             assert rel(dA[r].float(), dm * bv * sg * (1 + av * (1 - sg))) < 1e-2, ("bwd2 da", e)
             assert rel(dB[r].float(), dm * av * sg) < 1e-2, ("bwd2 db", e)
+            assert torch.equal(dA2[r], dA[r]) and torch.equal(dB2[r], dB[r]), ("bwd2_h da/db", e)
+            assert rel(H2[r].float(), torch.nn.functional.silu(av) * bv) < 1e-2, ("bwd2_h h", e)
+            assert rel(H2[r].float(), Hh[r].float()) < 1e-2, ("bwd2_h h vs forward h", e)
             dx = dA[r].float() @ W1[e].float() + dB[r].float() @ W3[e].float()
             assert rel(dxp[r].float(), dx) < 1e-2, ("bwd1", e)
         if len(pad):  # padded rows must come out exactly zero
-            for t, n in ((A, "A"), (Hh, "H"), (dA, "dA"), (dB, "dB"), (Oo, "O"), (dxp, "dxp")):
+            for t, n in ((A, "A"), (Hh, "H"), (dA, "dA"), (dB, "dB"), (Oo, "O"), (dxp, "dxp"), (H2, "H2")):
                 assert bool((t[pad] == 0).all()), ("pad", n, e)
         gw1 = dA[r].float().t() @ x
         gw3 = dB[r].float().t() @ x

@@ -109,6 +109,38 @@ def recompute_case(rank, world, dev, T=768, H=512, F=512, E=8, k=2):
     return ok
 
 
+def drop_h_case(rank, world, dev, T=768, H=512, F=512, E=8, k=2):
+    """p2p EP layer that keeps a, b but not h (BWD2 rebuilds h for WGRAD)
+    against the layer keeping h: y, dx, the router and dW1 / dW3 gradients
+    bit-identical (the same kernels on the same a, b, da, db); dW2 = do^T h
+    within bf16 rounding (the rebuilt h rounds silu(bf16 a) * bf16 b)."""
+    El = E // world
+    g = torch.Generator(device=dev).manual_seed(8)
+    W = [(torch.randn(s_, generator=g, device=dev) * 0.05).to(torch.bfloat16) for s_ in ((El, F, H), (El, H, F),
+                                                                                          (El, F, H))]
+    wg = torch.randn(H, E, generator=g, device=dev) * 0.05
+    gx = torch.Generator(device=dev).manual_seed(400 + rank)
+    x = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
+    dy = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
+    cfg = P.GateConfig(n_experts=E, top_k=k, capacity_factor=2.0)
+    res = []
+    for dh in (False, True):
+        lw = [t.clone().requires_grad_() for t in [wg, torch.zeros_like(wg)] + W]
+        ep = ExpertParallelMoE(*lw, cfg, transport="p2p", buffer_slot=42 + int(dh), drop_h=dh)
+        xe = x.clone().requires_grad_()
+        out = ep(xe)
+        ((out.output.float() * dy.float()).sum() + 0.1 * P.importance_penalty(out.gates)).backward()
+        torch.cuda.synchronize()
+        res.append(dict(y=out.output, dx=xe.grad, wg=lw[0].grad, w1=lw[2].grad, w3=lw[4].grad, w2=lw[3].grad))
+    a, b = res
+    exact = all(torch.equal(a[n], b[n]) for n in ("y", "dx", "wg", "w1", "w3"))
+    r2 = rel(b["w2"], a["w2"])
+    ok = exact and r2 < 1e-2
+    print(f"rank {rank}: {'PASS' if ok else 'FAIL'} [p2p drop_h] y/dx/dW_g/dW1/dW3 bit-identical={exact}, "
+          f"dW2 rel {r2:.2e}", flush=True)
+    return ok
+
+
 def oracle_case(rank, world, dev, T, H, F, router, policy, cf, noise, transport, E=8, k=2, lam=0.1):
     """EP layer against the CPU ORACLE (oracle/moe_oracle.py, the reference's
     closed form, moefold/moe.py:250-283) on each rank's own batch: routing
@@ -200,6 +232,7 @@ def main():
         ok &= oracle_case(rank, world, dev, 512, 256, 512, "mixtral", "position", 1.0, True, transport)
         ok &= oracle_case(rank, world, dev, 384, 256, 256, "st", "score", None, False, transport)
     ok &= recompute_case(rank, world, dev)
+    ok &= drop_h_case(rank, world, dev)
     # canary bands around every symmetric receive plane (written by peers over NVLink) untouched
     from paper_2412_09952_b200.ep import _PeerBuffers
     torch.cuda.synchronize()

@@ -54,6 +54,44 @@ def random_dense(cfg, device):
     return P.DenseCheckpoint(config=cfg, tensors=tensors)
 
 
+def profile_step(step, rank, world):
+    """One step under torch.profiler: device time per kernel name, the busy
+    (union) time and the window, written to gpurun_out/model_prof_r<rank>.json."""
+    from torch.profiler import ProfilerActivity, profile
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    spans, per = [], {}
+    for e in prof.events():
+        if e.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        d = e.time_range.end - e.time_range.start
+        k = per.setdefault(e.name[:120], [0.0, 0])
+        k[0] += d
+        k[1] += 1
+        spans.append((e.time_range.start, e.time_range.end))
+    spans.sort()
+    busy, cs, ce = 0.0, None, None
+    for s_, e_ in spans:
+        if ce is None or s_ > ce:
+            if ce is not None:
+                busy += ce - cs
+            cs, ce = s_, e_
+        else:
+            ce = max(ce, e_)
+    if ce is not None:
+        busy += ce - cs
+    out = {"rank": rank, "window_us": (spans[-1][1] - spans[0][0]) if spans else 0, "busy_us": busy,
+           "kernels": sorted(([n, round(t, 1), c] for n, (t, c) in per.items()), key=lambda r: -r[1])[:60]}
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(f"gpurun_out/model_prof_r{rank}.json", "w") as f:
+        json.dump(out, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=2)
@@ -79,6 +117,11 @@ def main():
                     help="persistent-grid cap of the projection GEMMs (0 = all SMs; caps measured no faster)")
     ap.add_argument("--zero", action="store_true",
                     help="ZeRO-1: shard the replicated tensors' optimizer state over the ranks")
+    ap.add_argument("--drop-h", action="store_true",
+                    help="MoE layers outside the recompute set keep a, b but not h (BWD2 rebuilds it)")
+    ap.add_argument("--profile", action="store_true",
+                    help="after the timed steps, one more step under torch.profiler (CUPTI kernel records) on every "
+                         "rank: kernel time by name -> gpurun_out/model_prof_r<rank>.json")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = 0
@@ -134,7 +177,8 @@ def main():
         for mb, (inputs, targets) in enumerate(batches):
             last = mb == M - 1
             fwd = P.forward_with_stats(moe, inputs, training=True, compute=state.compute, ep_group=group,
-                                       transport=a.transport, recompute_layers=range(a.recompute))
+                                       transport=a.transport, recompute_layers=range(a.recompute),
+                                       drop_h_layers=range(cfg.layers) if a.drop_h else ())
             loss = P.cross_entropy(fwd.logits, targets)
             for g in fwd.gates:
                 loss = loss + (aux / len(fwd.gates)) * P.importance_penalty(g)
@@ -175,6 +219,8 @@ def main():
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) / a.steps
     clocks = clk.summary()
+    if a.profile:
+        profile_step(step, rank, world)
     ms = float(np.median([e[0].elapsed_time(e[3]) for e in evs]))
     if world > 1:   # the step takes as long as the slowest rank
         t = torch.tensor([ms, float(kept)], device=dev, dtype=torch.float64)
@@ -202,7 +248,7 @@ def main():
         "expert_grad_accumulation": "fused into WGRAD" if (M > 1 and not a.no_fused_acc) else "autograd", "kept_slots_per_layer_per_rank": kept, "params_rank0": n_params,
         "max_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 1),
         "optimizer_state_gb_rank0": round(opt.state_bytes() / 2**30, 2), "zero1": bool(a.zero),
-        "recompute_moe_layers": a.recompute,
+        "recompute_moe_layers": a.recompute, "drop_h": bool(a.drop_h),
         "projections": "torch.matmul (cuBLAS), A/B run" if a.cublas_proj else
         f"tcgen05 dense GEMM (tensor.linear), grid cap {PT0._DENSE_GRID or 148}",
         "clocks": clocks,
