@@ -283,14 +283,18 @@ class _EPFunction(torch.autograd.Function):
 
 class _PeerBuffers:
     """Symmetric-memory receive buffers of the p2p transport.  A *forward*
-    set per (buffer slot, receive rows, hidden, group) holds xr (tokens in) and
-    O (expert outputs), each [R*E_local*cap_pad, H] bf16, plus the int32
-    receive-count table; xr and O are saved for the layer's backward, so every
-    layer alive in one autograd graph needs its own slot (the model forward
-    uses the layer index).  The *backward* planes dO and dxp live only inside
-    one layer's backward, and backward passes run one layer at a time, so one
-    set (slot -1) serves every layer.  Peers address the planes through device
-    arrays of per-rank base pointers; canary bands surround every plane."""
+    set per (buffer slot, receive rows, hidden, group) holds xr (tokens in,
+    [R*E_local*cap_pad, H] bf16) plus the int32 receive-count table; xr is
+    saved for the layer's backward (WGRAD's operand, and the recompute FWD1's
+    input), so every layer alive in one autograd graph needs its own slot (the
+    model forward uses the layer index).  The *shared* set (slot -1) holds two
+    planes that are live only transiently: O (expert outputs: written by FWD2,
+    read by the peers' combine right after, never in the backward, which uses
+    the combine's local row mirror `og`) and dO / dxp (inside one layer's
+    backward).  Every user of a shared plane is preceded by a device barrier
+    of all ranks, so one set serves every layer's forward and backward.  Peers
+    address the planes through device arrays of per-rank base pointers; canary
+    bands surround every plane."""
 
     _cache: dict = {}
     GUARD = 4096          # canary bytes before, between and after the planes
@@ -308,15 +312,17 @@ class _PeerBuffers:
 
     @classmethod
     def backward_set(cls, rows: int, H: int, group, device):
+        """The shared set (O in the forward, dO / dxp in the backward)."""
         return cls.get(rows, H, 0, group, device, slot=-1)
 
     def __init__(self, rows, H, n_counts, grp, device):
         import torch.distributed._symmetric_memory as symm
-        self.generation = 0   # bumped by every forward that (re)fills xr / O
+        self.generation = 0   # bumped by every forward that (re)fills xr
         G = self.GUARD
         plane = rows * H * 2
-        offs = [G + i * (plane + G) for i in range(2)]
-        cnt_off = offs[1] + plane + G
+        nplanes = 1 if n_counts else 2      # forward set: xr;  shared set: O / dO and dxp
+        offs = [G + i * (plane + G) for i in range(nplanes)]
+        cnt_off = offs[-1] + plane + G
         cnt_bytes = ((n_counts * 4 + 255) // 256) * 256
         total = cnt_off + cnt_bytes + G
         self.raw = symm.empty(total, dtype=torch.uint8, device=device)
@@ -338,14 +344,14 @@ class _PeerBuffers:
     def barrier(self):
         self.handle.barrier(channel=0)
 
-    # forward set: plane 0 = xr, plane 1 = O;  backward set: plane 0 = dO, plane 1 = dxp
+    # forward set: plane 0 = xr;  shared set: plane 0 = O (forward) / dO (backward), plane 1 = dxp
     @property
     def xr(self):
         return self.views[0]
 
     @property
     def o(self):
-        return self.views[1]
+        return self.views[0]
 
     @property
     def do(self):
@@ -374,6 +380,7 @@ class _EPPeerFunction(torch.autograd.Function):
         rt = _lib.ROUTER[cfg.router_type]
         Rs = plan.send_rows
         pb = _PeerBuffers.get(Rs, H, plan.world * El, group, dev, st.get("buffer_slot", 0))
+        pbs = _PeerBuffers.backward_set(Rs, H, group, dev)   # O lives in the shared set's first plane
 
         logits = torch.empty(T, E, **f32)
         gates = torch.empty(T, E, **f32)
@@ -411,7 +418,7 @@ class _EPPeerFunction(torch.autograd.Function):
         _lib.call("b200moe_expert_fwd1", pb.xr.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
                   rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, A.data_ptr(), B.data_ptr(), Hh.data_ptr(), s)
         _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
-                  rexp.data_ptr(), nseg, Rs, H, F, El, pb.o.data_ptr(), s)
+                  rexp.data_ptr(), nseg, Rs, H, F, El, pbs.o.data_ptr(), s)
         if st.get("recompute"):
             # selective recompute: a, b, h ([rows, F] x 3, the layer's largest
             # activations) are dropped here and rebuilt by one FWD1 launch at the
@@ -423,9 +430,9 @@ class _EPPeerFunction(torch.autograd.Function):
         pb.barrier()                            # all expert outputs are ready
         y = torch.empty(T, H, **bf)
         # the gathered expert rows are kept for the backward (read locally there
-        # instead of over NVLink again), except in recompute layers (memory)
-        og = None if st.get("recompute") else torch.empty(T * cfg.top_k, H, **bf)
-        _lib.call("b200moe_combine_peer", pb.peer[1].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
+        # instead of over NVLink again; O's plane is reused by the next layer)
+        og = torch.empty(T * cfg.top_k, H, **bf)
+        _lib.call("b200moe_combine_peer", pbs.peer[0].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
                   seg_peer.data_ptr(), T, H, E, y.data_ptr(), _lib.ptr(og), cfg.top_k, s)
         ctx.og = og
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_peer,
@@ -474,7 +481,7 @@ class _EPPeerFunction(torch.autograd.Function):
         dy = (torch.zeros(T, H, **bf) if dy is None else dy).to(torch.bfloat16).contiguous()
         dg = torch.empty(T, E, **f32)
         pbb.barrier()                           # every rank is done with the previous layer's dO / dxp
-        _lib.call("b200moe_combine_bwd_peer", dy.data_ptr(), pb.peer[1].data_ptr(), gates.data_ptr(),
+        _lib.call("b200moe_combine_bwd_peer", dy.data_ptr(), pbb.peer[0].data_ptr(), gates.data_ptr(),
                   slot_rank.data_ptr(), seg_peer.data_ptr(), counts.data_ptr(), T, H, E, El, pbb.peer[0].data_ptr(),
                   dg.data_ptr(), _lib.ptr(ctx.og), cfg.top_k, s)
         ctx.og = None
