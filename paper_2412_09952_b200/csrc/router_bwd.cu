@@ -144,8 +144,11 @@ struct DhIn {
     int e_per_rank;
 };
 
+#ifndef B200_DX_MIN_BLOCKS
+#define B200_DX_MIN_BLOCKS 2
+#endif
 template <int EP, int KM, bool kNoise, bool kFused = false>
-__global__ void __launch_bounds__(kDxThreads)
+__global__ void __launch_bounds__(kDxThreads, B200_DX_MIN_BLOCKS)
 router_dx_kernel(const __nv_bfloat16* __restrict__ dxp_local, const uint64_t* __restrict__ dxp_bufs,
                  const int32_t* __restrict__ rows_in,
                  float* __restrict__ dh, float* __restrict__ dn, const float4* __restrict__ wsw,

@@ -11,6 +11,6 @@ for rep in $(seq ${REPS:-3}); do
     python -c "
 import json;d=json.load(open('gpurun_out/ab_$v.json'))
 k=d['kernels_ms_per_step']
-print('$v', d['ms_per_step'], d['roofline']['gemm_ms_per_step'], d['clocks']['sm_mhz'], ' '.join(f'{n[7:]}={t}' for n,t in k.items() if n.startswith('expert')))" || tail -3 gpurun_out/ab_$v.err
+print('$v', d['ms_per_step'], d['roofline']['gemm_ms_per_step'], d['clocks']['sm_mhz'], ' '.join(f'{n[7:]}={t}' for n,t in k.items() if n.startswith('expert')), '|', ' '.join(f'{n}={t}' for n,t in k.items() if not n.startswith('expert')))" || tail -3 gpurun_out/ab_$v.err
   done
 done
