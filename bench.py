@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                    help="EP exchange: fused NVLink peer-memory kernels (default) or NCCL all-to-all")
     p.add_argument("--gemm-debug", type=int, default=0, help=argparse.SUPPRESS)  # A/B experiment switches
+    p.add_argument("--ep-pull", action="store_true", help=argparse.SUPPRESS)   # EP: peers pull expert rows (A/B)
     return p.parse_args()
 
 

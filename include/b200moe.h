@@ -182,6 +182,24 @@ int b200moe_combine_peer(const uint64_t* o_bufs, int e_per_rank, const float* ga
 int b200moe_combine_bwd_peer(const void* dy, const uint64_t* o_bufs, const float* gates, const int32_t* slot_rank,
                              const int32_t* seg_base, const int32_t* counts, int T, int H, int E, int e_per_rank,
                              const uint64_t* dout_bufs, float* dg, const void* og, int og_k, cudaStream_t stream);
+/* FWD2 / BWD1 fused with the return exchange: every output row tile goes
+ * straight from the epilogue (TMA bulk store) into its source rank's receive
+ * plane over NVLink, overlapped with the next tiles' MMAs.  Segment s of this
+ * owner is (src, el) = (s / E_local, s % E_local) (nseg = world * E_local, the
+ * receive layout of permute_peer); its rows land at row
+ * (rank * E_local + el) * cap_pad + r of rank src's plane -- the source's own
+ * expert-major dispatch layout (LAYOUT_FIXED, seg_stride = cap_pad) -- so the
+ * source's combine / router backward then read them locally.  dst_host: HOST
+ * array of the world planes' device base pointers (dst_rows x H bf16 each).
+ * The caller orders ranks with a device barrier before the consumers run. */
+int b200moe_expert_fwd2_peer(const void* h, const void* w2, const int* seg_base, const int* seg_count,
+                             const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
+                             const uint64_t* dst_host, int world, int rank, int cap_pad, int dst_rows,
+                             cudaStream_t stream);
+int b200moe_expert_bwd1_peer(const void* da, const void* db, const void* w1, const void* w3, const int* seg_base,
+                             const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F,
+                             int E_local, const uint64_t* dst_host, int world, int rank, int cap_pad, int dst_rows,
+                             cudaStream_t stream);
 int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int32_t* slot_rank,
                             const int32_t* seg_base, const float* dg, const float* dgates_ext,
                             int64_t dgates_stride_t, int64_t dgates_stride_e, const float* gates, const float* probs,

@@ -59,6 +59,8 @@ SIGNATURES = {
     "b200moe_expert_wgrad_acc": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "b200moe_expert_bwd2_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P],
     "b200moe_expert_bwd2_h": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
+    "b200moe_expert_fwd2_peer": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _I, _P],
+    "b200moe_expert_bwd1_peer": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _I, _P],
     "b200moe_expert_bwd1_ex": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P],
     "b200moe_expert_wgrad_ex": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P],
     "b200moe_dense_fwd": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P],
@@ -125,7 +127,8 @@ KERNELS_PER_CALL = {
     "b200moe_combine": 1, "b200moe_combine_bwd": 1, "b200moe_router_bwd": 1, "b200moe_router_wgrad": 1,
     "b200moe_importance_fwd": 1, "b200moe_importance_bwd": 1, "b200moe_importance_loss": 1, "b200moe_expert_fwd1": 1, "b200moe_expert_fwd2": 1,
     "b200moe_expert_bwd2": 1, "b200moe_expert_bwd1": 1, "b200moe_expert_wgrad": 1, "b200moe_expert_wgrad_acc": 1,
-    "b200moe_expert_bwd1_ex": 1, "b200moe_expert_wgrad_ex": 1, "b200moe_expert_bwd2_ex": 1, "b200moe_expert_bwd2_h": 1,
+    "b200moe_expert_bwd1_ex": 1, "b200moe_expert_wgrad_ex": 1, "b200moe_expert_bwd2_ex": 1, "b200moe_expert_bwd2_h": 1, "b200moe_expert_fwd2_peer": 1,
+    "b200moe_expert_bwd1_peer": 1,
     "b200moe_dense_fwd": 1, "b200moe_dense_dgrad": 1, "b200moe_dense_wgrad": 1,
     "b200moe_upcycle_copy": 3,
     "b200moe_permute_peer": 1, "b200moe_combine_peer": 1, "b200moe_combine_bwd_peer": 1, "b200moe_router_bwd_peer": 1,
@@ -204,7 +207,8 @@ class Profiler:
 # stream: FWD1 -> FWD2 and BWD2 -> WGRAD -> BWD1.
 GEMM_SPANS = (("b200moe_expert_fwd1", "b200moe_expert_bwd2", "b200moe_expert_bwd2_ex", "b200moe_expert_bwd2_h",
                "b200moe_expert_wgrad_ex"),
-              ("b200moe_expert_fwd2", "b200moe_expert_bwd1", "b200moe_expert_bwd1_ex"))
+              ("b200moe_expert_fwd2", "b200moe_expert_bwd1", "b200moe_expert_bwd1_ex", "b200moe_expert_fwd2_peer",
+               "b200moe_expert_bwd1_peer"))
 
 
 PROFILER: Profiler | None = None
@@ -228,6 +232,15 @@ def call(name: str, *args) -> None:
     if rc == ERR_GATE:
         raise GateError(msg)
     raise RuntimeError(f"{name}: {msg} (status {rc})")
+
+
+def host_u64(vals):
+    """(ctypes uint64 array, its address) for a C entry point taking a HOST
+    array of 64-bit values (e.g. per-rank device pointers); keep the array
+    referenced until the call returns."""
+    import ctypes
+    arr = (ctypes.c_uint64 * len(vals))(*vals)
+    return arr, ctypes.addressof(arr)
 
 
 def ptr(t) -> int | None:

@@ -67,9 +67,12 @@ constexpr bool kWideStores = false;  // see Geo::kWide
 constexpr bool kLsuStores = true;    // see emit32
 constexpr int kNumThreads = 64 + 32 * kNumEpiWarps;   // producer, MMA, 8 epilogue warps
 
+constexpr int kMaxPeers = 8;   // expert-parallel ranks an epilogue can push rows to
+
 struct TmaSet {
     CUtensorMap m[5];   // operand loads (SWIZZLE_128B)
     CUtensorMap st[3];  // epilogue stores: 32 x 32 bf16 boxes (SWIZZLE_64B)
+    CUtensorMap stp[kMaxPeers];  // FWD2 / BWD1 with peer output: every rank's receive plane (peer_El > 0)
 };
 
 struct GemmArgs {
@@ -88,6 +91,11 @@ struct GemmArgs {
     int dense;       // BWD1 as a plain dense GEMM: one (A, B) pair, K = F (0 = the two-pair expert BWD1)
     int wgrad_mfast; // WGRAD raster: output-row tiles fastest (dense wgrad with many more column tiles than row
                      // tiles and a long K: concurrent tiles then share the column block of dy in L2)
+    // FWD2 / BWD1 fused with the expert-parallel return exchange (peer_El > 0): segment s = (src, el) =
+    // (s / peer_El, s % peer_El) of this owner rank; its output rows go straight into rank src's receive
+    // plane (tm.stp[src], peer-mapped over NVLink) at row (peer_rank * peer_El + el) * peer_cap + r,
+    // i.e. where the source's own dispatch layout (expert-major, peer_cap rows each) expects them
+    int peer_El, peer_rank, peer_cap;
 };
 
 __host__ __device__ __forceinline__ int wgrad_mask(const GemmArgs& a) { return a.wgrad_subs ? a.wgrad_subs : 7; }
@@ -791,12 +799,20 @@ __device__ __forceinline__ void epilogue_tile(const TmaSet& tm, const GemmArgs& 
             }
         } else {  // kFwd2 / kBwd1: plain bf16 store
             const int col0 = ti.n_tile * kBN;
+            const CUtensorMap* smap = &tm.st[0];
+            int orow = row0;
+            int dbg = a.debug;
+            if (a.peer_El) {   // straight into the source rank's receive plane over NVLink (TMA store)
+                smap = &tm.stp[ti.seg / a.peer_El];
+                orow = (a.peer_rank * a.peer_El + ti.seg % a.peer_El) * a.peer_cap + rel;
+                dbg &= ~8;     // never the local LSU write-back
+            }
             for (int c = half * 128; c < half * 128 + 128; c += 32) {
                 ptx::tmem_ld_32x32b_x32(lane_addr + c, r0);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(r0[i]);
-                emit32<kRing>(ring, &tm.st[0], a.out0, a.H, v0, lane, col0 + c, row0, a.debug);
+                emit32<kRing>(ring, smap, a.out0, a.H, v0, lane, col0 + c, orow, dbg);
             }
         }
     }
@@ -1322,6 +1338,60 @@ int b200moe_expert_fwd2(const void* h, const void* w2, const int* seg_base, cons
     GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local,
                   (__nv_bfloat16*)o_out, nullptr, nullptr, nullptr, nullptr};
     return dispatch_launch<kFwd2>(tm, a, stream);
+}
+
+// Receive-plane store maps of every rank (host array of device base pointers,
+// each plane dst_rows x H bf16) for the peer-output FWD2 / BWD1.
+static int peer_maps(TmaSet& tm, const uint64_t* dst_host, int world, int H, int dst_rows) {
+    B200_CHECK_ARG(world >= 1 && world <= kMaxPeers, B200MOE_ERR_CONFIG, "world %d outside [1, %d]", world, kMaxPeers);
+    for (int r = 0; r < world; ++r) B200_TRY(make_map(&tm.stp[r], (const void*)dst_host[r], H, dst_rows, H, false, true));
+    return B200MOE_OK;
+}
+
+int b200moe_expert_fwd2_peer(const void* h, const void* w2, const int* seg_base, const int* seg_count,
+                             const int* seg_expert, int nseg, int rows, int H, int F, int E_local,
+                             const uint64_t* dst_host, int world, int rank, int cap_pad, int dst_rows,
+                             cudaStream_t stream) {
+    B200_TRY(check_common(nseg, H, F, E_local));
+    B200_CHECK_ARG(nseg == world * E_local && rank >= 0 && rank < world && cap_pad % 128 == 0 &&
+                       (int64_t)world * E_local * cap_pad <= dst_rows, B200MOE_ERR_CONFIG,
+                   "peer FWD2: nseg %d, world %d, E_local %d, rank %d, cap_pad %d, dst_rows %d", nseg, world, E_local,
+                   rank, cap_pad, dst_rows);
+    TmaSet tm = {};
+    B200_TRY(make_map(&tm.m[0], h, F, rows, F, false));
+    B200_TRY(make_map(&tm.m[1], w2, F, (uint64_t)E_local * H, F, false));
+    tm.m[2] = tm.m[3] = tm.m[4] = tm.m[0];
+    B200_TRY(peer_maps(tm, dst_host, world, H, dst_rows));
+    tm.st[0] = tm.st[1] = tm.st[2] = tm.stp[rank];
+    GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.peer_El = E_local;
+    a.peer_rank = rank;
+    a.peer_cap = cap_pad;
+    return dispatch_launch<kFwd2>(tm, a, stream);
+}
+
+int b200moe_expert_bwd1_peer(const void* da, const void* db, const void* w1, const void* w3, const int* seg_base,
+                             const int* seg_count, const int* seg_expert, int nseg, int rows, int H, int F,
+                             int E_local, const uint64_t* dst_host, int world, int rank, int cap_pad, int dst_rows,
+                             cudaStream_t stream) {
+    B200_TRY(check_common(nseg, H, F, E_local));
+    B200_CHECK_ARG(nseg == world * E_local && rank >= 0 && rank < world && cap_pad % 128 == 0 &&
+                       (int64_t)world * E_local * cap_pad <= dst_rows, B200MOE_ERR_CONFIG,
+                   "peer BWD1: nseg %d, world %d, E_local %d, rank %d, cap_pad %d, dst_rows %d", nseg, world, E_local,
+                   rank, cap_pad, dst_rows);
+    TmaSet tm = {};
+    B200_TRY(make_map(&tm.m[0], da, F, rows, F, false));
+    B200_TRY(make_map(&tm.m[1], db, F, rows, F, false));
+    B200_TRY(make_map(&tm.m[2], w1, H, (uint64_t)E_local * F, H, true));
+    B200_TRY(make_map(&tm.m[3], w3, H, (uint64_t)E_local * F, H, true));
+    tm.m[4] = tm.m[0];
+    B200_TRY(peer_maps(tm, dst_host, world, H, dst_rows));
+    tm.st[0] = tm.st[1] = tm.st[2] = tm.stp[rank];
+    GemmArgs a = {seg_base, seg_count, seg_expert, nseg, H, F, E_local, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.peer_El = E_local;
+    a.peer_rank = rank;
+    a.peer_cap = cap_pad;
+    return dispatch_launch<kBwd1>(tm, a, stream);
 }
 
 int b200moe_expert_bwd2(const void* dout, const void* w2, const void* a_pre, const void* b_pre, const int* seg_base,

@@ -333,7 +333,12 @@ class _PeerBuffers:
         self._guards = [(0, G)] + [(o + plane, G) for o in offs] + [(cnt_off + cnt_bytes, G)]
         ptrs = list(self.handle.buffer_ptrs)
         mk = lambda off: torch.tensor([p + off for p in ptrs], dtype=torch.int64, device=device)  # noqa: E731
-        self.peer = [mk(o) for o in offs]   # the two planes' base pointers on every rank
+        self.peer = [mk(o) for o in offs]   # the planes' base pointers on every rank (device arrays)
+        self.peer_host = [[p + o for p in ptrs] for o in offs]   # the same, host lists (GEMM store maps)
+        me = self.raw.data_ptr()
+        # this rank's own plane base repeated per rank: the peer kernels' row addressing with every
+        # "owner" local (consumers of rows the owners' GEMMs pushed here)
+        self.local_rep = [torch.tensor([me + o] * len(ptrs), dtype=torch.int64, device=device) for o in offs]
         self.peer_counts = mk(cnt_off)
 
     def guards_intact(self) -> bool:
@@ -417,8 +422,16 @@ class _EPPeerFunction(torch.autograd.Function):
         Hh = torch.empty(Rs, F, **bf)
         _lib.call("b200moe_expert_fwd1", pb.xr.data_ptr(), W1.data_ptr(), W3.data_ptr(), rbase.data_ptr(),
                   rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, A.data_ptr(), B.data_ptr(), Hh.data_ptr(), s)
-        _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
-                  rexp.data_ptr(), nseg, Rs, H, F, El, pbs.o.data_ptr(), s)
+        push = st.get("gemm_push", True)
+        if push:
+            # FWD2 pushes every output tile straight into its source rank's receive plane
+            # (the shared set's first plane, expert-major: the source's own dispatch layout)
+            arr, dst = _lib.host_u64(pbs.peer_host[0])
+            _lib.call("b200moe_expert_fwd2_peer", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
+                      rexp.data_ptr(), nseg, Rs, H, F, El, dst, plan.world, plan.rank, plan.cap_pad, Rs, s)
+        else:
+            _lib.call("b200moe_expert_fwd2", Hh.data_ptr(), W2.data_ptr(), rbase.data_ptr(), rcounts.data_ptr(),
+                      rexp.data_ptr(), nseg, Rs, H, F, El, pbs.o.data_ptr(), s)
         if st.get("recompute"):
             # selective recompute: a, b, h ([rows, F] x 3, the layer's largest
             # activations) are dropped here and rebuilt by one FWD1 launch at the
@@ -427,13 +440,17 @@ class _EPPeerFunction(torch.autograd.Function):
         elif st.get("drop_h"):
             # keep a, b only: BWD2 rebuilds h = silu(a) * b for WGRAD (b200moe_expert_bwd2_h)
             Hh = None
-        pb.barrier()                            # all expert outputs are ready
+        pb.barrier()                            # all expert outputs are ready (pushed: landed here)
         y = torch.empty(T, H, **bf)
         # the gathered expert rows are kept for the backward (read locally there
         # instead of over NVLink again; O's plane is reused by the next layer)
         og = torch.empty(T * cfg.top_k, H, **bf)
-        _lib.call("b200moe_combine_peer", pbs.peer[0].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
-                  seg_peer.data_ptr(), T, H, E, y.data_ptr(), _lib.ptr(og), cfg.top_k, s)
+        if push:   # this rank's tokens' expert rows are local now, at seg_local[e] + slot
+            _lib.call("b200moe_combine_peer", pbs.local_rep[0].data_ptr(), El, gates.data_ptr(),
+                      slot_rank.data_ptr(), seg_local.data_ptr(), T, H, E, y.data_ptr(), _lib.ptr(og), cfg.top_k, s)
+        else:
+            _lib.call("b200moe_combine_peer", pbs.peer[0].data_ptr(), El, gates.data_ptr(), slot_rank.data_ptr(),
+                      seg_peer.data_ptr(), T, H, E, y.data_ptr(), _lib.ptr(og), cfg.top_k, s)
         ctx.og = og
         st["routing"] = dict(logits=logits, slot_rank=slot_rank, counts=counts, seg_base=seg_peer,
                              gate_mass=gate_mass, importance=imp, importance_loss=imp_loss, stats=stats, err=err,
@@ -444,14 +461,15 @@ class _EPPeerFunction(torch.autograd.Function):
         ctx.generation = pb.generation
         ctx.recompute = A is None
         ctx.rebuild_h = A is not None and Hh is None
+        ctx.push = push
         ctx.save_for_backward(x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer,
-                              A, B, Hh)
+                              A, B, Hh, seg_local)
         return y, gates
 
     @staticmethod
     def backward(ctx, dy, dgates):
         (x, w_g, w_noise, W1, W2, W3, z, gates, probs, noise_act, slot_rank, counts, seg_peer, A, B,
-         Hh) = ctx.saved_tensors
+         Hh, seg_local) = ctx.saved_tensors
         st, pb = ctx.st, ctx.pb
         if pb.generation != ctx.generation:
             # another forward on the same buffer slot overwrote the saved xr / O
@@ -503,8 +521,15 @@ class _EPPeerFunction(torch.autograd.Function):
                   dW1.data_ptr(), dW2.data_ptr(), dW3.data_ptr(), s)
         if acc:
             dW1 = dW2 = dW3 = None
-        _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
-                  rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, pbb.dxp.data_ptr(), s)
+        if ctx.push:   # BWD1 pushes dxp tiles into the source ranks' planes (expert-major, as in the forward)
+            arr, dst = _lib.host_u64(pbb.peer_host[1])
+            _lib.call("b200moe_expert_bwd1_peer", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
+                      rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, dst, plan.world,
+                      plan.rank, plan.cap_pad, Rs, s)
+        else:
+            _lib.call("b200moe_expert_bwd1", dA.data_ptr(), dB.data_ptr(), W1.data_ptr(), W3.data_ptr(),
+                      rbase.data_ptr(), rcounts.data_ptr(), rexp.data_ptr(), nseg, Rs, H, F, El, pbb.dxp.data_ptr(),
+                      s)
         pbb.barrier()                           # all input gradients are ready
         dx = torch.empty(T, H, **bf)
         dh = torch.empty(T, E, **f32)
@@ -514,7 +539,8 @@ class _EPPeerFunction(torch.autograd.Function):
             dgx = dgates.to(torch.float32)
             sx_t, sx_e = dgx.stride()
         ws = torch.empty(2 * H * _ep(E) + T * _ep(E), **f32)
-        _lib.call("b200moe_router_bwd_peer", pbb.peer[1].data_ptr(), El, slot_rank.data_ptr(), seg_peer.data_ptr(),
+        dxp_bufs, dxp_base = (pbb.local_rep[1], seg_local) if ctx.push else (pbb.peer[1], seg_peer)
+        _lib.call("b200moe_router_bwd_peer", dxp_bufs.data_ptr(), El, slot_rank.data_ptr(), dxp_base.data_ptr(),
                   dg.data_ptr(), _lib.ptr(dgx), sx_t, sx_e, gates.data_ptr(), _lib.ptr(probs), w_g.data_ptr(),
                   w_noise.data_ptr(), _lib.ptr(z), _lib.ptr(noise_act), *_swizzled(ctx, H, E, z), T, H, E,
                   cfg.top_k, _lib.ROUTER[cfg.router_type], dx.data_ptr(), dh.data_ptr(), _lib.ptr(dn), ws.data_ptr(), s)
@@ -538,7 +564,7 @@ class ExpertParallelMoE:
     TRANSPORTS = ("p2p", "nccl")
 
     def __init__(self, w_g, w_noise, W1, W2, W3, cfg: GateConfig, group=None, transport: str = "p2p",
-                 buffer_slot: int = 0, recompute: bool = False, drop_h: bool = False):
+                 buffer_slot: int = 0, recompute: bool = False, drop_h: bool = False, gemm_push: bool = True):
         """transport: "p2p" (default) fuses the dispatch/combine exchange into the
         permute/combine kernels over NVLink symmetric memory; "nccl" uses
         all_to_all_single between separate kernels (the comparison baseline).
@@ -561,6 +587,7 @@ class ExpertParallelMoE:
         self.buffer_slot = buffer_slot
         self.recompute = recompute   # p2p: rebuild a, b, h in the backward instead of keeping them
         self.drop_h = drop_h         # p2p: keep a, b only; BWD2 rebuilds h (one third of the memory of a, b, h)
+        self.gemm_push = gemm_push   # p2p: FWD2 / BWD1 push their rows to the sources (else peers pull them)
 
     def _check_tokens(self, T: int, device) -> None:
         """The p2p transport sizes every rank's receive segments from T_local
@@ -592,7 +619,7 @@ class ExpertParallelMoE:
         plan = EPPlan.make(self.world, self.rank, self.cfg.n_experts, T, self.cfg.capacity_factor)
         z = _noise(T, self.cfg.n_experts, x.device, self.cfg.noise_enabled and training, rng, noise)
         st = dict(cfg=self.cfg, plan=plan, group=self.group, reduce_router=reduce_router, buffer_slot=self.buffer_slot,
-                  recompute=self.recompute, drop_h=self.drop_h)
+                  recompute=self.recompute, drop_h=self.drop_h, gemm_push=self.gemm_push)
         fn = _EPPeerFunction if self.transport == "p2p" else _EPFunction
         y, gates = fn.apply(x.to(torch.bfloat16).contiguous(), self.w_g.to(torch.float32).contiguous(),
                             self.w_noise.to(torch.float32).contiguous(), self.W1, self.W2, self.W3, z, st)
@@ -632,7 +659,8 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     wn.requires_grad_()
     gate = P.GateConfig(n_experts=E, top_k=K, router_type=args.router, capacity_factor=args.cf,
                         drop_policy=args.policy)
-    layer = ExpertParallelMoE(wg, wn, W1, W2, W3, gate, transport=args.transport)
+    layer = ExpertParallelMoE(wg, wn, W1, W2, W3, gate, transport=args.transport,
+                              gemm_push=not getattr(args, "ep_pull", False))
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     x = torch.randn(T, H, device=dev, generator=g).to(torch.bfloat16).requires_grad_()
     dy = torch.randn(T, H, device=dev, generator=g).to(torch.bfloat16)
@@ -741,17 +769,21 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     exchange = None
     if args.transport == "p2p" and world > 1:
         remote = s_send * H * 2 * (world - 1) / world
-        per = {"b200moe_permute_peer": remote, "b200moe_combine_peer": remote,
-               # the backward reads the forward's gathered rows locally (og): only the dO stores cross
-               "b200moe_combine_bwd_peer": remote, "b200moe_router_bwd_peer": remote}
-        exchange = {}
+        # permute and combine-backward store rows into the owners' planes; the return
+        # direction rides in FWD2's / BWD1's epilogues (TMA stores into the sources'
+        # planes, inside the GEMM time), so combine and the router backward read locally
+        per = {"b200moe_permute_peer": remote, "b200moe_combine_bwd_peer": remote,
+               "b200moe_combine_peer": 0, "b200moe_router_bwd_peer": 0}
+        exchange = {"return_exchange": "pushed by the FWD2 / BWD1 epilogues over NVLink, overlapped with their MMAs "
+                                      f"({int(remote)} bytes each way per GEMM; inside gemm_ms_per_step)"}
         for name, nbytes in per.items():
             if name in kt:
                 t_ms = kt[name][0] / n_prof
                 exchange[name.replace("b200moe_", "")] = {
                     "ms": round(t_ms, 4), "nvlink_bytes": int(nbytes),
                     "GBps": round(nbytes / (t_ms * 1e-3) / 1e9, 1),
-                    "frac_of_770": round(nbytes / (t_ms * 1e-3) / 1e9 / 770.0, 3)}
+                    "frac_of_770": round(nbytes / (t_ms * 1e-3) / 1e9 / 770.0, 3)} if nbytes else {
+                    "ms": round(t_ms, 4), "nvlink_bytes": 0, "note": "reads rows the owners' GEMMs pushed here"}
     # CPU baseline: the oracle on the R rank-local batches, run
     # one after the other on rank 0's host cores, each a bounded sample of
     # cpu_tokens tokens; tokens/s = R * sample / total time.
@@ -782,6 +814,9 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
                                 "(device barriers) + NCCL all_reduce(dW_g)" if args.transport == "p2p" else
                                 "NCCL all_to_all_single (exact splits) + all_reduce(dW_g)"),
                        "transport": args.transport,
+                       "return_exchange": ("peers pull expert rows in combine / router backward"
+                                           if getattr(args, "ep_pull", False) else
+                                           "pushed from the FWD2 / BWD1 epilogues (TMA stores over NVLink)"),
                        "launch": ("eager (one Python call chain per step)" if eager else
                                   f"CUDA graph of the {args.steps} timed steps per rank, replayed once untimed "
                                   f"before the timed replay"),
