@@ -104,8 +104,18 @@ def recompute_case(rank, world, dev, T=768, H=512, F=512, E=8, k=2):
         ((out.output.float() * dy.float()).sum() + 0.1 * P.importance_penalty(out.gates)).backward()
         torch.cuda.synchronize()
         res.append([out.output, xe.grad] + [t.grad for t in lw if t.grad is not None])
-    ok = len(res[0]) == len(res[1]) and all(torch.equal(a, b) for a, b in zip(*res))
-    print(f"rank {rank}: {'PASS' if ok else 'FAIL'} [p2p recompute] bit-identical to keeping a, b, h", flush=True)
+    # the pull variant of the return exchange (combine / router backward read the owners'
+    # planes instead of rows FWD2 / BWD1 pushed): the same bits
+    lw = [t.clone().requires_grad_() for t in [wg, torch.zeros_like(wg)] + W]
+    ep = ExpertParallelMoE(*lw, cfg, transport="p2p", buffer_slot=44, gemm_push=False)
+    xe = x.clone().requires_grad_()
+    out = ep(xe)
+    ((out.output.float() * dy.float()).sum() + 0.1 * P.importance_penalty(out.gates)).backward()
+    torch.cuda.synchronize()
+    res.append([out.output, xe.grad] + [t.grad for t in lw if t.grad is not None])
+    ok = all(len(r) == len(res[0]) and all(torch.equal(a, b) for a, b in zip(res[0], r)) for r in res[1:])
+    print(f"rank {rank}: {'PASS' if ok else 'FAIL'} [p2p recompute, pull exchange] bit-identical to keeping a, b, h "
+          f"with the GEMM-pushed exchange", flush=True)
     return ok
 
 
