@@ -462,8 +462,15 @@ def run_single(args, dev):
     if not args.eager:
         from paper_2412_09952_b200.graphs import capture
         _lib.PROFILER = prof
-        cap = capture(lambda: step(x, dy), repeat=args.steps, warmup=0)
+        try:
+            cap = capture(lambda: step(x, dy), repeat=args.steps, warmup=0)
+        except Exception as exc:   # noqa: BLE001 -- keep a valid (eager) line rather than none
+            print(f"[bench] CUDA-graph capture failed ({exc!r}); timing the eager loop", file=sys.stderr, flush=True)
+            torch.cuda.synchronize()
+            args.eager = True
+            prof = _lib.Profiler(spans=_lib.GEMM_SPANS)
         _lib.PROFILER = None
+    if cap is not None:
         cap.replay()
         torch.cuda.synchronize()
         warm += args.steps

@@ -710,8 +710,24 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     if not eager:
         from .graphs import capture
         _lib.PROFILER = prof
-        cap = capture(lambda: step(x, dy), repeat=args.steps, warmup=0)
+        err = None
+        try:
+            cap = capture(lambda: step(x, dy), repeat=args.steps, warmup=0)
+        except Exception as exc:   # noqa: BLE001 -- all ranks fall back together (below)
+            err, cap = exc, None
+            torch.cuda.synchronize()
         _lib.PROFILER = None
+        ok = torch.tensor([0 if cap is None else 1], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)     # a graph only if every rank captured one
+        if int(ok) == 0:
+            if err is not None:
+                import sys
+                print(f"[bench] CUDA-graph capture failed ({err!r}); timing the eager loop", file=sys.stderr,
+                      flush=True)
+            cap, eager = None, True
+            args.eager = True
+            prof = _lib.Profiler(spans=_lib.GEMM_SPANS)
+    if cap is not None:
         dist.barrier()
         cap.replay()
         torch.cuda.synchronize()
