@@ -371,9 +371,18 @@ router_wgrad_partial(const __nv_bfloat16* __restrict__ x, const float* __restric
 // 8 consumer warps take 4 rows of each 32-row stage, accumulate 8 hidden x EP
 // experts per lane in registers, and hand the slot back.  One cross-warp
 // reduction per block (through the drained ring), fixed order: deterministic.
-constexpr int kRgTok = 512;
-constexpr int kRgStageRows = 32;
-constexpr int kRgStages = 4;
+#ifndef B200_RG_TOK
+#define B200_RG_TOK 512
+#endif
+#ifndef B200_RG_ROWS
+#define B200_RG_ROWS 32
+#endif
+#ifndef B200_RG_STAGES
+#define B200_RG_STAGES 4
+#endif
+constexpr int kRgTok = B200_RG_TOK;
+constexpr int kRgStageRows = B200_RG_ROWS;
+constexpr int kRgStages = B200_RG_STAGES;
 constexpr int kRgStageBytes = kRgStageRows * 256 * 2;   // 16 KB
 constexpr int kRgConsumers = 8;
 
