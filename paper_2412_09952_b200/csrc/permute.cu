@@ -58,16 +58,21 @@ __device__ __forceinline__ int token_rows(const int32_t* __restrict__ slot_rank,
     return n;
 }
 
-// Zero rows [seg_base[e]+counts[e], seg_base[e]+round_up(counts[e],128)) of buf.
+// Zero rows [seg_base[e]+counts[e], seg_base[e]+round_up(counts[e],128)) of buf
+// (up to 127 rows = 1 MB at H=4096, over NVLink in the expert-parallel
+// kernels): kPadParts blocks per expert, each a slice.  The pad blocks are the
+// grid's FIRST blocks, so they run alongside the token blocks instead of
+// forming a tail of E single blocks after them.
+constexpr int kPadParts = 4;
 __device__ __forceinline__ void zero_pad_rows(__nv_bfloat16* buf, const int32_t* seg_base, const int32_t* counts,
-                                              int e, int H) {
+                                              int e, int part, int H) {
     const int c = counts[e];
     const size_t r0 = (size_t)seg_base[e] + c;
     const size_t r1 = (size_t)seg_base[e] + round_up(c, kSegPad);
     const size_t nvec = (r1 - r0) * (H / 8);
     uint4* p = reinterpret_cast<uint4*>(buf + r0 * H);
     const uint4 zero = make_uint4(0, 0, 0, 0);
-    for (size_t i = threadIdx.x; i < nvec; i += blockDim.x) p[i] = zero;
+    for (size_t i = threadIdx.x + (size_t)part * blockDim.x; i < nvec; i += (size_t)kPadParts * blockDim.x) p[i] = zero;
 }
 
 template <bool kPeer>
@@ -75,17 +80,17 @@ __global__ void __launch_bounds__(kPermThreads)
 permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ slot_rank,
                const int32_t* __restrict__ seg_base, const int32_t* __restrict__ counts, int T, int H, int E,
                int token_blocks, Rows out, const uint64_t* __restrict__ count_bufs, int rank) {
-    if ((int)blockIdx.x >= token_blocks) {
-        const int e = blockIdx.x - token_blocks;
-        zero_pad_rows(out.base<kPeer>(e), seg_base, counts, e, H);
-        if (kPeer && threadIdx.x == 0) {  // publish this rank's count into the owner's receive table
+    if ((int)blockIdx.x < E * kPadParts) {
+        const int e = blockIdx.x / kPadParts, part = blockIdx.x % kPadParts;
+        zero_pad_rows(out.base<kPeer>(e), seg_base, counts, e, part, H);
+        if (kPeer && part == 0 && threadIdx.x == 0) {  // publish this rank's count into the owner's receive table
             const int el = e % out.e_per_rank;
             reinterpret_cast<int32_t*>(count_bufs[e / out.e_per_rank])[rank * out.e_per_rank + el] = counts[e];
         }
         return;
     }
     const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x * (kPermThreads / 32) + (threadIdx.x >> 5);
+    const int t = ((int)blockIdx.x - E * kPadParts) * (kPermThreads / 32) + (threadIdx.x >> 5);
     if (t >= T) return;
     int rows[32], experts[32];
     const int n = token_rows(slot_rank, seg_base, t, E, rows, experts);
@@ -217,13 +222,13 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __
                    const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
                    const int32_t* __restrict__ counts, int T, int H, int E, int token_blocks, Rows dout,
                    float* __restrict__ dg, const __nv_bfloat16* __restrict__ og, int og_k) {
-    if ((int)blockIdx.x >= token_blocks) {
-        const int e = blockIdx.x - token_blocks;
-        zero_pad_rows(dout.base<kPeer>(e), seg_base, counts, e, H);
+    if ((int)blockIdx.x < E * kPadParts) {
+        const int e = blockIdx.x / kPadParts;
+        zero_pad_rows(dout.base<kPeer>(e), seg_base, counts, e, blockIdx.x % kPadParts, H);
         return;
     }
     const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x * (kPermThreads / 32) + (threadIdx.x >> 5);
+    const int t = ((int)blockIdx.x - E * kPadParts) * (kPermThreads / 32) + (threadIdx.x >> 5);
     if (t >= T) return;
     int rows[32], experts[32];
     const int n = token_rows(slot_rank, seg_base, t, E, rows, experts);
@@ -361,7 +366,7 @@ int b200moe_permute(const void* x, const int32_t* slot_rank, const int32_t* seg_
     int rc = check_perm(T, H, E);
     if (rc) return rc;
     const int tb = ceil_div(T, kPermThreads / 32);
-    permute_kernel<false><<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts,
+    permute_kernel<false><<<tb + E * kPadParts, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts,
                                                                 T, H, E, tb, local_rows(xp, E), nullptr, 0);
     B200_CHECK_LAUNCH("permute");
     return B200MOE_OK;
@@ -374,7 +379,7 @@ int b200moe_permute_peer(const void* x, const int32_t* slot_rank, const int32_t*
     if (rc) return rc;
     if ((rc = check_peer(E, e_per_rank))) return rc;
     const int tb = ceil_div(T, kPermThreads / 32);
-    permute_kernel<true><<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts,
+    permute_kernel<true><<<tb + E * kPadParts, kPermThreads, 0, stream>>>((const __nv_bfloat16*)x, slot_rank, seg_base, counts,
                                                                T, H, E, tb, peer_rows(xp_bufs, e_per_rank),
                                                                count_bufs, rank);
     B200_CHECK_LAUNCH("permute_peer");
@@ -412,7 +417,7 @@ int b200moe_combine_bwd(const void* dy, const void* o, const float* gates, const
     int rc = check_perm(T, H, E);
     if (rc) return rc;
     const int tb = ceil_div(T, kPermThreads / 32);
-    combine_bwd_kernel<false><<<tb + E, kPermThreads, 0, stream>>>((const __nv_bfloat16*)dy, local_rows((void*)o, E),
+    combine_bwd_kernel<false><<<tb + E * kPadParts, kPermThreads, 0, stream>>>((const __nv_bfloat16*)dy, local_rows((void*)o, E),
                                                                     gates, slot_rank, seg_base, counts, T, H, E, tb,
                                                                     local_rows(dout, E), dg, nullptr, 0);
     B200_CHECK_LAUNCH("combine_bwd");
@@ -427,7 +432,7 @@ int b200moe_combine_bwd_peer(const void* dy, const uint64_t* o_bufs, const float
     if ((rc = check_peer(E, e_per_rank))) return rc;
     B200_CHECK_ARG(og == nullptr || (og_k >= 1 && og_k <= E), B200MOE_ERR_CONFIG, "og_k %d outside [1, %d]", og_k, E);
     const int tb = ceil_div(T, kPermThreads / 32);
-    combine_bwd_kernel<true><<<tb + E, kPermThreads, 0, stream>>>(
+    combine_bwd_kernel<true><<<tb + E * kPadParts, kPermThreads, 0, stream>>>(
         (const __nv_bfloat16*)dy, peer_rows(o_bufs, e_per_rank), gates, slot_rank, seg_base, counts, T, H, E, tb,
         peer_rows(dout_bufs, e_per_rank), dg, (const __nv_bfloat16*)og, og_k);
     B200_CHECK_LAUNCH("combine_bwd_peer");
