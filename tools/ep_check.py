@@ -151,6 +151,55 @@ def drop_h_case(rank, world, dev, T=768, H=512, F=512, E=8, k=2):
     return ok
 
 
+def graph_case(rank, world, dev, T=768, H=512, F=512, E=8, k=2):
+    """The p2p EP layer step recorded into a CUDA graph (graphs.capture: device
+    barriers, peer kernels, the GEMM-pushed exchange and the dW_g all_reduce
+    are all stream work) replays the eager step's bits, also on new data
+    copied into the captured inputs."""
+    from paper_2412_09952_b200.graphs import capture
+    El = E // world
+    g = torch.Generator(device=dev).manual_seed(9)
+    W = [(torch.randn(s_, generator=g, device=dev) * 0.05).to(torch.bfloat16).requires_grad_()
+         for s_ in ((El, F, H), (El, H, F), (El, F, H))]
+    wg = (torch.randn(H, E, generator=g, device=dev) * 0.05).requires_grad_()
+    wn = torch.zeros(H, E, device=dev, requires_grad=True)
+    gx = torch.Generator(device=dev).manual_seed(500 + rank)
+    x = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16).requires_grad_()
+    dy = torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16)
+    cfg = P.GateConfig(n_experts=E, top_k=k, capacity_factor=1.0)
+    ep = ExpertParallelMoE(wg, wn, *W, cfg, transport="p2p", buffer_slot=46)
+    params = [wg, wn, x] + W
+    lam = torch.tensor(0.1, device=dev)
+
+    def step():
+        for p in params:
+            p.grad = None
+        out = ep(x)
+        torch.autograd.backward([out.output, P.importance_penalty(out.gates)], [dy, lam])
+        return out
+
+    def snap(out):
+        return [out.output.detach().clone()] + [p.grad.clone() for p in params if p.grad is not None]
+
+    ref = snap(step())
+    cap = capture(step, warmup=1)
+    ok = True
+    for _ in range(2):
+        cap.replay()
+        torch.cuda.synchronize()
+        got = snap(cap.outputs)
+        ok &= len(got) == len(ref) and all(torch.equal(a, b) for a, b in zip(got, ref))
+    with torch.no_grad():
+        x.copy_(torch.randn(T, H, generator=gx, device=dev).to(torch.bfloat16))
+    cap.replay()
+    torch.cuda.synchronize()
+    got = snap(cap.outputs)
+    want = snap(step())
+    ok &= all(torch.equal(a, b) for a, b in zip(got, want))
+    print(f"rank {rank}: {'PASS' if ok else 'FAIL'} [p2p graph] captured EP step replays the eager bits", flush=True)
+    return ok
+
+
 def oracle_case(rank, world, dev, T, H, F, router, policy, cf, noise, transport, E=8, k=2, lam=0.1):
     """EP layer against the CPU ORACLE (oracle/moe_oracle.py, the reference's
     closed form, moefold/moe.py:250-283) on each rank's own batch: routing
@@ -243,6 +292,7 @@ def main():
         ok &= oracle_case(rank, world, dev, 384, 256, 256, "st", "score", None, False, transport)
     ok &= recompute_case(rank, world, dev)
     ok &= drop_h_case(rank, world, dev)
+    ok &= graph_case(rank, world, dev)
     # canary bands around every symmetric receive plane (written by peers over NVLink) untouched
     from paper_2412_09952_b200.ep import _PeerBuffers
     torch.cuda.synchronize()
