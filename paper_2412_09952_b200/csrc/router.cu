@@ -308,16 +308,20 @@ router_fwd_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__
 // stage), one thread issues 4 MMAs (K = 16) per stage, and the 128 threads of
 // the epilogue each own one token (TMEM lane).  The CUDA-core K1 above stays
 // for E > 16 (N would exceed the TMEM budget of this layout).
-template <int EP, bool kNoise>
+template <int EP, bool kNoise, int CS = 2>
 struct RtcCfg {
     static constexpr int NB = ((3 * EP + 15) / 16) * 16;   // B rows per matrix (3 splits, padded)
     static constexpr int N = kNoise ? 2 * NB : NB;
-    static constexpr int kStages = 8;
+    // cluster of CS CTAs per 128-token tile, CTA r streaming the r-th hidden
+    // slice; with 4 the ring is halved so two CTAs share an SM (256 CTAs on 148
+    // SMs at T = 8192 instead of 128), and must still hold the 3 peers' partials
+    static constexpr int kStages = CS == 2 ? 8 : 4;
     static constexpr int kABytes = 128 * 64 * 2;         // 16 KB of x per stage
     static constexpr int kBBytes = N * 64 * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static_assert((CS - 1) * N * 128 * 4 <= kStages * kStageBytes, "the drained ring holds the peers' partials");
 };
 
 // W_g / W_noise [H, E] fp32 -> the bf16 split table B [N, H] (row s*EP + e of
@@ -357,13 +361,13 @@ __global__ void router_wsplit_kernel(const float* __restrict__ w_g, const float*
     }
 }
 
-template <int EP, bool kNoise>
+template <int EP, bool kNoise, int CS>
 __global__ void __launch_bounds__(128, 1)
 router_fwd_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
                      const float* __restrict__ z, int T, int H, int E, int k, int router_type,
                      float* __restrict__ logits, float* __restrict__ gates, float* __restrict__ probs,
                      float* __restrict__ noise_act, int32_t* __restrict__ err_flag) {
-    using C = RtcCfg<EP, kNoise>;
+    using C = RtcCfg<EP, kNoise, CS>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
@@ -371,14 +375,15 @@ router_fwd_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
     uint64_t* done = empty + C::kStages;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // a cluster of two CTAs shares one 128-token tile: CTA r accumulates the
-    // hidden half r (twice the SMs streaming x), then CTA 1 hands its partial
-    // sums to CTA 0 through distributed shared memory
+    // a cluster of CS CTAs shares one 128-token tile: CTA r accumulates the
+    // hidden slice r (CS times the SMs streaming x), then CTAs 1..CS-1 hand
+    // their partial sums to CTA 0 through distributed shared memory
     const uint32_t crank = ptx::cluster_ctarank();
     const int t0 = (int)ptx::cluster_id_x() * 128;
     const int nkb_all = H / 64;
-    const int kb0 = (int)crank * (nkb_all / 2);
-    const int nkb = crank ? nkb_all - nkb_all / 2 : nkb_all / 2;
+    const int per = nkb_all / CS;
+    const int kb0 = (int)crank * per;
+    const int nkb = (int)crank == CS - 1 ? nkb_all - per * (CS - 1) : per;
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&xmap);
         ptx::prefetch_tmap(&bmap);
@@ -429,21 +434,23 @@ router_fwd_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
 #pragma unroll
     for (int c = 0; c < kLoads; ++c) ptx::tmem_ld_32x32b_x32(lane_addr + c * 32, d + c * 32);
     ptx::tmem_ld_wait();
-    // cross-CTA reduction over the two hidden halves: both rings are drained
-    // (barrier 1), CTA 1 stores its partials into CTA 0's ring memory
-    // ([column][row] floats, conflict-free), barrier 2, CTA 0 adds them
+    // cross-CTA reduction over the hidden slices: every ring is drained
+    // (barrier 1), CTA r > 0 stores its partials into CTA 0's ring memory
+    // (block r - 1, [column][row] floats, conflict-free), barrier 2, CTA 0
+    // adds them in rank order
     float* red = reinterpret_cast<float*>(smem);
     ptx::cluster_sync();
-    if (crank == 1) {
+    if (crank != 0) {
         uint32_t remote;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(ptx::smem_u32(red)));
+        remote += (crank - 1) * (uint32_t)(C::N * 128 * 4);
 #pragma unroll
         for (int c = 0; c < C::N; ++c)
             asm volatile("st.shared::cluster.f32 [%0], %1;" :: "r"(remote + (uint32_t)(c * 128 + threadIdx.x) * 4u),
                          "f"(__uint_as_float(d[c])) : "memory");
     }
     ptx::cluster_sync();
-    if (crank == 1) {
+    if (crank != 0) {
         ptx::tc_fence_before();
         __syncthreads();
         if (warp == 1) {
@@ -453,7 +460,10 @@ router_fwd_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
         return;
     }
 #pragma unroll
-    for (int c = 0; c < C::N; ++c) d[c] = __float_as_uint(__uint_as_float(d[c]) + red[c * 128 + threadIdx.x]);
+    for (int r = 0; r < CS - 1; ++r)
+#pragma unroll
+        for (int c = 0; c < C::N; ++c)
+            d[c] = __float_as_uint(__uint_as_float(d[c]) + red[(r * C::N + c) * 128 + threadIdx.x]);
     const int t = t0 + threadIdx.x;
     float row[EP];
 #pragma unroll
@@ -986,6 +996,41 @@ namespace {
 // Diagnostics (A/B against the CUDA-core K1): thread-local, product default off.
 thread_local int g_router_fma = 0;
 
+#ifndef B200_RTC_CS4
+#define B200_RTC_CS4 1
+#endif
+template <int EP, bool kNoise, int CS>
+int router_fwd_tc_launch(const CUtensorMap& xmap, const CUtensorMap& bmap, const float* z, int T, int H, int E, int k,
+                         int router_type, float* logits, float* gates, float* probs, float* noise_act,
+                         int32_t* err_flag, cudaStream_t stream) {
+    using C = RtcCfg<EP, kNoise, CS>;
+    auto kern = router_fwd_tc_kernel<EP, kNoise, CS>;
+    static std::atomic<uint64_t> attr{0};
+    if (cudaError_t ae = ensure_smem_attr(kern, C::kSmem, attr); ae != cudaSuccess) {
+        set_error("router_fwd_tc smem attribute: %s", cudaGetErrorString(ae));
+        return B200MOE_ERR_CUDA;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS * ceil_div(T, 128));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = CS;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, xmap, bmap, z, T, H, E, k, router_type, logits, gates, probs,
+                                        noise_act, err_flag);
+    if (le != cudaSuccess) {
+        set_error("router_fwd_tc launch: %s", cudaGetErrorString(le));
+        return B200MOE_ERR_CUDA;
+    }
+    return B200MOE_OK;
+}
+
 template <int EP, bool kNoise>
 int router_fwd_tc(const void* x, const float* w_g, const float* w_noise, const float* z, int T, int H, int E, int k,
                   int router_type, float* logits, float* gates, float* probs, float* noise_act, float* workspace,
@@ -1000,31 +1045,14 @@ int router_fwd_tc(const void* x, const float* w_g, const float* w_noise, const f
     if (rc) return rc;
     rc = make_tmap_bf16_2d(&bmap, bsplit, (uint64_t)H, (uint64_t)C::N, (uint64_t)H, 64, C::N, true);
     if (rc) return rc;
-    auto kern = router_fwd_tc_kernel<EP, kNoise>;
-    static std::atomic<uint64_t> attr{0};
-    if (cudaError_t ae = ensure_smem_attr(kern, C::kSmem, attr); ae != cudaSuccess) {
-        set_error("router_fwd_tc smem attribute: %s", cudaGetErrorString(ae));
-        return B200MOE_ERR_CUDA;
+    // four hidden slices per tile (no noise: the peers' partials fit the halved ring)
+    if constexpr (!kNoise && B200_RTC_CS4) {
+        if (H % 256 == 0)
+            return router_fwd_tc_launch<EP, kNoise, 4>(xmap, bmap, z, T, H, E, k, router_type, logits, gates, probs,
+                                                       noise_act, err_flag, stream);
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * ceil_div(T, 128));
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = C::kSmem;
-    cfg.stream = stream;
-    cudaLaunchAttribute la[1];
-    la[0].id = cudaLaunchAttributeClusterDimension;
-    la[0].val.clusterDim.x = 2;
-    la[0].val.clusterDim.y = 1;
-    la[0].val.clusterDim.z = 1;
-    cfg.attrs = la;
-    cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, xmap, bmap, z, T, H, E, k, router_type, logits, gates, probs,
-                                        noise_act, err_flag);
-    if (le != cudaSuccess) {
-        set_error("router_fwd_tc launch: %s", cudaGetErrorString(le));
-        return B200MOE_ERR_CUDA;
-    }
-    return B200MOE_OK;
+    return router_fwd_tc_launch<EP, kNoise, 2>(xmap, bmap, z, T, H, E, k, router_type, logits, gates, probs,
+                                               noise_act, err_flag, stream);
 }
 
 template <int EP>
