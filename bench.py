@@ -60,12 +60,12 @@ def parse():
     return p.parse_args()
 
 
-def cpu_sample(tokens: int, cf: float, router: str, policy: str, reps: int):
+def cpu_sample(tokens: int, cf: float, router: str, policy: str, reps: int, threads: int | None = None):
     """Oracle (numpy port of moefold) fwd+bwd at the Llama shape on `tokens` tokens."""
     import numpy as np  # noqa: F401
     from threadpoolctl import threadpool_info, threadpool_limits
     from oracle import moe_oracle as O
-    cores = len(os.sched_getaffinity(0))
+    cores = threads or len(os.sched_getaffinity(0))
     # every host core, also under torchrun (which exports OMP_NUM_THREADS=1)
     with threadpool_limits(limits=cores, user_api="blas"):
         used = max([p["num_threads"] for p in threadpool_info() if p["user_api"] == "blas"] or [1])

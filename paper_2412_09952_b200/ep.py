@@ -28,6 +28,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -804,13 +806,18 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     # one after the other on rank 0's host cores, each a bounded sample of
     # cpu_tokens tokens; tokens/s = R * sample / total time.
     cpu = None
+    # the other ranks wait on a gloo barrier (a blocking socket read) instead of
+    # spinning in an NCCL barrier on host cores rank 0's BLAS threads need, and
+    # rank 0 leaves one core per other rank
+    cpu_group = dist.new_group(backend="gloo")
     if not getattr(args, "no_cpu_baseline", False) and rank == 0:
-        times, cores = B.cpu_sample(args.cpu_tokens, args.cf, args.router, args.policy, world)
+        spare = max(1, len(os.sched_getaffinity(0)) - (world - 1))
+        times, cores = B.cpu_sample(args.cpu_tokens, args.cf, args.router, args.policy, world, threads=spare)
         cpu = {"value": round(world * args.cpu_tokens / sum(times), 3), "unit": "tokens/s", "cores": cores,
                "kind": "port",
                "sample": f"{world} rank-local batches of {args.cpu_tokens} tokens, fwd+bwd at the Llama-3 shape run "
                          f"sequentially, numpy/OpenBLAS fp32 on {cores} threads, {B.cpu_model()}"}
-    dist.barrier()
+    dist.barrier(group=cpu_group)
     if rank == 0:
         tps = world * T / (ms_max * 1e-3)
         flops = 18.0 * H * F * S_tot + 6.0 * world * T * H * E
