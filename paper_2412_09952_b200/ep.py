@@ -2,10 +2,13 @@
 rank (reference ownership rule moefold/upcycle.py:207-208, byte
 model moefold/plan.py:246-247).  Two transports:
 
-* "p2p" (default, `_EPPeerFunction`): the dispatch / combine exchange is fused
-  into the permute / combine kernels, which write and read the expert owners'
-  receive buffers directly over NVLink (torch symmetric memory, device
-  barriers).  Counts never leave the device; no host synchronisation.
+* "p2p" (default, `_EPPeerFunction`): the exchange is fused into the kernels
+  over NVLink peer memory (torch symmetric memory, device barriers): the
+  permute and combine-backward kernels store rows straight into the expert
+  owners' planes, and the owners' FWD2 / BWD1 epilogues TMA-store their
+  output tiles straight into the source ranks' planes, so combine and the
+  router backward read locally.  Counts never leave the device; no host
+  synchronisation.
 * "nccl" (`_EPFunction`, the comparison baseline): separate kernels around
   NCCL all_to_all_single with exact splits (one host round trip for the
   counts), per rank r (T_local tokens, rank-local capacity, so routing equals
@@ -474,7 +477,7 @@ class _EPPeerFunction(torch.autograd.Function):
          Hh, seg_local) = ctx.saved_tensors
         st, pb = ctx.st, ctx.pb
         if pb.generation != ctx.generation:
-            # another forward on the same buffer slot overwrote the saved xr / O
+            # another forward on the same buffer slot overwrote the saved xr
             raise RuntimeError(f"EP symmetric buffer slot {st.get('buffer_slot', 0)} was refilled by a later forward "
                                f"before this backward; give layers that are alive in one graph distinct buffer_slot "
                                f"values")
@@ -572,7 +575,7 @@ class ExpertParallelMoE:
         all_to_all_single between separate kernels (the comparison baseline).
         buffer_slot: which symmetric receive buffers the p2p transport uses;
         layers whose forwards are alive in the same autograd graph need
-        distinct slots (a slot's xr / O are saved for its backward)."""
+        distinct slots (a slot's xr is saved for its backward)."""
         if transport not in self.TRANSPORTS:
             raise ConfigError(f"transport must be one of {self.TRANSPORTS}, got {transport!r}")
         self.transport = transport
