@@ -22,6 +22,9 @@
 namespace b200moe {
 
 constexpr int kPermThreads = 256;  // 8 warps
+#ifndef B200_COMBINE_MINB
+#define B200_COMBINE_MINB 1   // min resident blocks per SM for combine / combine-backward (A/B knob)
+#endif
 constexpr int kVecPerLane = 8;     // uint4 per lane per pass (4 KB per warp pass)
 
 struct Rows {
@@ -119,7 +122,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
 // j-th kept row (ascending expert), written while they pass through registers
 // so that the backward reads them locally instead of over NVLink again.
 template <bool kPeer>
-__global__ void __launch_bounds__(kPermThreads)
+__global__ void __launch_bounds__(kPermThreads, B200_COMBINE_MINB)
 combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restrict__ slot_rank,
                const int32_t* __restrict__ seg_base, int T, int H, int E, __nv_bfloat16* __restrict__ y,
                __nv_bfloat16* __restrict__ og, int og_k) {
@@ -217,7 +220,7 @@ combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restric
 // og (optional): the forward's gathered rows (combine_kernel): read locally
 // instead of from the owners' buffers.
 template <bool kPeer>
-__global__ void __launch_bounds__(kPermThreads)
+__global__ void __launch_bounds__(kPermThreads, B200_COMBINE_MINB)
 combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __restrict__ gates,
                    const int32_t* __restrict__ slot_rank, const int32_t* __restrict__ seg_base,
                    const int32_t* __restrict__ counts, int T, int H, int E, int token_blocks, Rows dout,
