@@ -98,24 +98,35 @@ def _smi_id(index: int) -> str:
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 20 ms in the
     background; only samples whose timestamp falls inside the timed region
-    (the `with` block) are summarised.  Started at construction so that the
-    process is up before the timed region begins."""
+    (the `with` block) are summarised.  Started at construction -- before the
+    warm-up, so that the GPU goes from the warm-up straight into the timed
+    region -- with a reader thread draining the pipe (a long warm-up would
+    otherwise fill it and stall the sampler)."""
 
     def __init__(self, index: int):
+        import threading
         self.index = index
         self.smi_id = _smi_id(index)
         self.proc = None
         self.t0 = self.t1 = None
         self.lines = []
+        self._reader = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", self.smi_id,
                  "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
+            self._reader = threading.Thread(target=self._drain, daemon=True)
+            self._reader.start()
             time.sleep(1.0)
         except OSError:
             self.proc = None
+
+    def _drain(self):
+        for ln in self.proc.stdout:
+            if ln.strip():
+                self.lines.append(ln)
 
     def __enter__(self):
         self.t0 = time.time()
@@ -127,11 +138,11 @@ class ClockSampler:
         if self.proc is not None:
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            if self._reader is not None:
+                self._reader.join(timeout=5)
 
     def summary(self):
         import datetime
@@ -475,6 +486,10 @@ def run_single(args, dev):
         return out, aux
 
     # warmup
+    # the clock sampler's process starts (and settles) before the warm-up, so
+    # the GPU goes from the warm-up straight into the timed region, without an
+    # idle second that would let the clock recover from the power cap
+    clk = ClockSampler(dev.index)
     warm = warmup(args, lambda: step(x, dy))
     # (the step's outputs die with this statement: no autograd graph of an eager
     # step may outlive it into a capture -- graphs.py)
@@ -512,7 +527,7 @@ def run_single(args, dev):
         _lib.PROFILER = prof
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
+    with clk:
         torch.cuda.synchronize()
         s0.record()
         h0 = time.perf_counter()

@@ -698,6 +698,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return int(t)
 
+    clk = B.ClockSampler(dev.index)   # started before the warm-up (see bench.run_single)
     warm = B.warmup(args, lambda: step(x, dy), agree)
     out = step(x, dy)[0]
     warm += 1
@@ -740,7 +741,7 @@ def run_ep_bench(args, rank: int, world: int, dev, measured: dict):
     else:
         _lib.PROFILER = prof
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with B.ClockSampler(dev.index) as clk:
+    with clk:
         dist.barrier()
         torch.cuda.synchronize()
         e0.record()

@@ -204,6 +204,8 @@ def main():
             ev[3].record()
         return loss, stats
 
+    from bench import ClockSampler
+    clk = ClockSampler(dev.index)   # started before the warm-up (see bench.run_single)
     for _ in range(a.warmup):
         loss, stats = step()
     torch.cuda.synchronize()
@@ -211,8 +213,7 @@ def main():
     if world > 1:
         dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
-    from bench import ClockSampler
-    with ClockSampler(dev.index) as clk:
+    with clk:
         t0 = time.perf_counter()
         for i in range(a.steps):
             loss, _ = step(evs[i])
