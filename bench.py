@@ -57,6 +57,7 @@ def parse():
                    help="EP exchange: fused NVLink peer-memory kernels (default) or NCCL all-to-all")
     p.add_argument("--gemm-debug", type=int, default=0, help=argparse.SUPPRESS)  # A/B experiment switches
     p.add_argument("--ep-pull", action="store_true", help=argparse.SUPPRESS)   # EP: peers pull expert rows (A/B)
+    p.add_argument("--idle-before", type=float, default=0.0, help=argparse.SUPPRESS)  # A/B: idle seconds before timing
     return p.parse_args()
 
 
@@ -527,6 +528,9 @@ def run_single(args, dev):
         _lib.PROFILER = prof
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
+    if args.idle_before:
+        torch.cuda.synchronize()
+        time.sleep(args.idle_before)
     with clk:
         torch.cuda.synchronize()
         s0.record()
