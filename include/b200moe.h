@@ -210,9 +210,10 @@ int b200moe_router_bwd_peer(const uint64_t* dxp_bufs, int e_per_rank, const int3
 
 /* Router weight gradients: dW_g = x^T.dh, dW_noise = x^T.dn (fp32, [H,E]),
  * deterministic (fixed-order partial sums).  workspace: >= ceil(T/64)*H*E
- * floats.  tickets (nullable): ceil(H/256) int32, zeroed once and left zeroed
+ * floats.  tickets (nullable): ceil(H/128) int32, zeroed once and left zeroed
  * -- with it (E <= 8) the last block of each hidden block finishes the
- * reduction in the same launch; without it a second kernel does. */
+ * reduction in the same launch (on tcgen05 when H % 128 == 0: x read once
+ * for both matrices); without it a second kernel does. */
 int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T, int H, int E, float* dw_g,
                          float* dw_noise, float* workspace, int32_t* tickets, cudaStream_t stream);
 

@@ -531,6 +531,188 @@ router_wgrad_ring(const __grid_constant__ CUtensorMap xmap, const float* __restr
     if (threadIdx.x == 0) tickets[blockIdx.x] = 0;
 }
 
+// Router weight gradients on tcgen05 (E <= 8): dW[h, e] = sum_t x[t, h] dh[t, e]
+// (and dW_noise from dn) as one MN-major GEMM per CTA: M = 128 hidden units
+// (TMEM lanes), N = 64 split columns, K = a chunk of kRwTok tokens.  The fp32
+// dh / dn are split into three bf16 parts hi + mid + lo (each the bf16
+// rounding of the remainder, together within 2^-24 of the value) written by
+// the producer warp straight into the swizzled B tile -- columns [0, 24) dh,
+// [32, 56) dn, the rest zero -- while x arrives by TMA (two 64-hidden boxes
+// per 64-token stage); x is bf16, so every product is exact and the MMA
+// accumulates in fp32.  The epilogue adds the parts smallest first; per-chunk
+// partials are summed in chunk order by the last CTA of each hidden block
+// (tickets), so the result is deterministic.  x is read once for both
+// matrices.
+#ifndef B200_RW_TOK
+#define B200_RW_TOK 1024
+#endif
+#ifndef B200_RW_STAGES
+#define B200_RW_STAGES 3
+#endif
+constexpr int kRwTok = B200_RW_TOK;
+constexpr int kRwStages = B200_RW_STAGES;
+constexpr int kRwABytes = 2 * 64 * 64 * 2;   // two 64-hidden x 64-token boxes (SWIZZLE_128B)
+constexpr int kRwBBytes = 64 * 64 * 2;       // 64 tokens x 64 split columns
+constexpr int kRwStageBytes = kRwABytes + kRwBBytes;
+constexpr int kRwSmem = kRwStages * kRwStageBytes + 1024 + 256;
+
+__device__ __forceinline__ void rw_split3(float v, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(v);
+    const float r1 = v - __bfloat162float(hi);
+    mid = __float2bfloat16_rn(r1);
+    lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+
+// element (row k, column n) of a [64 x 64] bf16 SWIZZLE_128B tile
+__device__ __forceinline__ int sw128_off(int k, int n) {
+    return k * 128 + ((((n * 2) >> 4) ^ (k & 7)) << 4) + ((n * 2) & 15);
+}
+
+template <bool kNoise>
+__global__ void __launch_bounds__(128, 1)
+router_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ dh,
+                       const float* __restrict__ dn, int T, int H, int E, float* __restrict__ part,
+                       float* __restrict__ out_g, float* __restrict__ out_n, int32_t* __restrict__ tickets) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRwStages * kRwStageBytes);
+    uint64_t* empty = full + kRwStages;
+    uint64_t* done = empty + kRwStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    __shared__ bool last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h0 = blockIdx.x * 128;
+    const int chunk = blockIdx.y;
+    const int t0 = chunk * kRwTok;
+    const int ntok = min(kRwTok, T - t0);
+    const int nkb = (ntok + 63) / 64;
+    // zero every stage's B tile once: the producer rewrites only the split columns
+    for (int i = threadIdx.x; i < kRwStages * kRwBBytes / 16; i += blockDim.x) {
+        const int st = i / (kRwBBytes / 16), j = i % (kRwBBytes / 16);
+        reinterpret_cast<uint4*>(smem + st * kRwStageBytes + kRwABytes)[j] = make_uint4(0, 0, 0, 0);
+    }
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&xmap);
+        for (int s = 0; s < kRwStages; ++s) {
+            ptx::mbar_init(&full[s], 2);     // the x TMA (with its bytes) + the split-B writers
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_mbar_init();
+    }
+    ptx::fence_proxy_async();   // the zeroed tiles, before the MMAs read them
+    if (warp == 1) ptx::tmem_alloc<1>(tslot, 64);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {                        // x producer: two TMA boxes per stage
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int st = kb % kRwStages;
+                if (kb >= kRwStages) ptx::mbar_wait(&empty[st], ((kb / kRwStages) - 1) & 1);
+                uint8_t* a = smem + st * kRwStageBytes;
+                ptx::mbar_arrive_expect_tx(&full[st], kRwABytes);   // tokens beyond T arrive as zeros
+                ptx::tma_load_2d(&xmap, &full[st], a, h0, t0 + kb * 64);
+                ptx::tma_load_2d(&xmap, &full[st], a + kRwABytes / 2, h0 + 64, t0 + kb * 64);
+            }
+        }
+    } else if (warp >= 2) {                 // split-B producers: one token row per thread (64 threads)
+        const int tt = threadIdx.x - 64;
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % kRwStages;
+            if (kb >= kRwStages) ptx::mbar_wait(&empty[st], ((kb / kRwStages) - 1) & 1);
+            uint8_t* b = smem + st * kRwStageBytes + kRwABytes;
+            const int t = t0 + kb * 64 + tt;
+            const bool ok = tt < ntok - kb * 64;
+            float g[8], q[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                g[e] = (ok && e < E) ? dh[(size_t)t * E + e] : 0.f;
+                if constexpr (kNoise) q[e] = (ok && e < E) ? dn[(size_t)t * E + e] : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                __nv_bfloat16 hi, mid, lo;
+                rw_split3(g[e], hi, mid, lo);
+                *reinterpret_cast<__nv_bfloat16*>(b + sw128_off(tt, e)) = hi;
+                *reinterpret_cast<__nv_bfloat16*>(b + sw128_off(tt, 8 + e)) = mid;
+                *reinterpret_cast<__nv_bfloat16*>(b + sw128_off(tt, 16 + e)) = lo;
+                if constexpr (kNoise) {
+                    rw_split3(q[e], hi, mid, lo);
+                    *reinterpret_cast<__nv_bfloat16*>(b + sw128_off(tt, 32 + e)) = hi;
+                    *reinterpret_cast<__nv_bfloat16*>(b + sw128_off(tt, 40 + e)) = mid;
+                    *reinterpret_cast<__nv_bfloat16*>(b + sw128_off(tt, 48 + e)) = lo;
+                }
+            }
+            ptx::fence_proxy_async();
+            asm volatile("bar.sync 1, 64;" ::: "memory");    // all 64 rows of the tile written
+            if (tt == 0) ptx::mbar_arrive(&full[st]);
+        }
+    } else if (warp == 1 && lane == 0) {    // MMA issuer
+        constexpr uint32_t idesc = ptx::make_idesc_bf16(128, 64, true, true);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % kRwStages;
+            ptx::mbar_wait(&full[st], (kb / kRwStages) & 1);
+            ptx::tc_fence_after();
+            const uint32_t a = ptx::smem_u32(smem + st * kRwStageBytes);
+            const uint32_t b = a + kRwABytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                ptx::mma_bf16<1>(tmem, ptx::make_sdesc(a + kk * 2048, 8192, 1024),
+                                 ptx::make_sdesc(b + kk * 2048, 8192, 1024), idesc, (kb | kk) != 0);
+            ptx::mma_commit<1>(&empty[st], 1);
+        }
+        ptx::mma_commit<1>(done, 1);
+    }
+    // ---- epilogue: thread i owns hidden unit h0 + i (TMEM lane i)
+    ptx::mbar_wait(done, 0);
+    ptx::tc_fence_after();
+    uint32_t d[64];
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    ptx::tmem_ld_32x32b_x32(lane_addr, d);
+    if constexpr (kNoise) ptx::tmem_ld_32x32b_x32(lane_addr + 32, d + 32);
+    ptx::tmem_ld_wait();
+    const int h = h0 + threadIdx.x;
+    float* pg = part + (size_t)chunk * (kNoise ? 2 : 1) * H * E;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        if (e < E && h < H) {
+            pg[(size_t)h * E + e] = (__uint_as_float(d[16 + e]) + __uint_as_float(d[8 + e])) + __uint_as_float(d[e]);
+            if constexpr (kNoise)
+                pg[(size_t)H * E + (size_t)h * E + e] =
+                    (__uint_as_float(d[48 + e]) + __uint_as_float(d[40 + e])) + __uint_as_float(d[32 + e]);
+        }
+    }
+    ptx::tc_fence_before();
+    __threadfence();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<1>(tmem, 64);
+    }
+    if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1) == (int)gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // the last chunk CTA of this hidden block: chunk-ordered sums of the partials
+    const int nch = gridDim.y;
+    const size_t stride = (size_t)(kNoise ? 2 : 1) * H * E;
+    for (int m = 0; m < (kNoise ? 2 : 1); ++m) {
+        float* out = m == 0 ? out_g : out_n;
+        for (int i = threadIdx.x; i < 128 * E; i += blockDim.x) {
+            const int hh = h0 + i / E, e = i % E;
+            if (hh >= H) continue;
+            const size_t o = (size_t)m * H * E + (size_t)hh * E + e;
+            float sum = 0.f;
+            for (int c = 0; c < nch; ++c) sum += __ldcg(part + (size_t)c * stride + o);
+            out[(size_t)hh * E + e] = sum;
+        }
+    }
+    if (threadIdx.x == 0) tickets[blockIdx.x] = 0;
+}
+
 __global__ void reduce_partials(const float* __restrict__ part, int nchunks, size_t n, float* __restrict__ out) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         float s = 0.f;
@@ -801,6 +983,37 @@ int b200moe_router_wgrad(const void* x, const float* dh, const float* dn, int T,
                          float* dw_noise, float* workspace, int32_t* tickets, cudaStream_t stream) {
     B200_CHECK_ARG(T >= 1 && E >= 1 && E <= 32, B200MOE_ERR_CONFIG, "bad T/E (%d, %d)", T, E);
     B200_CHECK_ARG(H % 4 == 0, B200MOE_ERR_SHAPE, "hidden must be a multiple of 4");
+#ifndef B200_RWGRAD_TC
+#define B200_RWGRAD_TC 1
+#endif
+    // tensor-core path: E <= 8, whole 128-hidden blocks, partials within the workspace bound
+    const int nch = ceil_div(T, kRwTok);
+    if (B200_RWGRAD_TC && tickets && E <= 8 && H % 128 == 0 &&
+        (size_t)nch * (dn ? 2 : 1) * H * E <= (size_t)ceil_div(T, 64) * H * E) {
+        CUtensorMap xmap;
+        const int rc = make_tmap_bf16_2d(&xmap, x, (uint64_t)H, (uint64_t)T, (uint64_t)H, 64, 64, true);
+        if (rc) return rc;
+        dim3 grid(H / 128, nch);
+        if (dn) {
+            auto kern = router_wgrad_tc_kernel<true>;
+            static std::atomic<uint64_t> attr{0};
+            if (cudaError_t ae = ensure_smem_attr(kern, kRwSmem, attr); ae != cudaSuccess) {
+                set_error("router_wgrad_tc smem attribute: %s", cudaGetErrorString(ae));
+                return B200MOE_ERR_CUDA;
+            }
+            kern<<<grid, 128, kRwSmem, stream>>>(xmap, dh, dn, T, H, E, workspace, dw_g, dw_noise, tickets);
+        } else {
+            auto kern = router_wgrad_tc_kernel<false>;
+            static std::atomic<uint64_t> attr{0};
+            if (cudaError_t ae = ensure_smem_attr(kern, kRwSmem, attr); ae != cudaSuccess) {
+                set_error("router_wgrad_tc smem attribute: %s", cudaGetErrorString(ae));
+                return B200MOE_ERR_CUDA;
+            }
+            kern<<<grid, 128, kRwSmem, stream>>>(xmap, dh, nullptr, T, H, E, workspace, dw_g, nullptr, tickets);
+        }
+        B200_CHECK_LAUNCH("router_wgrad");
+        return B200MOE_OK;
+    }
 #define CALL(EP, D, O) wgrad_impl<EP>(x, D, T, H, E, O, workspace, stream, tickets)
     int rc;
     if (E <= 4) rc = CALL(4, dh, dw_g);

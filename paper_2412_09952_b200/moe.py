@@ -316,7 +316,7 @@ def _wgrad_tickets(device, H: int) -> torch.Tensor:
     once; each launch leaves them zeroed), one buffer per (device, stream)."""
     key = ("wg_tickets", device, torch.cuda.current_stream(device).cuda_stream)
     t = _CACHE.get(key)
-    n = (H + 255) // 256
+    n = (H + 127) // 128          # one per 128-hidden block (tensor-core kernel; the ring kernel uses half)
     if t is None or t.numel() < n:
         t = torch.zeros(n, dtype=torch.int32, device=device)
         _CACHE[key] = t
