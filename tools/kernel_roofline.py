@@ -32,6 +32,7 @@ ALG = {  # algorithmic bytes per launch (bf16 activations, fp32 [T, E] routing t
     "combine_bwd_kernel": T * H * BF + 2 * S * H * BF + T * E * 4,
     "router_dx_kernel": S * H * BF + T * H * BF + 5 * T * E * 4,   # dxp rows, dx; dg, gates, slots in, dh out
     "router_wgrad_ring": T * H * BF + T * E * 4,
+    "router_wgrad_tc_kernel": T * H * BF + T * E * 4,
     "router_dh_kernel": 4 * T * E * 4,
 }
 
