@@ -135,6 +135,33 @@ combine_kernel(Rows o, const float* __restrict__ gates, const int32_t* __restric
     for (int r = 0; r < n; ++r) g[r] = gates[(size_t)t * E + experts[r]];
     const int nvec = H / 8;
     uint4* dst = reinterpret_cast<uint4*>(y + (size_t)t * H);
+    if (n <= 1) {   // zero or one kept slot: y = 0 or g * o, the row's loads all in flight
+        const uint4* s0 = n ? reinterpret_cast<const uint4*>(o.base<kPeer>(experts[0]) + (size_t)rows[0] * H) : nullptr;
+        uint4* m0 = (og && n) ? reinterpret_cast<uint4*>(og + (size_t)t * og_k * H) : nullptr;
+        const float g0 = n ? g[0] : 0.f;
+        for (int base = 0; base < nvec; base += 32 * 8) {
+            uint4 v0[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int j = base + i * 32 + lane;
+                v0[i] = make_uint4(0, 0, 0, 0);
+                if (n && j < nvec) v0[i] = kPeer ? s0[j] : ld_nc_v4(s0 + j);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int j = base + i * 32 + lane;
+                if (j < nvec) {
+                    if (m0) m0[j] = v0[i];
+                    float f0[8], a[8];
+                    unpack8(v0[i], f0);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) a[c] = n ? fmaf(g0, f0[c], 0.f) : 0.f;
+                    dst[j] = pack8(a);
+                }
+            }
+        }
+        return;
+    }
     if (n == 2) {
         // top-2 tokens (the common case): both expert rows' loads are issued
         // before any arithmetic, 8 x 16 B in flight per lane -- over NVLink the
@@ -242,6 +269,51 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, Rows o, const float* __
     }
     const int nvec = H / 8;
     const uint4* src = reinterpret_cast<const uint4*>(dy + (size_t)t * H);
+    if (n <= 1) {
+        // a token with no kept slot only zeroes its dg row (its dy is not read);
+        // one kept slot: dy and the expert row's loads in flight together
+        float* dgt = dg + (size_t)t * E;
+        if (lane < E) dgt[lane] = 0.f;
+        __syncwarp();
+        if (n == 0) return;
+        const bool mir = og != nullptr;
+        const uint4* os0 = mir ? reinterpret_cast<const uint4*>(og + (size_t)t * og_k * H)
+                               : reinterpret_cast<const uint4*>(o.base<kPeer>(experts[0]) + (size_t)rows[0] * H);
+        uint4* ds0 = reinterpret_cast<uint4*>(dout.base<kPeer>(experts[0]) + (size_t)rows[0] * H);
+        const float g0 = g[0];
+        float s0 = 0.f;
+        for (int base = 0; base < nvec; base += 32 * 4) {
+            uint4 dv[4], v0[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = base + i * 32 + lane;
+                if (j < nvec) {
+                    dv[i] = ld_nc_v4(src + j);
+                    v0[i] = (kPeer && !mir) ? os0[j] : ld_nc_v4(os0 + j);
+                }
+            }
+            float p0 = 0.f;   // the general path's per-chunk fma chain (bit-identical dg)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = base + i * 32 + lane;
+                if (j < nvec) {
+                    float d[8], f[8], w[8];
+                    unpack8(dv[i], d);
+                    unpack8(v0[i], f);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        p0 = fmaf(d[c], f[c], p0);
+                        w[c] = g0 * d[c];
+                    }
+                    ds0[j] = pack8(w);
+                }
+            }
+            s0 += p0;
+        }
+        const float a0 = warp_sum(s0);
+        if (lane == 0) dgt[experts[0]] = a0;
+        return;
+    }
     if (n == 2) {
         // top-2 tokens: dy and both expert rows' loads in flight together
         // (12 x 16 B per lane) before the dot products and the two stores
