@@ -776,7 +776,10 @@ __global__ void importance_loss_kernel_fwd(const float* __restrict__ imp, int E,
 // Workspace (int32 words, zero-initialised once): [0] ticket, [1] tile counter,
 // [2] epoch, [8..8+40) per-expert slot totals, then status words (uint64,
 // [tile][EP]) and per-tile partial sums (float2, [tile][EP]).
-constexpr int kScanTile = 256;
+#ifndef B200_SCAN_TILE
+#define B200_SCAN_TILE 256
+#endif
+constexpr int kScanTile = B200_SCAN_TILE;
 constexpr int kWsStatus = 64;   // int32 offset of the status words (8-byte aligned)
 
 __host__ __device__ constexpr size_t dispatch_ws_words(int T) {
