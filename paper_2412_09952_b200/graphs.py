@@ -19,6 +19,9 @@ Rules for a captured step (the same as for any CUDA graph):
     experts inside the graph on every replay, so in-place weight updates
     between replays are seen (the eager path caches the stack by version);
   * routing statistics read after a replay describe the last replayed step;
+  * a replay writes its gradients into the tensors `.grad` held when the
+    capture ended; an eager step afterwards rebinds `.grad` to new tensors,
+    so code that mixes the two keeps references to the captured ones;
   * no output of an earlier eager step may still be alive at capture time:
     its autograd graph keeps the parameters' gradient accumulators bound to
     the stream they were created on (the default stream), which a capture
